@@ -1,0 +1,976 @@
+// C ABI of the B200-native time-stepping core (include/tpflow_b200.h).
+//
+// A tp_ctx is the device-resident counterpart of one tpflow::Simulator
+// (/root/reference/proj/include/tpflow/solver.hpp:26-98): it owns two FP64 SoA
+// state buffers (A = u^n / u^{n+1}, B = u*), the 14 geometry fields, the device
+// step scalars and the per-tile boundary tallies, and drives the kernels of
+// tp_kernels.cu on one CUDA stream.  tp_steps runs Simulator::run's loop body
+// (solver.cpp:637-649) entirely on the device, replayed from a CUDA graph; the
+// host synchronises once per graph (graph_steps steps).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstddef>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/tpflow_b200.h"
+#include "tp_host.hpp"
+#include "tp_types.h"
+
+namespace tpb {
+size_t stage_smem_bytes();
+cudaError_t launch_stage(const StageArgs& a, bool fastdiv, bool corr, cudaStream_t st);
+cudaError_t launch_bc(const BcArgs& a, cudaStream_t st);
+cudaError_t launch_ghost_copy(const GridDesc& g, const double* src, double* dst, cudaStream_t st);
+cudaError_t launch_lambda(const GridDesc& g, const Phys& P, const double* s, const double* geo,
+                          DevScalars* sc, bool fastdiv, cudaStream_t st);
+cudaError_t launch_dt(const Phys& P, DevScalars* sc, int loop, cudaStream_t st);
+cudaError_t launch_post(const PostArgs& a, cudaStream_t st);
+cudaError_t launch_regularize(const GridDesc& g, const Phys& P, double* s, const double* geo,
+                              DevScalars* sc, bool fastdiv, cudaStream_t st);
+cudaError_t init_kernels();
+cudaError_t selftest_division(long long n, unsigned long long seed, unsigned long long* mismatches);
+}  // namespace tpb
+
+using tpb::DevScalars;
+using tpb::host::kGhost;
+
+namespace {
+
+struct ConfigErr { std::string msg; };
+struct NumErr { std::string msg; };
+struct CudaErr { std::string msg; };
+
+inline void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw CudaErr{std::string(what) + ": " + cudaGetErrorString(e)};
+}
+
+constexpr size_t kCtrlBytes = offsetof(DevScalars, lam_bits);
+
+}  // namespace
+
+struct tp_ctx {
+    std::string err;
+    tp_params p{};
+    int device = 0;
+    // grid
+    int ncols = 0, nrows_g = 0;      // interior dims of the whole DEM
+    int row0 = 0, row1 = 0, nrows = 0;  // owned interior rows [row0, row1)
+    int nx = 0, ny = 0, pitch = 0;
+    long long fs = 0;
+    double dxi = 0, deta = 0;
+    tpb::GridDesc g{};
+    tpb::Phys ph{};
+    std::vector<double> geo_h;  // 14 * nx * ny (dense, local rows)
+    tpb::host::Dem dem;
+    // device
+    double* dA = nullptr;
+    double* dB = nullptr;
+    double* dGeo = nullptr;
+    DevScalars* dSc = nullptr;
+    double* dTallyP = nullptr;
+    double* dTallyC = nullptr;
+    signed char* dSide = nullptr;
+    double* dSamples = nullptr;
+    double* dDts = nullptr;
+    long dts_cap = 0;
+    int ntx = 0, nty = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    // options / flags
+    bool fastdiv = true;
+    int graph_steps = 16;
+    bool lam_valid = false;
+    bool ghosts_in_B = false;
+    bool inflow_active = false;
+    int n_samples = 0;
+    bool hydro_set = false;
+    int adv_only = 0;
+    cudaGraphExec_t graphK = nullptr, graph1 = nullptr;
+    int graphK_steps = 0;
+    long launches = 0;
+    double t_next_last = 0.0;
+};
+
+namespace {
+
+tpb::Inflow inflow_desc(const tp_ctx* c) {
+    tpb::Inflow in{};
+    in.n_samples = c->n_samples;
+    in.samples = c->dSamples;
+    in.ghost_side = c->dSide;
+    in.t_unit = std::sqrt(c->p.L / c->p.g);
+    in.H = c->p.H;
+    in.v_unit = std::sqrt(c->p.g * c->p.L);
+    in.active = c->inflow_active ? 1 : 0;
+    return in;
+}
+
+void validate_params(const tp_params* p) {
+    // ModelParams::validate (params.hpp:40-50), ScalingConfig::validate (:21-25),
+    // SimConfig::validate numerics (config.hpp:31-40) — same order and messages.
+    if (!(p->delta_b >= 0.0 && p->delta_b < 90.0))
+        throw ConfigErr{"params: delta_b must be in [0, 90) degrees"};
+    if (!(p->C_d >= 0.0)) throw ConfigErr{"params: C_d must be >= 0"};
+    if (!(p->N_R > 0.0)) throw ConfigErr{"params: N_R must be > 0"};
+    if (!(p->theta_b >= 0.0)) throw ConfigErr{"params: theta_b must be >= 0"};
+    if (!(p->phi_s0 >= 0.0 && p->phi_s0 <= 1.0)) throw ConfigErr{"params: phi_s0 must be in [0, 1]"};
+    if (!(p->alpha_rho > 0.0 && p->alpha_rho <= 1.0))
+        throw ConfigErr{"params: alpha_rho must be in (0, 1]"};
+    if (!(p->L > 0.0)) throw ConfigErr{"scaling: L must be > 0"};
+    if (!(p->H > 0.0)) throw ConfigErr{"scaling: H must be > 0"};
+    if (!(p->g > 0.0)) throw ConfigErr{"scaling: g must be > 0"};
+    if (!(p->cfl > 0.0 && p->cfl <= 0.125))
+        throw ConfigErr{"config: cfl must be in (0, 0.125], got " + std::to_string(p->cfl)};
+    if (!(p->t_end > 0.0)) throw ConfigErr{"config: t_end must be > 0"};
+    if (!(p->dt_out > 0.0)) throw ConfigErr{"config: dt_out must be > 0"};
+    if (!(p->h_dry > 0.0)) throw ConfigErr{"config: h_dry must be > 0"};
+    if (!(p->eps_h > 0.0)) throw ConfigErr{"config: eps_h must be > 0"};
+}
+
+void build_phys(tp_ctx* c) {
+    const tp_params& p = c->p;
+    tpb::Phys& P = c->ph;
+    P.eps = p.H / p.L;  // ScalingConfig::epsilon
+    P.alpha = p.alpha_rho;
+    P.oma = 1.0 - p.alpha_rho;
+    P.C_d = p.C_d;
+    P.N_R = p.N_R;
+    P.theta_b = p.theta_b;
+    P.eps_chi = std::pow(P.eps, p.chi);                  // physics.hpp:60
+    P.tan_d = std::tan(p.delta_b * M_PI / 180.0);        // params.hpp:38
+    P.neg_eps_alpha = -P.eps * p.alpha_rho;              // physics.hpp:147
+    P.eps_NR = P.eps * p.N_R;                            // physics.hpp:115
+    P.h_dry = p.h_dry;
+    P.eps_h = p.eps_h;
+    P.dxi = c->dxi;
+    P.deta = c->deta;
+    P.two_dxi = 2.0 * c->dxi;
+    P.two_deta = 2.0 * c->deta;
+    P.cell_area = c->dxi * c->deta;
+    P.cfl = p.cfl;
+    P.r_dxi = 1.0 / P.dxi;
+    P.r_deta = 1.0 / P.deta;
+    P.r_two_dxi = 1.0 / P.two_dxi;
+    P.r_two_deta = 1.0 / P.two_deta;
+    P.r_eps_NR = 1.0 / P.eps_NR;
+    P.r_NR = 1.0 / P.N_R;
+    P.adv_only = c->adv_only;
+    P.cap_on = !(c->adv_only || P.tan_d == 0.0) ? 1 : 0;  // solver.cpp:454
+}
+
+void drop_graphs(tp_ctx* c) {
+    if (c->graphK) cudaGraphExecDestroy(c->graphK);
+    if (c->graph1) cudaGraphExecDestroy(c->graph1);
+    c->graphK = c->graph1 = nullptr;
+}
+
+tpb::StageArgs stage_args(tp_ctx* c, bool corr, int loop) {
+    tpb::StageArgs a{};
+    a.g = c->g;
+    a.ph = c->ph;
+    a.s = corr ? c->dB : c->dA;
+    a.u0 = c->dA;
+    a.out = corr ? c->dA : c->dB;
+    a.geo = c->dGeo;
+    a.sc = c->dSc;
+    a.tally = corr ? c->dTallyC : c->dTallyP;
+    a.ntx = c->ntx;
+    a.nty = c->nty;
+    a.loop = loop;
+    a.use_sc_dt = 1;
+    return a;
+}
+
+void launch_bc(tp_ctx* c, int buf, int tsrc, double t, int loop) {
+    tpb::BcArgs b{};
+    b.g = c->g;
+    b.s = buf ? c->dB : c->dA;
+    b.geo = c->dGeo;
+    b.inflow = inflow_desc(c);
+    b.sc = c->dSc;
+    b.t = t;
+    b.tsrc = tsrc;
+    b.loop = loop;
+    ck(tpb::launch_bc(b, c->stream), "bc_kernel");
+}
+
+void launch_post(tp_ctx* c, int loop) {
+    tpb::PostArgs a{};
+    a.sc = c->dSc;
+    a.tally_pred = c->dTallyP;
+    a.tally_corr = c->dTallyC;
+    a.ntx = c->ntx;
+    a.nty = c->nty;
+    a.loop = loop;
+    ck(tpb::launch_post(a, c->stream), "post_kernel");
+}
+
+// one whole step of the device loop: 6 kernels
+void enqueue_loop_step(tp_ctx* c) {
+    launch_bc(c, 0, 1, 0.0, 1);                                     // apply_boundaries(u, t)
+    ck(tpb::launch_dt(c->ph, c->dSc, 1, c->stream), "dt_kernel");   // compute_dt
+    ck(tpb::launch_stage(stage_args(c, false, 1), c->fastdiv, false, c->stream), "predictor");
+    launch_bc(c, 1, 2, 0.0, 1);                                     // apply_boundaries(u*, t+dt)
+    ck(tpb::launch_stage(stage_args(c, true, 1), c->fastdiv, true, c->stream), "corrector");
+    launch_post(c, 1);                                              // t += dt, audit, stop flag
+}
+
+cudaGraphExec_t capture_steps(tp_ctx* c, int k) {
+    cudaGraph_t graph = nullptr;
+    ck(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal), "begin capture");
+    try {
+        for (int s = 0; s < k; ++s) enqueue_loop_step(c);
+    } catch (...) {
+        cudaStreamEndCapture(c->stream, &graph);
+        if (graph) cudaGraphDestroy(graph);
+        throw;
+    }
+    ck(cudaStreamEndCapture(c->stream, &graph), "end capture");
+    cudaGraphExec_t exec = nullptr;
+    ck(cudaGraphInstantiate(&exec, graph, 0), "graph instantiate");
+    cudaGraphDestroy(graph);
+    return exec;
+}
+
+void write_ctrl(tp_ctx* c, double t, double t_next, double t_end, double dt, long long max_steps) {
+    DevScalars h{};
+    h.t = t;
+    h.t_next = t_next;
+    h.t_end = t_end;
+    h.dt = dt;
+    h.steps = 0;
+    h.max_steps = max_steps;
+    h.done = 0;
+    h.hit = 0;
+    ck(cudaMemcpyAsync(c->dSc, &h, kCtrlBytes, cudaMemcpyHostToDevice, c->stream), "ctrl H2D");
+}
+
+DevScalars read_scalars(tp_ctx* c) {
+    DevScalars h{};
+    ck(cudaMemcpyAsync(&h, c->dSc, sizeof(DevScalars), cudaMemcpyDeviceToHost, c->stream), "scalars D2H");
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    return h;
+}
+
+void fresh_lambda(tp_ctx* c) {
+    ck(cudaMemsetAsync(&c->dSc->lam_bits, 0, sizeof(unsigned long long), c->stream), "memset");
+    ck(tpb::launch_lambda(c->g, c->ph, c->dA, c->dGeo, c->dSc, c->fastdiv, c->stream), "lambda_kernel");
+    ck(cudaMemcpyAsync(&c->dSc->lam_cur, &c->dSc->lam_bits, sizeof(unsigned long long),
+                       cudaMemcpyDeviceToDevice, c->stream),
+       "lam copy");
+    c->lam_valid = true;
+}
+
+double read_cell(tp_ctx* c, const double* buf, int field, int X, int Y) {
+    double v = 0.0;
+    ck(cudaMemcpy(&v, buf + field * c->fs + static_cast<long long>(Y) * c->pitch + X, sizeof(double),
+                  cudaMemcpyDeviceToHost),
+       "cell D2H");
+    return v;
+}
+
+// Turn a device error key into the reference's NumericsError text and clear it.
+// pred_buf: buffer the class-0 (regularize) errors refer to.
+void raise_error_key(tp_ctx* c, unsigned long long key, const double* pred_buf) {
+    unsigned long long none = tpb::kNoError;
+    ck(cudaMemcpy(&c->dSc->err_key, &none, sizeof(none), cudaMemcpyHostToDevice), "err reset");
+    const unsigned cls = static_cast<unsigned>(key >> 62);
+    if (cls <= 1) {
+        const int Y = static_cast<int>((key >> 32) & 0x3fffffffull);
+        const int X = static_cast<int>((key >> 1) & 0x7fffffffull);
+        const int p = static_cast<int>(key & 1ull);
+        const double* buf = cls == 0 ? pred_buf : c->dA;
+        const double w = read_cell(c, buf, p, X, Y);
+        const double jb = c->geo_h[3ull * c->nx * c->ny + static_cast<size_t>(Y) * c->nx + X];
+        const double hp = w / jb;
+        throw NumErr{std::string("negative ") + (p == 0 ? "solid" : "fluid") + " thickness " +
+                     tpb::host::to_string_f(hp) + " at cell (" + std::to_string(X - kGhost) + ", " +
+                     std::to_string(Y - kGhost + c->row0) + ")"};
+    }
+    static const char* names[6] = {"ws", "wf", "qsx", "qsy", "qfx", "qfy"};
+    const int f = static_cast<int>((key >> 56) & 0x3full);
+    const int Y = static_cast<int>((key >> 28) & 0xfffffffull);
+    const int X = static_cast<int>(key & 0xfffffffull);
+    throw NumErr{std::string("non-finite value in field '") + names[f] + "' at cell (" +
+                 std::to_string(X - kGhost) + ", " + std::to_string(Y - kGhost + c->row0) +
+                 ") during advance_step"};
+}
+
+void check_error(tp_ctx* c, const double* pred_buf) {
+    unsigned long long key = 0;
+    ck(cudaMemcpyAsync(&key, &c->dSc->err_key, sizeof(key), cudaMemcpyDeviceToHost, c->stream), "err D2H");
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    if (key != tpb::kNoError) raise_error_key(c, key, pred_buf);
+}
+
+// host dense (nx*ny per field) <-> device pitched
+void upload_state(tp_ctx* c, double* dst, const double* src) {
+    ck(cudaMemcpy2DAsync(dst, c->pitch * sizeof(double), src, c->nx * sizeof(double),
+                         c->nx * sizeof(double), 6ull * c->ny, cudaMemcpyHostToDevice, c->stream),
+       "state H2D");
+}
+void download_state(tp_ctx* c, double* dst, const double* src) {
+    ck(cudaMemcpy2DAsync(dst, c->nx * sizeof(double), src, c->pitch * sizeof(double),
+                         c->nx * sizeof(double), 6ull * c->ny, cudaMemcpyDeviceToHost, c->stream),
+       "state D2H");
+    ck(cudaStreamSynchronize(c->stream), "sync");
+}
+
+void sync_ghosts(tp_ctx* c) {
+    if (c->ghosts_in_B) {
+        ck(tpb::launch_ghost_copy(c->g, c->dB, c->dA, c->stream), "ghost copy");
+        c->ghosts_in_B = false;
+    }
+}
+
+std::vector<double> host_state(tp_ctx* c) {
+    sync_ghosts(c);
+    std::vector<double> s(6ull * c->nx * c->ny);
+    download_state(c, s.data(), c->dA);
+    return s;
+}
+
+void set_host_state(tp_ctx* c, const std::vector<double>& s) {
+    upload_state(c, c->dA, s.data());
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    c->lam_valid = false;
+    c->ghosts_in_B = false;
+}
+
+int fail(tp_ctx* c, int code, const std::string& msg) {
+    if (c) c->err = msg;
+    return code;
+}
+
+#define TP_GUARD(c, ...)                                          \
+    try {                                                         \
+        if (c) cudaSetDevice((c)->device);                        \
+        __VA_ARGS__;                                              \
+        return TP_OK;                                             \
+    } catch (const ConfigErr& e) {                                \
+        return fail(c, TP_ERR_CONFIG, e.msg);                     \
+    } catch (const NumErr& e) {                                   \
+        return fail(c, TP_ERR_NUMERICS, e.msg);                   \
+    } catch (const CudaErr& e) {                                  \
+        return fail(c, TP_ERR_CUDA, e.msg);                       \
+    } catch (const std::exception& e) {                           \
+        return fail(c, TP_ERR_INTERNAL, e.what());                \
+    }
+
+void create_impl(tp_ctx* c, const tp_params* p, const tp_dem* dem, int row0, int row1) {
+    validate_params(p);
+    if (!dem || dem->ncols < 2 || dem->nrows < 2)
+        throw ConfigErr{"grid must be at least 2x2"};
+    if (!(dem->cellsize > 0.0)) throw ConfigErr{"cellsize must be positive"};
+    if (row0 < 0 || row1 > dem->nrows || row1 - row0 < 2)
+        throw ConfigErr{"slab rows out of range (need at least 2 rows)"};
+    c->p = *p;
+    c->device = p->device;
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    ck(tpb::init_kernels(), "init kernels");
+    c->ncols = dem->ncols;
+    c->nrows_g = dem->nrows;
+    c->row0 = row0;
+    c->row1 = row1;
+    c->nrows = row1 - row0;
+    c->dem.ncols = dem->ncols;
+    c->dem.nrows = dem->nrows;
+    c->dem.xll = dem->xll;
+    c->dem.yll = dem->yll;
+    c->dem.cellsize = dem->cellsize;
+    c->dem.z.assign(dem->z, dem->z + static_cast<size_t>(dem->ncols) * dem->nrows);
+
+    // Simulator ctor: geometry of the whole extended DEM (solver.cpp:16), then our rows
+    tpb::host::Geometry G = tpb::host::compute_geometry(tpb::host::extend_grid(c->dem, kGhost), p->L);
+    c->nx = G.nx;
+    c->ny = c->nrows + 2 * kGhost;
+    c->dxi = G.dxi;
+    c->deta = G.deta;
+    c->geo_h.resize(14ull * c->nx * c->ny);
+    for (int k = 0; k < 14; ++k)
+        std::memcpy(c->geo_h.data() + static_cast<size_t>(k) * c->nx * c->ny,
+                    G.field(k) + static_cast<size_t>(row0) * G.nx,
+                    sizeof(double) * static_cast<size_t>(c->nx) * c->ny);
+
+    c->pitch = (c->nx + 7) & ~7;
+    c->fs = static_cast<long long>(c->pitch) * c->ny;
+    c->g.nx = c->nx;
+    c->g.ny = c->ny;
+    c->g.pitch = c->pitch;
+    c->g.fs = c->fs;
+    c->g.has_south = row0 == 0 ? 1 : 0;
+    c->g.has_north = row1 == dem->nrows ? 1 : 0;
+    build_phys(c);
+
+    c->ntx = (c->ncols + tpb::TX - 1) / tpb::TX;
+    c->nty = (c->nrows + tpb::TY - 1) / tpb::TY;
+
+    const size_t sbytes = sizeof(double) * 6ull * c->fs;
+    ck(cudaMalloc(&c->dA, sbytes), "cudaMalloc state A");
+    ck(cudaMalloc(&c->dB, sbytes), "cudaMalloc state B");
+    ck(cudaMalloc(&c->dGeo, sizeof(double) * 14ull * c->fs), "cudaMalloc geometry");
+    ck(cudaMalloc(&c->dSc, sizeof(DevScalars)), "cudaMalloc scalars");
+    const size_t tb = sizeof(double) * 4ull * c->ntx * c->nty;
+    ck(cudaMalloc(&c->dTallyP, tb), "cudaMalloc tally");
+    ck(cudaMalloc(&c->dTallyC, tb), "cudaMalloc tally");
+    ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
+    c->own_stream = true;
+    ck(cudaMemsetAsync(c->dA, 0, sbytes, c->stream), "memset");
+    ck(cudaMemsetAsync(c->dB, 0, sbytes, c->stream), "memset");
+    ck(cudaMemsetAsync(c->dTallyP, 0, tb, c->stream), "memset");
+    ck(cudaMemsetAsync(c->dTallyC, 0, tb, c->stream), "memset");
+    ck(cudaMemsetAsync(c->dGeo, 0, sizeof(double) * 14ull * c->fs, c->stream), "memset");
+    ck(cudaMemcpy2DAsync(c->dGeo, c->pitch * sizeof(double), c->geo_h.data(), c->nx * sizeof(double),
+                         c->nx * sizeof(double), 14ull * c->ny, cudaMemcpyHostToDevice, c->stream),
+       "geometry H2D");
+    DevScalars h{};
+    h.lam_bits = 0;
+    h.lam_cur = 0;
+    h.err_key = tpb::kNoError;
+    h.max_steps = LLONG_MAX;
+    ck(cudaMemcpyAsync(c->dSc, &h, sizeof(h), cudaMemcpyHostToDevice, c->stream), "scalars H2D");
+    ck(cudaStreamSynchronize(c->stream), "sync");
+}
+
+// index of padded local cell (i, j) in the ghost band enumeration of bc_kernel, or -1
+long band_index(const tp_ctx* c, int i, int j) {
+    const int nx = c->nx, ny = c->ny;
+    const long nS = c->g.has_south ? 3L * nx : 0;
+    const long nN = c->g.has_north ? 3L * nx : 0;
+    if (j < 3) return c->g.has_south ? static_cast<long>(j) * nx + i : -1;
+    if (j >= ny - 3) return c->g.has_north ? nS + static_cast<long>(j - (ny - 3)) * nx + i : -1;
+    const long rows = ny - 6;
+    if (i < 3) return nS + nN + static_cast<long>(j - 3) * 3 + i;
+    if (i >= nx - 3) return nS + nN + 3 * rows + static_cast<long>(j - 3) * 3 + (i - (nx - 3));
+    return -1;
+}
+
+}  // namespace
+
+extern "C" {
+
+int tp_create_slab(const tp_params* p, const tp_dem* dem, int row0, int row1, tp_ctx** out) {
+    tp_ctx* c = new tp_ctx();
+    *out = c;
+    TP_GUARD(c, create_impl(c, p, dem, row0, row1))
+}
+
+int tp_create(const tp_params* p, const tp_dem* dem, tp_ctx** out) {
+    return tp_create_slab(p, dem, 0, dem ? dem->nrows : 0, out);
+}
+
+void tp_destroy(tp_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    drop_graphs(c);
+    cudaFree(c->dA);
+    cudaFree(c->dB);
+    cudaFree(c->dGeo);
+    cudaFree(c->dSc);
+    cudaFree(c->dTallyP);
+    cudaFree(c->dTallyC);
+    cudaFree(c->dSide);
+    cudaFree(c->dSamples);
+    cudaFree(c->dDts);
+    if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+int tp_geometry(const tp_dem* dem, double L, double* out) {
+    try {
+        tpb::host::Dem d;
+        d.ncols = dem->ncols;
+        d.nrows = dem->nrows;
+        d.xll = dem->xll;
+        d.yll = dem->yll;
+        d.cellsize = dem->cellsize;
+        d.z.assign(dem->z, dem->z + static_cast<size_t>(dem->ncols) * dem->nrows);
+        tpb::host::Geometry G = tpb::host::compute_geometry(tpb::host::extend_grid(d, kGhost), L);
+        std::memcpy(out, G.f.data(), sizeof(double) * G.f.size());
+        return TP_OK;
+    } catch (...) {
+        return TP_ERR_INTERNAL;
+    }
+}
+
+const char* tp_last_error(const tp_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+int tp_dims(const tp_ctx* c, int* nx, int* ny, double* dxi, double* deta) {
+    if (!c) return TP_ERR_INTERNAL;
+    *nx = c->nx;
+    *ny = c->ny;
+    *dxi = c->dxi;
+    *deta = c->deta;
+    return TP_OK;
+}
+
+int tp_set_option(tp_ctx* c, const char* key, long value) {
+    TP_GUARD(c, {
+        std::string k(key);
+        if (k == "fastdiv") {
+            c->fastdiv = value != 0;
+            drop_graphs(c);
+        } else if (k == "graph_steps") {
+            if (value < 1 || value > 4096) throw ConfigErr{"graph_steps must be in [1, 4096]"};
+            c->graph_steps = static_cast<int>(value);
+            drop_graphs(c);
+        } else {
+            throw ConfigErr{"unknown option '" + k + "'"};
+        }
+    })
+}
+
+int tp_set_initial_thickness(tp_ctx* c, const double* h_m) {
+    TP_GUARD(c, {
+        // Simulator::set_initial_thickness (solver.cpp:35-57)
+        std::vector<double> s = host_state(c);
+        const double phi = c->p.phi_s0;
+        const size_t n = static_cast<size_t>(c->nx) * c->ny;
+        const double* jbf = c->geo_h.data() + 3 * n;
+        for (int j = 0; j < c->nrows_g; ++j) {
+            for (int i = 0; i < c->ncols; ++i) {
+                double h = h_m[static_cast<size_t>(j) * c->ncols + i];
+                if (h < 0.0)
+                    throw ConfigErr{"initial state: negative thickness at column " + std::to_string(i) +
+                                    ", row " + std::to_string(j)};
+                if (j < c->row0 || j >= c->row1) continue;
+                double h_scaled = h / c->p.H;
+                const size_t k = static_cast<size_t>(j - c->row0 + kGhost) * c->nx + (i + kGhost);
+                double jb = jbf[k];
+                s[0 * n + k] = jb * h_scaled * phi;
+                s[1 * n + k] = jb * h_scaled * (1.0 - phi);
+                s[2 * n + k] = 0.0;
+                s[3 * n + k] = 0.0;
+                s[4 * n + k] = 0.0;
+                s[5 * n + k] = 0.0;
+            }
+        }
+        set_host_state(c, s);
+    })
+}
+
+int tp_set_initial_velocity(tp_ctx* c, const double* vx, const double* vy) {
+    TP_GUARD(c, {
+        // Simulator::set_initial_velocity (solver.cpp:59-76)
+        std::vector<double> s = host_state(c);
+        const size_t n = static_cast<size_t>(c->nx) * c->ny;
+        const double* jbf = c->geo_h.data() + 3 * n;
+        const double vu = std::sqrt(c->p.g * c->p.L);
+        for (int j = c->row0; j < c->row1; ++j) {
+            for (int i = 0; i < c->ncols; ++i) {
+                const size_t k = static_cast<size_t>(j - c->row0 + kGhost) * c->nx + (i + kGhost);
+                double jb = jbf[k];
+                double hs = s[0 * n + k] / jb;
+                double hf = s[1 * n + k] / jb;
+                const size_t q = static_cast<size_t>(j) * c->ncols + i;
+                double ux = vx[q] / vu, uy = vy[q] / vu;
+                s[2 * n + k] = jb * hs * ux;
+                s[3 * n + k] = jb * hs * uy;
+                s[4 * n + k] = jb * hf * ux;
+                s[5 * n + k] = jb * hf * uy;
+            }
+        }
+        set_host_state(c, s);
+    })
+}
+
+int tp_set_hydrograph(tp_ctx* c, int n_cells, const int* ci, const int* cj, const char* side,
+                      int n_samples, const double* t, const double* h, const double* phi_s,
+                      const double* speed) {
+    TP_GUARD(c, {
+        // Hydrograph::validate (hydrograph.hpp:49-77), same messages
+        for (int k = 1; k < n_samples; ++k)
+            if (!(t[k] > t[k - 1]))
+                throw ConfigErr{"hydrograph: sample times must be strictly increasing (t=" +
+                                std::to_string(t[k]) + " after t=" + std::to_string(t[k - 1]) + ")"};
+        for (int k = 0; k < n_samples; ++k) {
+            if (h[k] < 0.0) throw ConfigErr{"hydrograph: negative thickness"};
+            if (speed[k] < 0.0) throw ConfigErr{"hydrograph: negative speed"};
+            if (phi_s[k] < 0.0 || phi_s[k] > 1.0) throw ConfigErr{"hydrograph: phi_s out of [0, 1]"};
+        }
+        for (int k = 0; k < n_cells; ++k) {
+            bool ok = false;
+            switch (side[k]) {
+                case 'N': ok = cj[k] == c->nrows_g - 1; break;
+                case 'S': ok = cj[k] == 0; break;
+                case 'E': ok = ci[k] == c->ncols - 1; break;
+                case 'W': ok = ci[k] == 0; break;
+                default:
+                    throw ConfigErr{std::string("hydrograph: unknown side '") + side[k] + "'"};
+            }
+            if (ci[k] < 0 || ci[k] >= c->ncols || cj[k] < 0 || cj[k] >= c->nrows_g) ok = false;
+            if (!ok)
+                throw ConfigErr{"hydrograph: cell (" + std::to_string(ci[k]) + ", " + std::to_string(cj[k]) +
+                                ") is not on the boundary ring of side " + std::string(1, side[k])};
+        }
+        // ghost-band side map for bc_kernel (apply_boundaries inflow, solver.cpp:108-136)
+        const long nband = (c->g.has_south ? 3L * c->nx : 0) + (c->g.has_north ? 3L * c->nx : 0) +
+                           6L * (c->ny - 6);
+        std::vector<signed char> map(static_cast<size_t>(nband), 0);
+        for (int k = 0; k < n_cells; ++k) {
+            int di = 0, dj = 0;
+            switch (side[k]) {
+                case 'E': di = 1; break;
+                case 'W': di = -1; break;
+                case 'N': dj = 1; break;
+                case 'S': dj = -1; break;
+            }
+            const int pi = ci[k] + kGhost, pj = cj[k] + kGhost;
+            for (int g = 1; g <= kGhost; ++g) {
+                const int gi = pi + di * g;
+                const int gj = pj + dj * g - c->row0;  // local padded row
+                if (gj < 0 || gj >= c->ny) continue;
+                // W/E ghosts of rows we do not own are the neighbours' (halo rows)
+                if (dj == 0 && (gj < kGhost || gj >= c->ny - kGhost)) continue;
+                const long b = band_index(c, gi, gj);
+                if (b >= 0) map[static_cast<size_t>(b)] = static_cast<signed char>(side[k]);
+            }
+        }
+        cudaFree(c->dSide);
+        cudaFree(c->dSamples);
+        c->dSide = nullptr;
+        c->dSamples = nullptr;
+        ck(cudaMalloc(&c->dSide, std::max<size_t>(1, map.size())), "cudaMalloc side map");
+        if (!map.empty())
+            ck(cudaMemcpy(c->dSide, map.data(), map.size(), cudaMemcpyHostToDevice), "side map H2D");
+        std::vector<double> smp(4ull * std::max(1, n_samples), 0.0);
+        for (int k = 0; k < n_samples; ++k) {
+            smp[4 * k + 0] = t[k];
+            smp[4 * k + 1] = h[k];
+            smp[4 * k + 2] = phi_s[k];
+            smp[4 * k + 3] = speed[k];
+        }
+        ck(cudaMalloc(&c->dSamples, sizeof(double) * smp.size()), "cudaMalloc samples");
+        ck(cudaMemcpy(c->dSamples, smp.data(), sizeof(double) * smp.size(), cudaMemcpyHostToDevice),
+           "samples H2D");
+        c->n_samples = n_samples;
+        c->hydro_set = true;
+        c->inflow_active = c->p.mode == 1;  // cfg_.mode == InflowHydrograph && hydro_
+        drop_graphs(c);
+    })
+}
+
+int tp_get_state(tp_ctx* c, double* out) {
+    TP_GUARD(c, {
+        sync_ghosts(c);
+        download_state(c, out, c->dA);
+    })
+}
+
+int tp_set_state(tp_ctx* c, const double* in) {
+    TP_GUARD(c, {
+        upload_state(c, c->dA, in);
+        ck(cudaStreamSynchronize(c->stream), "sync");
+        c->lam_valid = false;
+        c->ghosts_in_B = false;
+    })
+}
+
+int tp_get_geometry(tp_ctx* c, double* out) {
+    TP_GUARD(c, std::memcpy(out, c->geo_h.data(), sizeof(double) * c->geo_h.size()))
+}
+
+int tp_apply_boundaries(tp_ctx* c, double t_scaled) {
+    TP_GUARD(c, {
+        launch_bc(c, 0, 0, t_scaled, 0);
+        ck(cudaStreamSynchronize(c->stream), "sync");
+        c->ghosts_in_B = false;
+    })
+}
+
+int tp_compute_dt(tp_ctx* c, double t_scaled, double t_next_scaled, double* dt) {
+    TP_GUARD(c, {
+        write_ctrl(c, t_scaled, t_next_scaled, INFINITY, 0.0, LLONG_MAX);
+        fresh_lambda(c);
+        ck(tpb::launch_dt(c->ph, c->dSc, 0, c->stream), "dt_kernel");
+        DevScalars h = read_scalars(c);
+        *dt = h.dt;
+    })
+}
+
+int tp_advance_step(tp_ctx* c, double dt_scaled, double t_scaled) {
+    TP_GUARD(c, {
+        // Simulator::advance_step (solver.cpp:496-545)
+        write_ctrl(c, t_scaled, t_scaled, INFINITY, dt_scaled, LLONG_MAX);
+        ck(tpb::launch_stage(stage_args(c, false, 0), c->fastdiv, false, c->stream), "predictor");
+        launch_bc(c, 1, 2, 0.0, 0);
+        ck(tpb::launch_stage(stage_args(c, true, 0), c->fastdiv, true, c->stream), "corrector");
+        launch_post(c, 0);
+        c->lam_valid = false;
+        c->ghosts_in_B = true;
+        check_error(c, c->dB);
+    })
+}
+
+int tp_regularize(tp_ctx* c) {
+    TP_GUARD(c, {
+        sync_ghosts(c);
+        ck(tpb::launch_regularize(c->g, c->ph, c->dA, c->dGeo, c->dSc, c->fastdiv, c->stream),
+           "regularize_kernel");
+        c->lam_valid = false;
+        check_error(c, c->dA);
+    })
+}
+
+int tp_set_advection_only(tp_ctx* c, int on) {
+    TP_GUARD(c, {
+        c->adv_only = on ? 1 : 0;
+        build_phys(c);
+        drop_graphs(c);
+        c->lam_valid = false;
+    })
+}
+
+int tp_steps(tp_ctx* c, double t_next, double t_end, long max_steps, double* t, long* steps, int* hit,
+             double* dts) {
+    TP_GUARD(c, {
+        *steps = 0;
+        *hit = 0;
+        c->launches = 0;
+        if (max_steps <= 0 || !(*t < t_end)) return TP_OK;
+        if (dts && c->dts_cap < max_steps) {
+            cudaFree(c->dDts);
+            c->dDts = nullptr;
+            ck(cudaMalloc(&c->dDts, sizeof(double) * max_steps), "cudaMalloc dts");
+            c->dts_cap = max_steps;
+        }
+        double* dts_dev = dts ? c->dDts : nullptr;
+        ck(cudaMemcpyAsync(&c->dSc->dts, &dts_dev, sizeof(double*), cudaMemcpyHostToDevice, c->stream),
+           "dts ptr");
+        write_ctrl(c, *t, t_next, t_end, 0.0, max_steps);
+        if (!c->lam_valid) {
+            fresh_lambda(c);
+            c->launches += 1;
+        }
+        if (!c->graphK || c->graphK_steps != c->graph_steps) {
+            drop_graphs(c);
+            c->graphK = capture_steps(c, c->graph_steps);
+            c->graph1 = capture_steps(c, 1);
+            c->graphK_steps = c->graph_steps;
+        }
+        long long done_steps = 0;
+        DevScalars h{};
+        for (;;) {
+            const bool big = (max_steps - done_steps) >= c->graph_steps;
+            ck(cudaGraphLaunch(big ? c->graphK : c->graph1, c->stream), "graph launch");
+            c->launches += 6L * (big ? c->graph_steps : 1);
+            h = read_scalars(c);
+            done_steps = h.steps;
+            if (h.done) break;
+        }
+        *steps = static_cast<long>(h.steps);
+        *t = h.t;
+        *hit = h.steps > 0 ? h.hit : 0;
+        c->lam_valid = h.steps > 0 || c->lam_valid;
+        c->ghosts_in_B = c->ghosts_in_B || h.steps > 0;
+        if (dts && h.steps > 0)
+            ck(cudaMemcpy(dts, c->dDts, sizeof(double) * h.steps, cudaMemcpyDeviceToHost), "dts D2H");
+        if (h.err_key != tpb::kNoError) {
+            c->lam_valid = false;
+            raise_error_key(c, h.err_key, c->dB);
+        }
+    })
+}
+
+int tp_get_audit(tp_ctx* c, double* a) {
+    TP_GUARD(c, {
+        DevScalars h = read_scalars(c);
+        std::memcpy(a, h.audit, sizeof(h.audit));
+    })
+}
+
+int tp_set_audit(tp_ctx* c, const double* a) {
+    TP_GUARD(c, {
+        ck(cudaMemcpyAsync(&c->dSc->audit, a, sizeof(double) * 10, cudaMemcpyHostToDevice, c->stream),
+           "audit H2D");
+        ck(cudaStreamSynchronize(c->stream), "sync");
+    })
+}
+
+int tp_interior_mass(tp_ctx* c, double* ms, double* mf) {
+    TP_GUARD(c, {
+        // Simulator::interior_mass (solver.cpp:582-588): KahanSum (field.hpp:46-59) in (j, i) order
+        std::vector<double> w(2ull * c->nx * c->ny);
+        ck(cudaMemcpy2DAsync(w.data(), c->nx * sizeof(double), c->dA, c->pitch * sizeof(double),
+                             c->nx * sizeof(double), 2ull * c->ny, cudaMemcpyDeviceToHost, c->stream),
+           "mass D2H");
+        ck(cudaStreamSynchronize(c->stream), "sync");
+        for (int p = 0; p < 2; ++p) {
+            double sum = 0.0, comp = 0.0;
+            const double* f = w.data() + static_cast<size_t>(p) * c->nx * c->ny;
+            for (int j = kGhost; j < c->ny - kGhost; ++j)
+                for (int i = kGhost; i < c->nx - kGhost; ++i) {
+                    double x = f[static_cast<size_t>(j) * c->nx + i];
+                    double y = x - comp;
+                    double t = sum + y;
+                    comp = (t - sum) - y;
+                    sum = t;
+                }
+            (p == 0 ? *ms : *mf) = sum * c->dxi * c->deta;
+        }
+    })
+}
+
+int tp_snapshot(tp_ctx* c, double* out) {
+    TP_GUARD(c, {
+        // Simulator::snapshot (solver.cpp:590-617)
+        std::vector<double> s = host_state(c);
+        const size_t n = static_cast<size_t>(c->nx) * c->ny;
+        const size_t m = static_cast<size_t>(c->ncols) * c->nrows;
+        const double* jbf = c->geo_h.data() + 3 * n;
+        const double vu = std::sqrt(c->p.g * c->p.L);
+        const double eps_h = c->p.eps_h;
+        std::fill(out, out + 6 * m, 0.0);
+        auto desing = [&](double q, double jb, double hp) {
+            double hm = std::max(hp, eps_h);
+            double denom = hp * hp + hm * hm;
+            return (q / jb) * (2.0 * hp / denom);
+        };
+        for (int j = 0; j < c->nrows; ++j) {
+            for (int i = 0; i < c->ncols; ++i) {
+                const size_t k = static_cast<size_t>(j + kGhost) * c->nx + (i + kGhost);
+                const size_t o = static_cast<size_t>(j) * c->ncols + i;
+                double jb = jbf[k];
+                double hs = s[0 * n + k] / jb;
+                double hf = s[1 * n + k] / jb;
+                double h = hs + hf;
+                out[0 * m + o] = h * c->p.H;
+                if (h < c->p.h_dry) continue;
+                out[1 * m + o] = hs / h;
+                out[2 * m + o] = desing(s[2 * n + k], jb, hs) * vu;
+                out[3 * m + o] = desing(s[3 * n + k], jb, hs) * vu;
+                out[4 * m + o] = desing(s[4 * n + k], jb, hf) * vu;
+                out[5 * m + o] = desing(s[5 * n + k], jb, hf) * vu;
+            }
+        }
+    })
+}
+
+// ---- multi-GPU slab plumbing ----------------------------------------------------
+
+long tp_halo_bytes(const tp_ctx* c) { return 2L * 6L * c->nx * static_cast<long>(sizeof(double)); }
+
+int tp_halo_pack(tp_ctx* c, int buf, int side, void* dst) {
+    TP_GUARD(c, {
+        if (buf == 0) sync_ghosts(c);
+        const double* base = buf ? c->dB : c->dA;
+        const int row = side == 0 ? kGhost : c->ny - kGhost - 2;  // our 2 edge interior rows
+        for (int f = 0; f < 6; ++f)
+            ck(cudaMemcpy2DAsync(static_cast<double*>(dst) + 2L * f * c->nx, c->nx * sizeof(double),
+                                 base + f * c->fs + static_cast<long long>(row) * c->pitch,
+                                 c->pitch * sizeof(double), c->nx * sizeof(double), 2,
+                                 cudaMemcpyDeviceToDevice, c->stream),
+               "halo pack");
+    })
+}
+
+int tp_halo_unpack(tp_ctx* c, int buf, int side, const void* src) {
+    TP_GUARD(c, {
+        double* base = buf ? c->dB : c->dA;
+        const int row = side == 0 ? kGhost - 2 : c->ny - kGhost;  // the 2 halo rows next to the interior
+        for (int f = 0; f < 6; ++f)
+            ck(cudaMemcpy2DAsync(base + f * c->fs + static_cast<long long>(row) * c->pitch,
+                                 c->pitch * sizeof(double),
+                                 static_cast<const double*>(src) + 2L * f * c->nx, c->nx * sizeof(double),
+                                 c->nx * sizeof(double), 2, cudaMemcpyDeviceToDevice, c->stream),
+               "halo unpack");
+    })
+}
+
+int tp_step_begin(tp_ctx* c, double t, double t_next, double t_end) {
+    TP_GUARD(c, {
+        write_ctrl(c, t, t_next, t_end, 0.0, LLONG_MAX);
+        c->t_next_last = t_next;
+        ck(cudaMemsetAsync(&c->dSc->dts, 0, sizeof(double*), c->stream), "dts null");
+    })
+}
+
+int tp_bc(tp_ctx* c, int buf) {
+    TP_GUARD(c, {
+        launch_bc(c, buf ? 1 : 0, buf ? 2 : 1, 0.0, 0);
+        if (!buf) c->ghosts_in_B = false;
+    })
+}
+
+int tp_lambda_local(tp_ctx* c, void* dst) {
+    TP_GUARD(c, {
+        if (!c->lam_valid) {
+            ck(cudaMemsetAsync(&c->dSc->lam_bits, 0, sizeof(unsigned long long), c->stream), "memset");
+            ck(tpb::launch_lambda(c->g, c->ph, c->dA, c->dGeo, c->dSc, c->fastdiv, c->stream),
+               "lambda_kernel");
+        }
+        ck(cudaMemcpyAsync(dst, &c->dSc->lam_bits, sizeof(double), cudaMemcpyDeviceToDevice, c->stream),
+           "lambda export");
+    })
+}
+
+int tp_dt_from(tp_ctx* c, const void* lam) {
+    TP_GUARD(c, {
+        ck(cudaMemcpyAsync(&c->dSc->lam_cur, lam, sizeof(double), cudaMemcpyDeviceToDevice, c->stream),
+           "lambda import");
+        ck(tpb::launch_dt(c->ph, c->dSc, 0, c->stream), "dt_kernel");
+    })
+}
+
+int tp_stage(tp_ctx* c, int corrector) {
+    TP_GUARD(c, {
+        ck(tpb::launch_stage(stage_args(c, corrector != 0, 0), c->fastdiv, corrector != 0, c->stream),
+           corrector ? "corrector" : "predictor");
+        if (corrector) {
+            c->lam_valid = true;  // lam_bits now holds the local lambda of u^{n+1}
+            c->ghosts_in_B = true;
+        }
+    })
+}
+
+int tp_step_end(tp_ctx* c, double* t, int* hit, double* dt) {
+    TP_GUARD(c, {
+        // clear a stale done flag so post_kernel runs its loop bookkeeping
+        int zero = 0;
+        ck(cudaMemcpyAsync(&c->dSc->done, &zero, sizeof(int), cudaMemcpyHostToDevice, c->stream), "done");
+        launch_post(c, 1);
+        DevScalars h = read_scalars(c);
+        *t = h.t;
+        *hit = h.hit;
+        *dt = h.dt;
+        if (h.err_key != tpb::kNoError) {
+            c->lam_valid = false;
+            raise_error_key(c, h.err_key, c->dB);
+        }
+    })
+}
+
+int tp_set_stream(tp_ctx* c, void* s) {
+    TP_GUARD(c, {
+        ck(cudaStreamSynchronize(c->stream), "sync");
+        if (c->own_stream) cudaStreamDestroy(c->stream);
+        c->stream = static_cast<cudaStream_t>(s);
+        c->own_stream = false;
+        drop_graphs(c);
+    })
+}
+
+int tp_synchronize(tp_ctx* c) { TP_GUARD(c, ck(cudaStreamSynchronize(c->stream), "sync")) }
+
+int tp_device_state(tp_ctx* c, int buf, void** ptr, long* pitch, long* field_stride) {
+    if (!c) return TP_ERR_INTERNAL;
+    *ptr = buf ? c->dB : c->dA;
+    *pitch = c->pitch;
+    *field_stride = static_cast<long>(c->fs);
+    return TP_OK;
+}
+
+int tp_selftest_division(int device, long n, unsigned long long seed, unsigned long long* mismatches) {
+    if (cudaSetDevice(device) != cudaSuccess) return TP_ERR_CUDA;
+    return tpb::selftest_division(n, seed, mismatches) == cudaSuccess ? TP_OK : TP_ERR_CUDA;
+}
+
+long tp_kernel_launches(const tp_ctx* c) { return c ? c->launches : 0; }
+
+}  // extern "C"

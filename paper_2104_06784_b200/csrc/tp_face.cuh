@@ -1,0 +1,100 @@
+// One Kurganov–Tadmor central face flux of the six-equation system.
+// Restates Simulator::compute_face_fluxes' `face_flux` lambda
+// (/root/reference/proj/src/solver.cpp:239-316) with physics::directional_flux
+// (physics.hpp:84-95) and physics::desingularized_velocity (physics.hpp:33-37).
+#pragma once
+
+#include "tp_math.cuh"
+
+namespace tpb {
+
+// L[k], R[k]: reconstructed edge states of the 6 fields (ws,wf,qsx,qsy,qfx,qfy)
+// on the left (cell i, +edge) and right (cell i+1, -edge) of the face.
+// XI = true for a xi face (normal X: a_nn = a11, a_nt = a12), false for eta
+// (normal Y: a_nn = a22, a_nt = a21).  out[6] in field order.
+template <bool FD, bool XI>
+__device__ __forceinline__ void face_flux(const double (&L)[6], const double (&R)[6], double jb_l,
+                                          double jb_r, double nZ_l, double nZ_r, double ann_l,
+                                          double ann_r, double ant_l, double ant_r, const Phys& P,
+                                          double (&out)[6]) {
+    // solver.cpp:242-245
+    const double jbf = 0.5 * (jb_l + jb_r);
+    const double cf = 0.5 * (nZ_l + nZ_r);
+    const double ann = 0.5 * (ann_l + ann_r);
+    const double ant = 0.5 * (ant_l + ant_r);
+    const Rcp rj = mkrcp<FD>(jbf);
+
+    // solver.cpp:265-275
+    const double hL0 = dv<FD>(L[0], rj), hL1 = dv<FD>(L[1], rj);
+    const double hR0 = dv<FD>(R[0], rj), hR1 = dv<FD>(R[1], rj);
+    const double htL = hL0 + hL1;
+    const double htR = hR0 + hR1;
+    if (htL < P.h_dry && htR < P.h_dry) {
+#pragma unroll
+        for (int k = 0; k < 6; ++k) out[k] = 0.0;
+        return;
+    }
+
+    // solver.cpp:277-285
+    const double celL = sqrt(P.eps * cf * smax(htL, 0.0));
+    const double celR = sqrt(P.eps * cf * smax(htR, 0.0));
+    // normal / transverse momenta (solver.cpp:259-262)
+    const double qnL0 = XI ? L[2] : L[3], qtL0 = XI ? L[3] : L[2];
+    const double qnR0 = XI ? R[2] : R[3], qtR0 = XI ? R[3] : R[2];
+    const double qnL1 = XI ? L[4] : L[5], qtL1 = XI ? L[5] : L[4];
+    const double qnR1 = XI ? R[4] : R[5], qtR1 = XI ? R[5] : R[4];
+
+    const double vnL0 = dv<FD>(qnL0, rj) * desing_factor<FD>(smax(hL0, 0.0), P.eps_h);
+    const double vnR0 = dv<FD>(qnR0, rj) * desing_factor<FD>(smax(hR0, 0.0), P.eps_h);
+    const double vnL1 = dv<FD>(qnL1, rj) * desing_factor<FD>(smax(hL1, 0.0), P.eps_h);
+    const double vnR1 = dv<FD>(qnR1, rj) * desing_factor<FD>(smax(hR1, 0.0), P.eps_h);
+    double a = 0.0;
+    a = smax(a, smax(fabs(vnL0) + celL, fabs(vnR0) + celR));
+    a = smax(a, smax(fabs(vnL1) + celL, fabs(vnR1) + celR));
+
+    // solver.cpp:288-296
+    double prL0, prR0, prL1, prR1;
+    if (P.adv_only) {
+        prL0 = prR0 = prL1 = prR1 = 0.0;
+    } else {
+        prL0 = cf * P.oma * hL0 * 0.5;
+        prR0 = cf * P.oma * hR0 * 0.5;
+        prL1 = cf * htL * 0.5;
+        prR1 = cf * htR * 0.5;
+    }
+
+    // physics::directional_flux (physics.hpp:84-95) + solver.cpp:298-315
+    const double ejL = P.eps * jbf * htL;
+    const double ejR = P.eps * jbf * htR;
+    const double ha = 0.5 * a;
+    // solid
+    {
+        const double flm = L[0] * vnL0, frm = R[0] * vnR0;
+        const double fln = qnL0 * vnL0 + ejL * ann * prL0;
+        const double frn = qnR0 * vnR0 + ejR * ann * prR0;
+        const double flt = qtL0 * vnL0 + ejL * ant * prL0;
+        const double frt = qtR0 * vnR0 + ejR * ant * prR0;
+        const double mass = 0.5 * (flm + frm) - ha * (R[0] - L[0]);
+        const double momn = 0.5 * (fln + frn) - ha * (qnR0 - qnL0);
+        const double momt = 0.5 * (flt + frt) - ha * (qtR0 - qtL0);
+        out[0] = mass;
+        out[2] = XI ? momn : momt;
+        out[3] = XI ? momt : momn;
+    }
+    // fluid
+    {
+        const double flm = L[1] * vnL1, frm = R[1] * vnR1;
+        const double fln = qnL1 * vnL1 + ejL * ann * prL1;
+        const double frn = qnR1 * vnR1 + ejR * ann * prR1;
+        const double flt = qtL1 * vnL1 + ejL * ant * prL1;
+        const double frt = qtR1 * vnR1 + ejR * ant * prR1;
+        const double mass = 0.5 * (flm + frm) - ha * (R[1] - L[1]);
+        const double momn = 0.5 * (fln + frn) - ha * (qnR1 - qnL1);
+        const double momt = 0.5 * (flt + frt) - ha * (qtR1 - qtL1);
+        out[1] = mass;
+        out[4] = XI ? momn : momt;
+        out[5] = XI ? momt : momn;
+    }
+}
+
+}  // namespace tpb

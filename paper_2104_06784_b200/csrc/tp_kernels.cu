@@ -1,0 +1,801 @@
+// sm_100a kernels of the MoSES_2PDF time-stepping core.
+//
+//   stage_kernel<FD, CORR>  one fused Heun stage over a 16x15 interior tile:
+//       cell fields (solver.cpp:168-208) + xi/eta KT face fluxes (:220-350)
+//       + boundary mass tally (:352-376) + residual (:378-448) + stage update
+//       (:516-519 / :529-532) + Coulomb cap (:450-480) + [corrector: Heun
+//       average (:538-541)] + regularize (:139-166) + [corrector: finiteness
+//       check (:482-494) and the CFL wave-speed bound of the NEW state
+//       (:556-573) reduced to one atomicMax per block].  Every intermediate
+//       (velocities, pjb, viscous brackets, 12 face fluxes, rhs) stays in
+//       shared memory; HBM sees state in, geometry in, state out.
+//   bc_kernel        apply_boundaries (:83-137), O(perimeter)
+//   lambda_kernel    compute_dt's lambda loop + reduce_max (:556-575, parallel.cpp:109-132)
+//   dt_kernel        compute_dt's tail (:576-579) + exact_hit (:641), 1 thread
+//   post_kernel      run-loop bookkeeping (:643-644) + audit folding, 1 block
+//   regularize_kernel, ghost_copy_kernel
+//
+// Error keys (atomicMin, smallest = the error the serial reference throws first):
+//   regularize:   (cls << 62) | (j << 32) | (i << 1) | phase   cls 0 = predictor / standalone,
+//                                                              cls 1 = corrector
+//   check_finite: (2 << 62) | (field << 56) | (j << 28) | i
+#include <cuda_runtime.h>
+
+#include "tp_face.cuh"
+#include "tp_types.h"
+
+namespace tpb {
+
+__device__ __forceinline__ double ldg(const double* p) { return __ldg(p); }
+
+__device__ __forceinline__ void lam_block_max(double lam, DevScalars* sc) {
+    // lam >= 0 (or NaN, which reduce_max ignores: std::max(m, NaN) == m)
+    unsigned long long b = (lam == lam) ? static_cast<unsigned long long>(__double_as_longlong(lam)) : 0ull;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        unsigned long long x = __shfl_xor_sync(0xffffffffu, b, o);
+        b = x > b ? x : b;
+    }
+    __shared__ unsigned long long wmax[NT / 32];
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) wmax[w] = b;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long m = 0;
+        for (int k = 0; k < NT / 32; ++k) m = wmax[k] > m ? wmax[k] : m;
+        if (m) atomicMax(&sc->lam_bits, m);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// The fused stage kernel.
+// ---------------------------------------------------------------------------
+template <bool FD, bool CORR>
+__global__ void __launch_bounds__(NT, 2) stage_kernel(StageArgs A) {
+    extern __shared__ double sm[];
+    double* S = sm;               // [6][H2][W2] state on the radius-2 box
+    double* JB = S + 6 * BOX;     // [H2][W2]    jb
+    double* RJ = JB + BOX;        // [H2][W2]    RN(1/jb) (FASTDIV)
+    double* V = RJ + BOX;         // [4][H2][W2] vxs, vys, vxf, vyf
+    double* PJ = V + 4 * BOX;     // [H2][W2]    jb*h*p_bar_f
+    double* BR = PJ + BOX;        // [3][H2][W2] viscous brackets bx, by, bxy
+    double* FX = BR + 3 * BOX;    // [6][TY][TX+1] xi face fluxes
+    double* FY = FX + 6 * NFX;    // [6][TY+1][TX] eta face fluxes
+
+    DevScalars* sc = A.sc;
+    if (A.loop && *(volatile int*)&sc->done) return;
+
+    const GridDesc& g = A.g;
+    const Phys& P = A.ph;
+    const int nx = g.nx, ny = g.ny, pitch = g.pitch;
+    const long long fs = g.fs;
+    const int X0 = 3 + blockIdx.x * TX;
+    const int Y0 = 3 + blockIdx.y * TY;
+    const int bx0 = X0 - 2, by0 = Y0 - 2;
+    const double* __restrict__ geo = A.geo;
+
+    // ---- Phase 0: stage the state and jb of the radius-2 box ----------------
+    for (int k = threadIdx.x; k < BOX; k += NT) {
+        const int gx = bx0 + k % W2, gy = by0 + k / W2;
+        const bool in = gx < nx && gy < ny;
+        const long long o = static_cast<long long>(gy) * pitch + gx;
+#pragma unroll
+        for (int f = 0; f < 6; ++f) S[f * BOX + k] = in ? A.s[f * fs + o] : 0.0;
+        JB[k] = in ? ldg(geo + G_JB * fs + o) : 1.0;
+    }
+    __syncthreads();
+
+    // ---- Phase 1: xi faces, eta faces, cell fields -----------------------------
+    constexpr int NXP = ((NFX + 31) / 32) * 32;   // face lists padded to warp multiples
+    constexpr int NYP = ((NFY + 31) / 32) * 32;
+    constexpr int N1 = NXP + NYP + BOX;
+    for (int it = threadIdx.x; it < N1; it += NT) {
+        if (it < NXP) {
+            if (it >= NFX) continue;
+            // xi face between box cells (fx+1, by) and (fx+2, by); stored at FX[ty][fx]
+            const int fx = it % (TX + 1), ty = it / (TX + 1);
+            const int by = ty + 2;
+            const int gy = by0 + by, gxl = bx0 + fx + 1;
+            double L[6], R[6];
+#pragma unroll
+            for (int f = 0; f < 6; ++f) {
+                const double* row = S + f * BOX + by * W2 + fx;
+                const double c0 = row[0], c1 = row[1], c2 = row[2], c3 = row[3];
+                L[f] = edge_plus(c0, c1, c2);
+                R[f] = edge_minus(c1, c2, c3);
+            }
+            const bool in = (gxl + 1) < nx && gy < ny;
+            const long long o = static_cast<long long>(gy) * pitch + gxl;
+            const double nZl = in ? ldg(geo + G_NZ * fs + o) : 1.0;
+            const double nZr = in ? ldg(geo + G_NZ * fs + o + 1) : 1.0;
+            const double a11l = in ? ldg(geo + G_A11 * fs + o) : 0.0;
+            const double a11r = in ? ldg(geo + G_A11 * fs + o + 1) : 0.0;
+            const double a12l = in ? ldg(geo + G_A12 * fs + o) : 0.0;
+            const double a12r = in ? ldg(geo + G_A12 * fs + o + 1) : 0.0;
+            double out[6];
+            face_flux<FD, true>(L, R, JB[by * W2 + fx + 1], JB[by * W2 + fx + 2], nZl, nZr, a11l,
+                                a11r, a12l, a12r, P, out);
+#pragma unroll
+            for (int f = 0; f < 6; ++f) FX[f * NFX + ty * (TX + 1) + fx] = out[f];
+        } else if (it < NXP + NYP) {
+            const int jt = it - NXP;
+            if (jt >= NFY) continue;
+            // eta face between box cells (bx, fy+1) and (bx, fy+2); stored at FY[fy][tx]
+            const int tx = jt % TX, fy = jt / TX;
+            const int bx = tx + 2;
+            const int gx = bx0 + bx, gyl = by0 + fy + 1;
+            double L[6], R[6];
+#pragma unroll
+            for (int f = 0; f < 6; ++f) {
+                const double* col = S + f * BOX + fy * W2 + bx;
+                const double c0 = col[0], c1 = col[W2], c2 = col[2 * W2], c3 = col[3 * W2];
+                L[f] = edge_plus(c0, c1, c2);
+                R[f] = edge_minus(c1, c2, c3);
+            }
+            const bool in = gx < nx && (gyl + 1) < ny;
+            const long long o = static_cast<long long>(gyl) * pitch + gx;
+            const double nZl = in ? ldg(geo + G_NZ * fs + o) : 1.0;
+            const double nZr = in ? ldg(geo + G_NZ * fs + o + pitch) : 1.0;
+            const double a22l = in ? ldg(geo + G_A22 * fs + o) : 0.0;
+            const double a22r = in ? ldg(geo + G_A22 * fs + o + pitch) : 0.0;
+            const double a21l = in ? ldg(geo + G_A21 * fs + o) : 0.0;
+            const double a21r = in ? ldg(geo + G_A21 * fs + o + pitch) : 0.0;
+            double out[6];
+            face_flux<FD, false>(L, R, JB[(fy + 1) * W2 + bx], JB[(fy + 2) * W2 + bx], nZl, nZr,
+                                 a22l, a22r, a21l, a21r, P, out);
+#pragma unroll
+            for (int f = 0; f < 6; ++f) FY[f * NFY + fy * TX + tx] = out[f];
+        } else {
+            // cell fields (solver.cpp:172-184) on the box cell k
+            const int k = it - NXP - NYP;
+            const int bx = k % W2, by = k / W2;
+            const double jb = JB[k];
+            const Rcp rj = mkrcp<FD>(jb);
+            if (FD) RJ[k] = rj.r;
+            if (P.adv_only) continue;  // velocities/pjb feed sources and brackets only
+            const double hs = dv<FD>(S[0 * BOX + k], rj);
+            const double hf = dv<FD>(S[1 * BOX + k], rj);
+            const double h = hs + hf;
+            const double fsld = desing_factor<FD>(hs, P.eps_h);
+            const double fflu = desing_factor<FD>(hf, P.eps_h);
+            V[0 * BOX + k] = dv<FD>(S[2 * BOX + k], rj) * fsld;
+            V[1 * BOX + k] = dv<FD>(S[3 * BOX + k], rj) * fsld;
+            V[2 * BOX + k] = dv<FD>(S[4 * BOX + k], rj) * fflu;
+            V[3 * BOX + k] = dv<FD>(S[5 * BOX + k], rj) * fflu;
+            if (bx >= 1 && bx <= TX + 2 && by >= 1 && by <= TY + 2) {
+                const int gx = bx0 + bx, gy = by0 + by;
+                const double nZ = (gx < nx && gy < ny)
+                                      ? ldg(geo + G_NZ * fs + static_cast<long long>(gy) * pitch + gx)
+                                      : 1.0;
+                PJ[k] = jb * h * (nZ * h * 0.5);  // solver.cpp:182
+            }
+        }
+    }
+    __syncthreads();
+
+    // ---- Phase 2: viscous brackets on the cross neighbours of the tile --------
+    const Rcp r2x = mkrcp_const<FD>(P.two_dxi, P.r_two_dxi);
+    const Rcp r2y = mkrcp_const<FD>(P.two_deta, P.r_two_deta);
+    if (!P.adv_only) {
+        constexpr int NB1 = (TX + 2) * TY;  // rows 2..TY+1, cols 1..TX+2
+        constexpr int NB = NB1 + 2 * TX;    // + rows 1 and TY+2, cols 2..TX+1
+        for (int it = threadIdx.x; it < NB; it += NT) {
+            int bx, by;
+            if (it < NB1) {
+                bx = 1 + it % (TX + 2);
+                by = 2 + it / (TX + 2);
+            } else {
+                const int r = it - NB1;
+                bx = 2 + r % TX;
+                by = (r < TX) ? 1 : TY + 2;
+            }
+            const int k = by * W2 + bx;
+            const int gx = bx0 + bx, gy = by0 + by;
+            const bool in = gx < nx && gy < ny;
+            const long long o = static_cast<long long>(gy) * pitch + gx;
+            const double jb = JB[k];
+            const double a11 = in ? ldg(geo + G_A11 * fs + o) : 0.0;
+            const double a12 = in ? ldg(geo + G_A12 * fs + o) : 0.0;
+            const double a21 = in ? ldg(geo + G_A21 * fs + o) : 0.0;
+            const double a22 = in ? ldg(geo + G_A22 * fs + o) : 0.0;
+            Rcp rj;
+            if (FD) rj = mkrcp_const<FD>(jb, RJ[k]); else rj = mkrcp<FD>(jb);
+            // solver.cpp:197-205 + physics::viscous_brackets (physics.hpp:166-174)
+            const double h = dv<FD>(S[0 * BOX + k] + S[1 * BOX + k], rj);
+            const double* vxf = V + 2 * BOX;
+            const double* vyf = V + 3 * BOX;
+            const double gux = dv<FD>(vxf[k + 1] - vxf[k - 1], r2x);
+            const double guy = dv<FD>(vxf[k + W2] - vxf[k - W2], r2y);
+            const double gwx = dv<FD>(vyf[k + 1] - vyf[k - 1], r2x);
+            const double gwy = dv<FD>(vyf[k + W2] - vyf[k - W2], r2y);
+            const double jh = jb * h;
+            BR[0 * BOX + k] = jh * (a11 * gux + a21 * guy);
+            BR[1 * BOX + k] = jh * (a12 * gwx + a22 * gwy);
+            BR[2 * BOX + k] = jh * ((a12 * gux + a22 * guy) + (a11 * gwx + a21 * gwy));
+        }
+    }
+    __syncthreads();
+
+    // ---- Phase 3: residual + update + cap + [average] + regularize + [finite, lambda]
+    const double dt = sc->dt;
+    const Rcp rdx = mkrcp_const<FD>(P.dxi, P.r_dxi);
+    const Rcp rdy = mkrcp_const<FD>(P.deta, P.r_deta);
+    double lam_local = 0.0;
+    for (int k = threadIdx.x; k < TX * TY; k += NT) {
+        const int tx = k % TX, ty = k / TX;
+        const int X = X0 + tx, Y = Y0 + ty;
+        if (X > nx - 4 || Y > ny - 4) continue;
+        const int bk = (ty + 2) * W2 + (tx + 2);
+        const long long o = static_cast<long long>(Y) * pitch + X;
+
+        double rhs[6];
+#pragma unroll
+        for (int f = 0; f < 6; ++f) {
+            const double* fx = FX + f * NFX + ty * (TX + 1) + tx;
+            const double* fy = FY + f * NFY + ty * TX + tx;
+            rhs[f] = dv<FD>(-(fx[1] - fx[0]), rdx) + dv<FD>(-(fy[TX] - fy[0]), rdy);  // :397-398
+        }
+
+        const double jb = JB[bk];
+        Rcp rj;
+        if (FD) rj = mkrcp_const<FD>(jb, RJ[bk]); else rj = mkrcp<FD>(jb);
+        double nX = 0, nY = 0, nZ = 1, a11 = 0, a12 = 0, a21 = 0, a22 = 0;
+        double dXx = 0, dYx = 0, dZx = 0, dXy = 0, dYy = 0, dZy = 0;
+        if (!P.adv_only || P.cap_on || CORR) nZ = ldg(geo + G_NZ * fs + o);
+        if (!P.adv_only || P.cap_on) {
+            nX = ldg(geo + G_NX * fs + o);
+            nY = ldg(geo + G_NY * fs + o);
+            dXx = ldg(geo + G_DNX_DXI * fs + o);
+            dYx = ldg(geo + G_DNY_DXI * fs + o);
+            dZx = ldg(geo + G_DNZ_DXI * fs + o);
+            dXy = ldg(geo + G_DNX_DETA * fs + o);
+            dYy = ldg(geo + G_DNY_DETA * fs + o);
+            dZy = ldg(geo + G_DNZ_DETA * fs + o);
+        }
+        const Rcp rnz = mkrcp<FD>(nZ);
+
+        if (!P.adv_only) {
+            a11 = ldg(geo + G_A11 * fs + o);
+            a12 = ldg(geo + G_A12 * fs + o);
+            a21 = ldg(geo + G_A21 * fs + o);
+            a22 = ldg(geo + G_A22 * fs + o);
+            // solver.cpp:406-445
+            const double hs = dv<FD>(S[0 * BOX + bk], rj);
+            const double hf = dv<FD>(S[1 * BOX + bk], rj);
+            const double h = hs + hf;
+            const Rcp rh = mkrcp<FD>(h);
+            const double phi_s = h < P.h_dry ? 0.0 : dv<FD>(hs, rh);
+            const double phi_f = h < P.h_dry ? 0.0 : dv<FD>(hf, rh);
+            const double vsx = V[0 * BOX + bk], vsy = V[1 * BOX + bk];
+            const double vfx = V[2 * BOX + bk], vfy = V[3 * BOX + bk];
+            const double kap_s = curvature_accel<FD>(vsx, vsy, nX, nY, rnz, dXx, dYx, dZx, dXy, dYy, dZy);
+            const double kap_f = curvature_accel<FD>(vfx, vfy, nX, nY, rnz, dXx, dYx, dZx, dXy, dYy, dZy);
+            // physics::hydrostatic_terms (physics.hpp:56-69)
+            const double p_b_s = smax(0.0, hs * (nZ * P.oma - P.eps_chi * kap_s));
+            const double p_b_f = smax(0.0, hf * (nZ - P.eps_chi * kap_f));
+            // gradient of jb*h*p_bar_f (solver.cpp:419-420)
+            const double gPx = dv<FD>(PJ[bk + 1] - PJ[bk - 1], r2x);
+            const double gPy = dv<FD>(PJ[bk + W2] - PJ[bk - W2], r2y);
+            // solid: gravity + pressure gradient + drag (physics.hpp:98-155)
+            const double sn_sx = jb * p_b_s * nX, sn_sy = jb * p_b_s * nY;
+            const double Avx = a11 * gPx + a21 * gPy;
+            const double Avy = a12 * gPx + a22 * gPy;
+            const double fsp = P.neg_eps_alpha * phi_s;
+            const double sf_sx = fsp * Avx, sf_sy = fsp * Avy;
+            double sv_sx = 0.0, sv_sy = 0.0, sv_fx = 0.0, sv_fy = 0.0;
+            if (!(h <= 0.0)) {
+                const double common = jb * P.C_d * dv<FD>(hs * hf, rh);
+                const double cx = common * (vfx - vsx);
+                const double cy = common * (vfy - vsy);
+                sv_sx = P.alpha * cx;
+                sv_sy = P.alpha * cy;
+                sv_fx = -cx;
+                sv_fy = -cy;
+            }
+            // fluid: gravity + friction + pressure gradient + drag + viscous
+            const double sn_fx = jb * p_b_f * nX, sn_fy = jb * p_b_f * nY;
+            const double coeff = dv<FD>(jb * hf * P.theta_b, mkrcp_const<FD>(P.eps_NR, P.r_eps_NR));
+            const double sd_fx = -coeff * vfx, sd_fy = -coeff * vfy;
+            const double ephf = P.eps * phi_f;
+            const double sf_fx = ephf * Avx, sf_fy = ephf * Avy;
+            const double visc = dv<FD>(ephf, mkrcp_const<FD>(P.N_R, P.r_NR));
+            const double* bvx = BR;
+            const double* bvy = BR + BOX;
+            const double* bxy = BR + 2 * BOX;
+            const double svis_x = visc * (dv<FD>(2.0 * (bvx[bk + 1] - bvx[bk - 1]), r2x) +
+                                          dv<FD>(bxy[bk + W2] - bxy[bk - W2], r2y));
+            const double svis_y = visc * (dv<FD>(2.0 * (bvy[bk + W2] - bvy[bk - W2]), r2y) +
+                                          dv<FD>(bxy[bk + 1] - bxy[bk - 1], r2x));
+            rhs[2] = rhs[2] + (sn_sx + sf_sx + sv_sx);
+            rhs[3] = rhs[3] + (sn_sy + sf_sy + sv_sy);
+            rhs[4] = rhs[4] + (sn_fx + sd_fx + sf_fx + sv_fx + svis_x);
+            rhs[5] = rhs[5] + (sn_fy + sd_fy + sf_fy + sv_fy + svis_y);
+        }
+
+        // stage update: predictor u = u0 + dt*R (:518), corrector u += dt*R (:531)
+        double un[6];
+#pragma unroll
+        for (int f = 0; f < 6; ++f) un[f] = S[f * BOX + bk] + dt * rhs[f];
+
+        // Coulomb cap (solver.cpp:458-479) on the updated state
+        if (P.cap_on) {
+            const double qx = un[2], qy = un[3];
+            if (!(qx == 0.0 && qy == 0.0)) {
+                const double hs = dv<FD>(un[0], rj);
+                if (!(hs < P.h_dry)) {
+                    const double fsld = desing_factor<FD>(hs, P.eps_h);
+                    const double vsx = dv<FD>(qx, rj) * fsld;
+                    const double vsy = dv<FD>(qy, rj) * fsld;
+                    const double kap = curvature_accel<FD>(vsx, vsy, nX, nY, rnz, dXx, dYx, dZx, dXy, dYy, dZy);
+                    const double p_b_s = smax(0.0, hs * (nZ * P.oma - P.eps_chi * kap));
+                    const double rate = jb * p_b_s * P.tan_d;
+                    const double qnorm = sqrt(qx * qx + qy * qy);
+                    const double factor = smax(0.0, 1.0 - dt * rate / qnorm);
+                    un[2] = qx * factor;
+                    un[3] = qy * factor;
+                }
+            }
+        }
+
+        if (CORR) {  // Heun average (solver.cpp:538-541)
+#pragma unroll
+            for (int f = 0; f < 6; ++f) un[f] = 0.5 * (A.u0[f * fs + o] + un[f]);
+        }
+
+        // regularize (solver.cpp:139-166), solid then fluid
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+            double w = un[p];
+            double hp = dv<FD>(w, rj);
+            if (hp < 0.0) {
+                if (hp < -1e-12) {
+                    const unsigned long long key =
+                        (static_cast<unsigned long long>(CORR ? 1 : 0) << 62) |
+                        (static_cast<unsigned long long>(Y) << 32) |
+                        (static_cast<unsigned long long>(X) << 1) | static_cast<unsigned long long>(p);
+                    atomicMin(&sc->err_key, key);
+                    break;  // the reference throws here; leave the cell as computed
+                }
+                atomicAdd(&sc->audit[5 * p + 4], -w * P.cell_area);
+                un[p] = 0.0;
+                hp = 0.0;
+            }
+            if (hp < P.h_dry) {
+                un[2 + 2 * p] = 0.0;
+                un[3 + 2 * p] = 0.0;
+            }
+        }
+
+        if (CORR) {
+            // check_finite (solver.cpp:482-494)
+#pragma unroll
+            for (int f = 0; f < 6; ++f) {
+                if (!isfinite(un[f])) {
+                    const unsigned long long key = (2ull << 62) |
+                                                   (static_cast<unsigned long long>(f) << 56) |
+                                                   (static_cast<unsigned long long>(Y) << 28) |
+                                                   static_cast<unsigned long long>(X);
+                    atomicMin(&sc->err_key, key);
+                }
+            }
+            // lambda of the new state for the next compute_dt (solver.cpp:560-571)
+            const double hs = dv<FD>(un[0], rj);
+            const double hf = dv<FD>(un[1], rj);
+            const double h = hs + hf;
+            if (!(h < P.h_dry)) {
+                const double fsld = desing_factor<FD>(hs, P.eps_h);
+                const double fflu = desing_factor<FD>(hf, P.eps_h);
+                const double vsx = dv<FD>(un[2], rj) * fsld, vsy = dv<FD>(un[3], rj) * fsld;
+                const double vfx = dv<FD>(un[4], rj) * fflu, vfy = dv<FD>(un[5], rj) * fflu;
+                const double cel = sqrt(P.eps * nZ * h);
+                const double lx = smax(fabs(vsx), fabs(vfx)) + cel;
+                const double ly = smax(fabs(vsy), fabs(vfy)) + cel;
+                lam_local = smax(lam_local, smax(lx, ly));
+            }
+        }
+
+#pragma unroll
+        for (int f = 0; f < 6; ++f) A.out[f * fs + o] = un[f];
+    }
+
+    // ---- boundary mass tally of this stage (solver.cpp:352-376), edge tiles only
+    const bool w_edge = X0 == 3;
+    const bool e_edge = (nx - 4) >= X0 && (nx - 4) < X0 + TX;
+    const bool s_edge = g.has_south && Y0 == 3;
+    const bool n_edge = g.has_north && (ny - 4) >= Y0 && (ny - 4) < Y0 + TY;
+    const bool ring = blockIdx.x == 0 || blockIdx.x == A.ntx - 1 || blockIdx.y == 0 ||
+                      blockIdx.y == A.nty - 1;  // every ring tile writes its slot (zeros if no edge)
+    if (ring && threadIdx.x < 2) {
+        const int p = threadIdx.x;
+        const double wdt = dt * 0.5;  // weight_dt = dt / 2.0 (solver.cpp:512, :526)
+        double in = 0.0, outf = 0.0;
+        auto add = [&](double outward) {
+            if (outward >= 0.0) outf += outward;
+            else in += -outward;
+        };
+        const int fxE = nx - 3 - X0;  // xi face index of the east boundary face
+        for (int ty = 0; ty < TY && Y0 + ty <= ny - 4; ++ty) {
+            if (w_edge) add(-FX[p * NFX + ty * (TX + 1) + 0] * P.deta * wdt);
+            if (e_edge) add(FX[p * NFX + ty * (TX + 1) + fxE] * P.deta * wdt);
+        }
+        const int fyN = ny - 3 - Y0;
+        for (int tx = 0; tx < TX && X0 + tx <= nx - 4; ++tx) {
+            if (s_edge) add(-FY[p * NFY + 0 * TX + tx] * P.dxi * wdt);
+            if (n_edge) add(FY[p * NFY + fyN * TX + tx] * P.dxi * wdt);
+        }
+        double* t = A.tally + 4ll * (blockIdx.y * A.ntx + blockIdx.x);
+        t[2 * p + 0] = in;
+        t[2 * p + 1] = outf;
+    }
+
+    if (CORR) lam_block_max(lam_local, sc);
+}
+
+// ---------------------------------------------------------------------------
+// apply_boundaries (solver.cpp:83-137).  One thread per ghost cell of the
+// (slab's) ghost band: zero-gradient == clamp indexing (W/E over interior rows,
+// then S/N over all columns, corners from the corner interior cell), then the
+// Mode-II inflow override of the listed cells' ghosts.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int ghost_band_count(const GridDesc& g) {
+    return (g.has_south ? 3 * g.nx : 0) + (g.has_north ? 3 * g.nx : 0) + 2 * 3 * (g.ny - 6);
+}
+
+__device__ __forceinline__ void ghost_band_cell(const GridDesc& g, int idx, int& i, int& j) {
+    const int nS = g.has_south ? 3 * g.nx : 0;
+    const int nN = g.has_north ? 3 * g.nx : 0;
+    if (idx < nS) { i = idx % g.nx; j = idx / g.nx; return; }
+    idx -= nS;
+    if (idx < nN) { i = idx % g.nx; j = g.ny - 3 + idx / g.nx; return; }
+    idx -= nN;
+    const int rows = g.ny - 6;
+    if (idx < 3 * rows) { i = idx % 3; j = 3 + idx / 3; return; }
+    idx -= 3 * rows;
+    i = g.nx - 3 + idx % 3;
+    j = 3 + idx / 3;
+}
+
+// Hydrograph::at (hydrograph.hpp:31-45), same arithmetic.
+__device__ void hydro_at(const Inflow& in, double t, double& h, double& phi, double& speed) {
+    const double* s = in.samples;
+    const int n = in.n_samples;
+    if (n == 0 || t > s[4 * (n - 1)]) { h = phi = speed = 0.0; return; }
+    if (t <= s[0]) { h = s[1]; phi = s[2]; speed = s[3]; return; }
+    for (int k = 1; k < n; ++k) {
+        if (t <= s[4 * k]) {
+            const double* a = s + 4 * (k - 1);
+            const double* b = s + 4 * k;
+            const double w = (t - a[0]) / (b[0] - a[0]);
+            h = a[1] + w * (b[1] - a[1]);
+            phi = a[2] + w * (b[2] - a[2]);
+            speed = a[3] + w * (b[3] - a[3]);
+            return;
+        }
+    }
+    h = s[4 * (n - 1) + 1]; phi = s[4 * (n - 1) + 2]; speed = s[4 * (n - 1) + 3];
+}
+
+__global__ void bc_kernel(BcArgs a) {
+    if (a.loop && *(volatile int*)&a.sc->done) return;
+    const GridDesc& g = a.g;
+    const int n = ghost_band_count(g);
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= n) return;
+    int i, j;
+    ghost_band_cell(g, idx, i, j);
+    const int si = min(max(i, 3), g.nx - 4);
+    const int sj = min(max(j, 3), g.ny - 4);
+    const long long o = static_cast<long long>(j) * g.pitch + i;
+    const long long so = static_cast<long long>(sj) * g.pitch + si;
+    double v[6];
+#pragma unroll
+    for (int f = 0; f < 6; ++f) v[f] = a.s[f * g.fs + so];
+    if (a.inflow.active) {
+        const int side = a.inflow.ghost_side[idx];
+        if (side) {
+            double t = a.t;
+            if (a.tsrc == 1) t = a.sc->t;
+            else if (a.tsrc == 2) t = a.sc->t + a.sc->dt;
+            const double t_seconds = t * a.inflow.t_unit;
+            double sh, sphi, sspeed;
+            hydro_at(a.inflow, t_seconds, sh, sphi, sspeed);
+            const double h = sh / a.inflow.H;
+            const double speed = sspeed / a.inflow.v_unit;
+            const double hs = h * sphi;
+            const double hf = h * (1.0 - sphi);
+            double vx = 0.0, vy = 0.0;
+            switch (side) {
+                case 'E': vx = -speed; break;
+                case 'W': vx = speed; break;
+                case 'N': vy = -speed; break;
+                case 'S': vy = speed; break;
+            }
+            const double jb = __ldg(a.geo + G_JB * g.fs + o);
+            v[0] = jb * hs;
+            v[1] = jb * hf;
+            v[2] = jb * hs * vx;
+            v[3] = jb * hs * vy;
+            v[4] = jb * hf * vx;
+            v[5] = jb * hf * vy;
+        }
+    }
+#pragma unroll
+    for (int f = 0; f < 6; ++f) a.s[f * g.fs + o] = v[f];
+}
+
+// Copy the ghost band of src into dst (the reference's u_ keeps the ghosts of
+// apply_boundaries(u*, t+dt) after a step, solver.cpp:523).
+__global__ void ghost_copy_kernel(GridDesc g, const double* __restrict__ src, double* dst) {
+    const int n = ghost_band_count(g);
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= n) return;
+    int i, j;
+    ghost_band_cell(g, idx, i, j);
+    const long long o = static_cast<long long>(j) * g.pitch + i;
+#pragma unroll
+    for (int f = 0; f < 6; ++f) dst[f * g.fs + o] = src[f * g.fs + o];
+}
+
+// ---------------------------------------------------------------------------
+// compute_dt lambda loop (solver.cpp:556-573) + exact reduce_max.
+// ---------------------------------------------------------------------------
+template <bool FD>
+__global__ void __launch_bounds__(NT) lambda_kernel(GridDesc g, Phys P, const double* __restrict__ s,
+                                                    const double* __restrict__ geo, DevScalars* sc) {
+    const int X = 3 + blockIdx.x * 32 + (threadIdx.x & 31);
+    const int Y = 3 + blockIdx.y * (NT / 32) + (threadIdx.x >> 5);
+    double lam = 0.0;
+    if (X <= g.nx - 4 && Y <= g.ny - 4) {
+        const long long o = static_cast<long long>(Y) * g.pitch + X;
+        const double jb = __ldg(geo + G_JB * g.fs + o);
+        const Rcp rj = mkrcp<FD>(jb);
+        const double hs = dv<FD>(s[0 * g.fs + o], rj);
+        const double hf = dv<FD>(s[1 * g.fs + o], rj);
+        const double h = hs + hf;
+        const double fsld = desing_factor<FD>(hs, P.eps_h);
+        const double fflu = desing_factor<FD>(hf, P.eps_h);
+        const double vsx = dv<FD>(s[2 * g.fs + o], rj) * fsld;
+        const double vsy = dv<FD>(s[3 * g.fs + o], rj) * fsld;
+        const double vfx = dv<FD>(s[4 * g.fs + o], rj) * fflu;
+        const double vfy = dv<FD>(s[5 * g.fs + o], rj) * fflu;
+        if (!(h < P.h_dry)) {  // physics::wave_speed_bound (physics.hpp:178-189)
+            const double cel = sqrt(P.eps * __ldg(geo + G_NZ * g.fs + o) * h);
+            const double lx = smax(fabs(vsx), fabs(vfx)) + cel;
+            const double ly = smax(fabs(vsy), fabs(vfy)) + cel;
+            lam = smax(lx, ly);
+        }
+    }
+    lam_block_max(lam, sc);
+}
+
+// compute_dt's tail (solver.cpp:575-579) and exact_hit (:641).  One thread.
+__global__ void dt_kernel(Phys P, DevScalars* sc, int loop) {
+    if (loop) {
+        if (sc->done) return;
+        if (!(sc->t < sc->t_end) || sc->steps >= sc->max_steps) { sc->done = 1; return; }
+    }
+    const double lam_max = __longlong_as_double(static_cast<long long>(sc->lam_cur));
+    const double remaining = sc->t_next - sc->t;
+    double dt;
+    if (lam_max <= 0.0) {
+        dt = remaining;
+    } else {
+        dt = P.cfl * smin(P.dxi, P.deta) / lam_max;
+        dt = smin(dt, remaining);
+    }
+    sc->dt = dt;
+    sc->hit = dt == sc->t_next - sc->t;
+    sc->lam_bits = 0ull;
+}
+
+// After the corrector: fold the two stage tallies into the audit (predictor then
+// corrector, as the reference's two accumulate_boundary_fluxes calls), advance
+// t (solver.cpp:643-644), publish lambda for the next dt, set the stop flag.
+__device__ __forceinline__ int ring_tile_count(int ntx, int nty) {
+    if (nty == 1) return ntx;
+    if (ntx == 1) return nty;
+    return 2 * ntx + 2 * (nty - 2);
+}
+__device__ __forceinline__ int ring_tile(int ntx, int nty, int r) {
+    if (nty == 1) return r;
+    if (ntx == 1) return r * ntx;
+    if (r < ntx) return r;                            // bottom row
+    r -= ntx;
+    if (r < ntx) return (nty - 1) * ntx + r;          // top row
+    r -= ntx;
+    const int row = 1 + r / 2;
+    return row * ntx + ((r & 1) ? ntx - 1 : 0);       // left/right columns
+}
+
+__global__ void __launch_bounds__(NT) post_kernel(PostArgs a) {
+    DevScalars* sc = a.sc;
+    if (a.loop && sc->done) return;
+    __shared__ double red[4][NT];
+    const int nring = ring_tile_count(a.ntx, a.nty);
+    for (int stage = 0; stage < 2; ++stage) {
+        const double* tal = stage == 0 ? a.tally_pred : a.tally_corr;
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int r = threadIdx.x; r < nring; r += NT) {
+            const double* t = tal + 4ll * ring_tile(a.ntx, a.nty, r);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[q] += t[q];
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) red[q][threadIdx.x] = acc[q];
+        __syncthreads();
+        for (int w = NT / 2; w > 0; w >>= 1) {
+            if (threadIdx.x < w)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) red[q][threadIdx.x] += red[q][threadIdx.x + w];
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            sc->audit[2] += red[0][0];  // solid injected
+            sc->audit[3] += red[1][0];  // solid outflow
+            sc->audit[7] += red[2][0];  // fluid injected
+            sc->audit[8] += red[3][0];  // fluid outflow
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0 && a.loop) {
+        const double dt = sc->dt;
+        if (sc->dts) sc->dts[sc->steps] = dt;
+        sc->steps += 1;
+        sc->t = sc->hit ? sc->t_next : sc->t + dt;
+        sc->lam_cur = sc->lam_bits;
+        if (sc->err_key != kNoError || sc->hit || sc->steps >= sc->max_steps) sc->done = 1;
+    }
+}
+
+// Standalone Simulator::regularize (solver.cpp:139-166) on the interior.
+template <bool FD>
+__global__ void __launch_bounds__(NT) regularize_kernel(GridDesc g, Phys P, double* s,
+                                                        const double* __restrict__ geo, DevScalars* sc) {
+    const int X = 3 + blockIdx.x * 32 + (threadIdx.x & 31);
+    const int Y = 3 + blockIdx.y * (NT / 32) + (threadIdx.x >> 5);
+    if (X > g.nx - 4 || Y > g.ny - 4) return;
+    const long long o = static_cast<long long>(Y) * g.pitch + X;
+    const double jb = __ldg(geo + G_JB * g.fs + o);
+    const Rcp rj = mkrcp<FD>(jb);
+    for (int p = 0; p < 2; ++p) {
+        const double w = s[p * g.fs + o];
+        double hp = dv<FD>(w, rj);
+        if (hp < 0.0) {
+            if (hp < -1e-12) {
+                const unsigned long long key = (static_cast<unsigned long long>(Y) << 32) |
+                                               (static_cast<unsigned long long>(X) << 1) |
+                                               static_cast<unsigned long long>(p);
+                atomicMin(&sc->err_key, key);
+                return;
+            }
+            atomicAdd(&sc->audit[5 * p + 4], -w * P.cell_area);
+            s[p * g.fs + o] = 0.0;
+            hp = 0.0;
+        }
+        if (hp < P.h_dry) {
+            s[(2 + 2 * p) * g.fs + o] = 0.0;
+            s[(3 + 2 * p) * g.fs + o] = 0.0;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// host-side launch helpers (called from tp_capi.cpp)
+// ---------------------------------------------------------------------------
+size_t stage_smem_bytes() {
+    return sizeof(double) * (6 * BOX + BOX + BOX + 4 * BOX + BOX + 3 * BOX + 6 * NFX + 6 * NFY);
+}
+
+template <bool FD, bool CORR>
+static cudaError_t launch_stage_t(const StageArgs& a, cudaStream_t st) {
+    dim3 grid(a.ntx, a.nty);
+    stage_kernel<FD, CORR><<<grid, NT, stage_smem_bytes(), st>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_stage(const StageArgs& a, bool fastdiv, bool corr, cudaStream_t st) {
+    if (fastdiv) return corr ? launch_stage_t<true, true>(a, st) : launch_stage_t<true, false>(a, st);
+    return corr ? launch_stage_t<false, true>(a, st) : launch_stage_t<false, false>(a, st);
+}
+
+cudaError_t launch_bc(const BcArgs& a, cudaStream_t st) {
+    const int n = (a.g.has_south ? 3 * a.g.nx : 0) + (a.g.has_north ? 3 * a.g.nx : 0) + 6 * (a.g.ny - 6);
+    bc_kernel<<<(n + 255) / 256, 256, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_ghost_copy(const GridDesc& g, const double* src, double* dst, cudaStream_t st) {
+    const int n = (g.has_south ? 3 * g.nx : 0) + (g.has_north ? 3 * g.nx : 0) + 6 * (g.ny - 6);
+    ghost_copy_kernel<<<(n + 255) / 256, 256, 0, st>>>(g, src, dst);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_lambda(const GridDesc& g, const Phys& P, const double* s, const double* geo,
+                          DevScalars* sc, bool fastdiv, cudaStream_t st) {
+    dim3 grid((g.nx - 6 + 31) / 32, (g.ny - 6 + NT / 32 - 1) / (NT / 32));
+    if (fastdiv) lambda_kernel<true><<<grid, NT, 0, st>>>(g, P, s, geo, sc);
+    else lambda_kernel<false><<<grid, NT, 0, st>>>(g, P, s, geo, sc);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dt(const Phys& P, DevScalars* sc, int loop, cudaStream_t st) {
+    dt_kernel<<<1, 1, 0, st>>>(P, sc, loop);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_post(const PostArgs& a, cudaStream_t st) {
+    post_kernel<<<1, NT, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_regularize(const GridDesc& g, const Phys& P, double* s, const double* geo,
+                              DevScalars* sc, bool fastdiv, cudaStream_t st) {
+    dim3 grid((g.nx - 6 + 31) / 32, (g.ny - 6 + NT / 32 - 1) / (NT / 32));
+    if (fastdiv) regularize_kernel<true><<<grid, NT, 0, st>>>(g, P, s, geo, sc);
+    else regularize_kernel<false><<<grid, NT, 0, st>>>(g, P, s, geo, sc);
+    return cudaGetLastError();
+}
+
+}  // namespace tpb
+
+namespace tpb {
+// Opt every stage variant into its dynamic shared memory before any graph capture.
+cudaError_t init_kernels() {
+    const int smem = static_cast<int>(stage_smem_bytes());
+    cudaError_t e;
+    if ((e = cudaFuncSetAttribute(stage_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) != cudaSuccess) return e;
+    if ((e = cudaFuncSetAttribute(stage_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) != cudaSuccess) return e;
+    if ((e = cudaFuncSetAttribute(stage_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) != cudaSuccess) return e;
+    if ((e = cudaFuncSetAttribute(stage_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) != cudaSuccess) return e;
+    return cudaSuccess;
+}
+}  // namespace tpb
+
+// ---------------------------------------------------------------------------
+// Self-test of the FASTDIV identity: dv<true>(a, mkrcp(b)) == a / b bit for bit
+// over random operands (random mantissas, exponents spread over the whole
+// in-range window, plus values straddling the guard limits and signed zeros).
+// ---------------------------------------------------------------------------
+namespace tpb {
+__device__ __forceinline__ unsigned long long splitmix(unsigned long long& s) {
+    unsigned long long z = (s += 0x9e3779b97f4a7c15ull);
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+}
+__device__ double rand_double(unsigned long long& s, int emin, int emax) {
+    unsigned long long r = splitmix(s);
+    unsigned long long mant = r & 0xfffffffffffffull;
+    int e = emin + static_cast<int>(splitmix(s) % static_cast<unsigned long long>(emax - emin + 1));
+    unsigned long long sign = (r >> 63) << 63;
+    if ((r & 0x3f0000000000000ull) == 0) mant = (r & 1) ? 0xfffffffffffffull : 0ull;  // edge mantissas
+    return __longlong_as_double(static_cast<long long>(sign | (static_cast<unsigned long long>(e + 1023) << 52) | mant));
+}
+__global__ void selftest_div_kernel(long long n, unsigned long long seed, unsigned long long* bad) {
+    long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+    unsigned long long local = 0;
+    for (; i < n; i += stride) {
+        unsigned long long s = seed ^ (static_cast<unsigned long long>(i) * 0x2545F4914F6CDD1Dull);
+        const int mode = static_cast<int>(splitmix(s) & 3);
+        double b = rand_double(s, mode == 0 ? -210 : -40, mode == 0 ? 210 : 40);
+        double a = rand_double(s, mode == 1 ? -820 : -60, mode == 1 ? 820 : 60);
+        if (mode == 3 && (i & 7) == 0) a = (i & 8) ? 0.0 : -0.0;
+        const Rcp r = mkrcp<true>(b);
+        const double q = dv<true>(a, r);
+        const double ref = a / b;
+        if (__double_as_longlong(q) != __double_as_longlong(ref)) ++local;
+    }
+    if (local) atomicAdd(bad, local);
+}
+cudaError_t selftest_division(long long n, unsigned long long seed, unsigned long long* mismatches) {
+    unsigned long long* d = nullptr;
+    cudaError_t e = cudaMalloc(&d, sizeof(unsigned long long));
+    if (e != cudaSuccess) return e;
+    cudaMemset(d, 0, sizeof(unsigned long long));
+    selftest_div_kernel<<<148 * 8, 256>>>(n, seed, d);
+    e = cudaMemcpy(mismatches, d, sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    return e;
+}
+}  // namespace tpb

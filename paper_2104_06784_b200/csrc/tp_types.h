@@ -1,0 +1,119 @@
+// Plain data structures shared by the kernels (nvcc) and the host library (g++).
+// No device code here: this header is included by tp_capi.cpp.
+#pragma once
+
+#include <cstdint>
+
+
+
+namespace tpb {
+
+struct Phys {
+    // model constants (params.hpp:29-51, config.hpp:18-22), host-evaluated once
+    double eps;        // ScalingConfig::epsilon()
+    double alpha;      // alpha_rho
+    double oma;        // 1.0 - alpha_rho
+    double C_d, N_R, theta_b;
+    double eps_chi;    // std::pow(eps, chi)          (physics.hpp:60, solver.cpp:470)
+    double tan_d;      // params.tan_delta_b()        (params.hpp:38)
+    double neg_eps_alpha;  // -eps * alpha_rho         (physics.hpp:147)
+    double eps_NR;     // eps * N_R                   (physics.hpp:115)
+    double h_dry, eps_h;
+    double dxi, deta, two_dxi, two_deta;
+    double cell_area;  // dxi * deta                  (solver.cpp:140)
+    double cfl;
+    // RN(1/x) of the constant divisors (FASTDIV)
+    double r_dxi, r_deta, r_two_dxi, r_two_deta, r_eps_NR, r_NR;
+    int adv_only;      // Simulator::set_advection_only (solver.hpp:60-62)
+    int cap_on;        // !(adv_only || tan_delta_b() == 0.0)  (solver.cpp:454)
+};
+
+
+// Geometry field order = TerrainGeometry declaration order (terrain.hpp:59-63).
+enum GeoField {
+    G_NX = 0, G_NY, G_NZ, G_JB, G_A11, G_A12, G_A21, G_A22,
+    G_DNX_DXI, G_DNY_DXI, G_DNZ_DXI, G_DNX_DETA, G_DNY_DETA, G_DNZ_DETA, G_COUNT
+};
+// State field order = MixtureState::fields() (state.hpp:29).
+enum StateField { S_WS = 0, S_WF, S_QSX, S_QSY, S_QFX, S_QFY, S_COUNT };
+
+constexpr unsigned long long kNoError = ~0ull;
+
+// Device-resident step scalars: the time loop of Simulator::run
+// (solver.cpp:637-649) lives here so the host never waits on dt.
+struct DevScalars {
+    double t;        // scaled time
+    double t_next;   // target of this tp_steps call (min(next_out, t_end))
+    double t_end;    // loop bound (solver.cpp:637)
+    double dt;       // dt of the step in flight
+    long long steps;
+    long long max_steps;
+    int done;        // stop flag: every loop kernel returns immediately when set
+    int hit;         // exact_hit of the step in flight (solver.cpp:641)
+    unsigned long long lam_bits;  // atomicMax accumulator of lambda (bits of a double >= 0)
+    unsigned long long lam_cur;   // lambda_max of the current state (compute_dt input)
+    unsigned long long err_key;   // earliest error (see error keys in tp_kernels.cu)
+    double audit[10];             // solid {initial, final, injected, outflow, clipped}, fluid {...}
+    double* dts;                  // optional per-step dt record (device)
+};
+
+struct GridDesc {
+    int nx, ny;       // padded dims of this (slab of the) grid
+    int pitch;        // row pitch in doubles
+    long long fs;     // field stride in doubles
+    int has_south, has_north;  // physical S/N boundaries (always 1 on a single device)
+};
+
+struct Inflow {
+    int n_samples;
+    const double* samples;  // [n][4] t, h, phi_s, speed (physical units)
+    const signed char* ghost_side;  // per ghost-band index: 0 or 'E','W','N','S'
+    double t_unit, H, v_unit;
+    int active;
+};
+
+// Stage kernel tile: TX x TY interior cells, NT threads.  TX*TY*2 + TX + TY = 511
+// faces <= 2 * NT, so the face work of a tile is exactly two rounds.
+constexpr int TX = 16;
+constexpr int TY = 15;
+constexpr int NT = 256;
+constexpr int W2 = TX + 4;
+constexpr int H2 = TY + 4;
+constexpr int BOX = W2 * H2;
+constexpr int NFX = (TX + 1) * TY;
+constexpr int NFY = TX * (TY + 1);
+
+struct StageArgs {
+    GridDesc g;
+    Phys ph;
+    const double* __restrict__ s;    // stage input state (6 fields, ghosts filled)
+    const double* __restrict__ u0;   // corrector: u^n (interior read at own cell only)
+    double* out;                     // stage output state (interior written)
+    const double* __restrict__ geo;  // 14 geometry fields
+    DevScalars* sc;
+    double* tally;                   // per-tile boundary mass tally [ntiles][4]
+    int ntx, nty;
+    int loop;                        // 1 = obey sc->done (device-resident loop)
+    int use_sc_dt;                   // read dt from sc (always 1 in practice)
+};
+
+struct BcArgs {
+    GridDesc g;
+    double* s;
+    const double* __restrict__ geo;
+    Inflow inflow;
+    DevScalars* sc;
+    double t;       // used when tsrc == 0
+    int tsrc;       // 0: t argument, 1: sc->t, 2: sc->t + sc->dt
+    int loop;
+};
+
+struct PostArgs {
+    DevScalars* sc;
+    const double* tally_pred;
+    const double* tally_corr;
+    int ntx, nty;
+    int loop;
+};
+
+}  // namespace tpb
