@@ -7,6 +7,8 @@
 // tp_kernels.cu on one CUDA stream.  tp_steps runs Simulator::run's loop body
 // (solver.cpp:637-649) entirely on the device, replayed from a CUDA graph; the
 // host synchronises once per graph (graph_steps steps).
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -51,6 +53,37 @@ inline void ck(cudaError_t e, const char* what) {
 
 constexpr size_t kCtrlBytes = offsetof(DevScalars, lam_bits);
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        ck(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q),
+           "cuTensorMapEncodeTiled entry point");
+        if (!p || q != cudaDriverEntryPointSuccess) throw CudaErr{"cuTensorMapEncodeTiled unavailable"};
+        fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+// 3-D tiled descriptor over [nfields][ny][pitch] doubles with the stage-kernel box
+CUtensorMap make_box_map(void* base, int nx, int ny, int pitch, long long fs, int nfields) {
+    CUtensorMap m;
+    cuuint64_t dims[3] = {static_cast<cuuint64_t>(nx), static_cast<cuuint64_t>(ny),
+                          static_cast<cuuint64_t>(nfields)};
+    cuuint64_t strides[2] = {static_cast<cuuint64_t>(pitch) * sizeof(double),
+                             static_cast<cuuint64_t>(fs) * sizeof(double)};
+    cuuint32_t box[3] = {static_cast<cuuint32_t>(tpb::W2), static_cast<cuuint32_t>(tpb::H2),
+                         static_cast<cuuint32_t>(nfields)};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, estr,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw CudaErr{"cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")"};
+    return m;
+}
+
 }  // namespace
 
 struct tp_ctx {
@@ -68,6 +101,12 @@ struct tp_ctx {
     std::vector<double> geo_h;  // 14 * nx * ny (dense, local rows)
     tpb::host::Dem dem;
     // device
+    // logical element (i, j) of a field lives at raw[f*fs + j*pitch + i + 1]: one
+    // leading pad column makes every stage-kernel box origin (column X0-2, X0 = 3+16k)
+    // 16-byte aligned, which TMA requires.  dX = rawX + 1.
+    double* rawA = nullptr;
+    double* rawB = nullptr;
+    double* rawGeo = nullptr;
     double* dA = nullptr;
     double* dB = nullptr;
     double* dGeo = nullptr;
@@ -94,6 +133,7 @@ struct tp_ctx {
     int graphK_steps = 0;
     long launches = 0;
     double t_next_last = 0.0;
+    CUtensorMap tmA{}, tmB{}, tmG{};
 };
 
 namespace {
@@ -171,6 +211,8 @@ void drop_graphs(tp_ctx* c) {
 
 tpb::StageArgs stage_args(tp_ctx* c, bool corr, int loop) {
     tpb::StageArgs a{};
+    a.tm_s = corr ? c->tmB : c->tmA;
+    a.tm_g = c->tmG;
     a.g = c->g;
     a.ph = c->ph;
     a.s = corr ? c->dB : c->dA;
@@ -286,7 +328,7 @@ void raise_error_key(tp_ctx* c, unsigned long long key, const double* pred_buf) 
         const int p = static_cast<int>(key & 1ull);
         const double* buf = cls == 0 ? pred_buf : c->dA;
         const double w = read_cell(c, buf, p, X, Y);
-        const double jb = c->geo_h[3ull * c->nx * c->ny + static_cast<size_t>(Y) * c->nx + X];
+        const double jb = c->geo_h[static_cast<size_t>(tpb::R_JB) * c->nx * c->ny + static_cast<size_t>(Y) * c->nx + X];
         const double hp = w / jb;
         throw NumErr{std::string("negative ") + (p == 0 ? "solid" : "fluid") + " thickness " +
                      tpb::host::to_string_f(hp) + " at cell (" + std::to_string(X - kGhost) + ", " +
@@ -397,7 +439,7 @@ void create_impl(tp_ctx* c, const tp_params* p, const tp_dem* dem, int row0, int
                     G.field(k) + static_cast<size_t>(row0) * G.nx,
                     sizeof(double) * static_cast<size_t>(c->nx) * c->ny);
 
-    c->pitch = (c->nx + 7) & ~7;
+    c->pitch = (c->nx + 1 + 7) & ~7;
     c->fs = static_cast<long long>(c->pitch) * c->ny;
     c->g.nx = c->nx;
     c->g.ny = c->ny;
@@ -411,23 +453,59 @@ void create_impl(tp_ctx* c, const tp_params* p, const tp_dem* dem, int row0, int
     c->nty = (c->nrows + tpb::TY - 1) / tpb::TY;
 
     const size_t sbytes = sizeof(double) * 6ull * c->fs;
-    ck(cudaMalloc(&c->dA, sbytes), "cudaMalloc state A");
-    ck(cudaMalloc(&c->dB, sbytes), "cudaMalloc state B");
-    ck(cudaMalloc(&c->dGeo, sizeof(double) * 14ull * c->fs), "cudaMalloc geometry");
+    ck(cudaMalloc(&c->rawA, sbytes), "cudaMalloc state A");
+    ck(cudaMalloc(&c->rawB, sbytes), "cudaMalloc state B");
+    ck(cudaMalloc(&c->rawGeo, sizeof(double) * tpb::G_COUNT * c->fs), "cudaMalloc geometry");
+    c->dA = c->rawA + 1;
+    c->dB = c->rawB + 1;
+    c->dGeo = c->rawGeo + 1;
     ck(cudaMalloc(&c->dSc, sizeof(DevScalars)), "cudaMalloc scalars");
     const size_t tb = sizeof(double) * 4ull * c->ntx * c->nty;
     ck(cudaMalloc(&c->dTallyP, tb), "cudaMalloc tally");
     ck(cudaMalloc(&c->dTallyC, tb), "cudaMalloc tally");
     ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
     c->own_stream = true;
-    ck(cudaMemsetAsync(c->dA, 0, sbytes, c->stream), "memset");
-    ck(cudaMemsetAsync(c->dB, 0, sbytes, c->stream), "memset");
+    ck(cudaMemsetAsync(c->rawA, 0, sbytes, c->stream), "memset");
+    ck(cudaMemsetAsync(c->rawB, 0, sbytes, c->stream), "memset");
     ck(cudaMemsetAsync(c->dTallyP, 0, tb, c->stream), "memset");
     ck(cudaMemsetAsync(c->dTallyC, 0, tb, c->stream), "memset");
-    ck(cudaMemsetAsync(c->dGeo, 0, sizeof(double) * 14ull * c->fs, c->stream), "memset");
-    ck(cudaMemcpy2DAsync(c->dGeo, c->pitch * sizeof(double), c->geo_h.data(), c->nx * sizeof(double),
-                         c->nx * sizeof(double), 14ull * c->ny, cudaMemcpyHostToDevice, c->stream),
-       "geometry H2D");
+    {
+        // device geometry layout (tp_types.h GeoField): the 14 reference fields
+        // regrouped + RN(1/jb), RN(1/nZ) and the face RN(1/jbf) of the whole grid
+        const size_t n = static_cast<size_t>(c->nx) * c->ny;
+        const size_t gnx = static_cast<size_t>(G.nx);
+        std::vector<double> dg(static_cast<size_t>(tpb::G_COUNT) * n, 0.0);
+        auto src = [&](int rf) { return c->geo_h.data() + static_cast<size_t>(rf) * n; };
+        const int map[][2] = {{tpb::G_JB, tpb::R_JB},   {tpb::G_NZ, tpb::R_NZ},   {tpb::G_A11, tpb::R_A11},
+                              {tpb::G_A12, tpb::R_A12}, {tpb::G_A21, tpb::R_A21}, {tpb::G_A22, tpb::R_A22},
+                              {tpb::G_NX, tpb::R_NX},   {tpb::G_NY, tpb::R_NY},
+                              {tpb::G_DNX_DXI, tpb::R_DNX_DXI},   {tpb::G_DNY_DXI, tpb::R_DNY_DXI},
+                              {tpb::G_DNZ_DXI, tpb::R_DNZ_DXI},   {tpb::G_DNX_DETA, tpb::R_DNX_DETA},
+                              {tpb::G_DNY_DETA, tpb::R_DNY_DETA}, {tpb::G_DNZ_DETA, tpb::R_DNZ_DETA}};
+        for (const auto& m : map) std::memcpy(dg.data() + m[0] * n, src(m[1]), sizeof(double) * n);
+        const double* gjb = G.field(tpb::R_JB);  // global rows: the face average may reach row1+3
+        for (int j = 0; j < c->ny; ++j) {
+            const int gj = j + row0;
+            for (int i = 0; i < c->nx; ++i) {
+                const size_t k = static_cast<size_t>(j) * c->nx + i;
+                const double jb = gjb[gj * gnx + i];
+                dg[tpb::G_RJB * n + k] = 1.0 / jb;
+                dg[tpb::G_RNZ * n + k] = 1.0 / src(tpb::R_NZ)[k];
+                if (i + 1 < c->nx) dg[tpb::G_RJBFX * n + k] = 1.0 / (0.5 * (jb + gjb[gj * gnx + i + 1]));
+                if (gj + 1 < G.ny) dg[tpb::G_RJBFY * n + k] = 1.0 / (0.5 * (jb + gjb[(gj + 1) * gnx + i]));
+            }
+        }
+        ck(cudaMemsetAsync(c->rawGeo, 0, sizeof(double) * tpb::G_COUNT * c->fs, c->stream), "memset");
+        ck(cudaMemcpy2DAsync(c->dGeo, c->pitch * sizeof(double), dg.data(), c->nx * sizeof(double),
+                             c->nx * sizeof(double), static_cast<size_t>(tpb::G_COUNT) * c->ny,
+                             cudaMemcpyHostToDevice, c->stream),
+           "geometry H2D");
+        ck(cudaStreamSynchronize(c->stream), "sync");
+    }
+    // the maps cover the pad column too (x coordinate = logical column + 1)
+    c->tmA = make_box_map(c->rawA, c->nx + 1, c->ny, c->pitch, c->fs, 6);
+    c->tmB = make_box_map(c->rawB, c->nx + 1, c->ny, c->pitch, c->fs, 6);
+    c->tmG = make_box_map(c->rawGeo, c->nx + 1, c->ny, c->pitch, c->fs, tpb::NGBOX);
     DevScalars h{};
     h.lam_bits = 0;
     h.lam_cur = 0;
@@ -469,9 +547,9 @@ void tp_destroy(tp_ctx* c) {
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
     drop_graphs(c);
-    cudaFree(c->dA);
-    cudaFree(c->dB);
-    cudaFree(c->dGeo);
+    cudaFree(c->rawA);
+    cudaFree(c->rawB);
+    cudaFree(c->rawGeo);
     cudaFree(c->dSc);
     cudaFree(c->dTallyP);
     cudaFree(c->dTallyC);

@@ -12,21 +12,29 @@ namespace tpb {
 // on the left (cell i, +edge) and right (cell i+1, -edge) of the face.
 // XI = true for a xi face (normal X: a_nn = a11, a_nt = a12), false for eta
 // (normal Y: a_nn = a22, a_nt = a21).  out[6] in field order.
+// rjbf = RN(1/jbf) precomputed on the host (geometry field G_RJBFX/G_RJBFY).
 template <bool FD, bool XI>
 __device__ __forceinline__ void face_flux(const double (&L)[6], const double (&R)[6], double jb_l,
                                           double jb_r, double nZ_l, double nZ_r, double ann_l,
-                                          double ann_r, double ant_l, double ant_r, const Phys& P,
-                                          double (&out)[6]) {
+                                          double ann_r, double ant_l, double ant_r, double rjbf,
+                                          const Phys& P, double (&out)[6]) {
     // solver.cpp:242-245
     const double jbf = 0.5 * (jb_l + jb_r);
     const double cf = 0.5 * (nZ_l + nZ_r);
     const double ann = 0.5 * (ann_l + ann_r);
     const double ant = 0.5 * (ant_l + ant_r);
-    const Rcp rj = mkrcp<FD>(jbf);
+    const Rcp rj = mkrcp_const<FD>(jbf, rjbf);
 
     // solver.cpp:265-275
-    const double hL0 = dv<FD>(L[0], rj), hL1 = dv<FD>(L[1], rj);
-    const double hR0 = dv<FD>(R[0], rj), hR1 = dv<FD>(R[1], rj);
+    bool ok = rj.ok;
+    double hL0 = dq<FD>(L[0], rj, ok), hL1 = dq<FD>(L[1], rj, ok);
+    double hR0 = dq<FD>(R[0], rj, ok), hR1 = dq<FD>(R[1], rj, ok);
+    if (!ok) {
+        dfix<FD>(hL0, L[0], rj);
+        dfix<FD>(hL1, L[1], rj);
+        dfix<FD>(hR0, R[0], rj);
+        dfix<FD>(hR1, R[1], rj);
+    }
     const double htL = hL0 + hL1;
     const double htR = hR0 + hR1;
     if (htL < P.h_dry && htR < P.h_dry) {
@@ -44,10 +52,19 @@ __device__ __forceinline__ void face_flux(const double (&L)[6], const double (&R
     const double qnL1 = XI ? L[4] : L[5], qtL1 = XI ? L[5] : L[4];
     const double qnR1 = XI ? R[4] : R[5], qtR1 = XI ? R[5] : R[4];
 
-    const double vnL0 = dv<FD>(qnL0, rj) * desing_factor<FD>(smax(hL0, 0.0), P.eps_h);
-    const double vnR0 = dv<FD>(qnR0, rj) * desing_factor<FD>(smax(hR0, 0.0), P.eps_h);
-    const double vnL1 = dv<FD>(qnL1, rj) * desing_factor<FD>(smax(hL1, 0.0), P.eps_h);
-    const double vnR1 = dv<FD>(qnR1, rj) * desing_factor<FD>(smax(hR1, 0.0), P.eps_h);
+    ok = rj.ok;
+    double jL0 = dq<FD>(qnL0, rj, ok), jR0 = dq<FD>(qnR0, rj, ok);
+    double jL1 = dq<FD>(qnL1, rj, ok), jR1 = dq<FD>(qnR1, rj, ok);
+    if (!ok) {
+        dfix<FD>(jL0, qnL0, rj);
+        dfix<FD>(jR0, qnR0, rj);
+        dfix<FD>(jL1, qnL1, rj);
+        dfix<FD>(jR1, qnR1, rj);
+    }
+    const double vnL0 = jL0 * desing_factor<FD>(smax(hL0, 0.0), P.eps_h);
+    const double vnR0 = jR0 * desing_factor<FD>(smax(hR0, 0.0), P.eps_h);
+    const double vnL1 = jL1 * desing_factor<FD>(smax(hL1, 0.0), P.eps_h);
+    const double vnR1 = jR1 * desing_factor<FD>(smax(hR1, 0.0), P.eps_h);
     double a = 0.0;
     a = smax(a, smax(fabs(vnL0) + celL, fabs(vnR0) + celR));
     a = smax(a, smax(fabs(vnL1) + celL, fabs(vnR1) + celR));

@@ -48,19 +48,68 @@ __device__ __forceinline__ void lam_block_max(double lam, DevScalars* sc) {
 }
 
 // ---------------------------------------------------------------------------
+// TMA / mbarrier helpers (sm_90+ PTX, used here on sm_100a)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, int x, int y, int z,
+                                            unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<unsigned long long>(tm)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
+// shared-memory carve-up of the stage kernel (doubles)
+constexpr int SM_S = 0;                                   // [6][BOX] state box (TMA)
+constexpr int SM_G = ((6 * BOX * 8 + 127) / 128) * 16;    // [NGBOX][BOX] geometry box (TMA), 128B aligned
+constexpr int SM_V = SM_G + NGBOX * BOX;                  // [4][BOX] cell velocities
+constexpr int SM_PJ = SM_V + 4 * BOX;                     // [BOX] jb*h*p_bar_f
+constexpr int SM_BR = SM_PJ + BOX;                        // [3][BOX] viscous brackets
+constexpr int SM_FX = SM_BR + 3 * BOX;                    // [6][NFX] xi face fluxes
+constexpr int SM_FY = SM_FX + 6 * NFX;                    // [6][NFY] eta face fluxes
+constexpr int SM_END = SM_FY + 6 * NFY;
+constexpr unsigned kTmaBytes = (6 + NGBOX) * BOX * 8;
+
+// ---------------------------------------------------------------------------
 // The fused stage kernel.
 // ---------------------------------------------------------------------------
 template <bool FD, bool CORR>
-__global__ void __launch_bounds__(NT, 2) stage_kernel(StageArgs A) {
-    extern __shared__ double sm[];
-    double* S = sm;               // [6][H2][W2] state on the radius-2 box
-    double* JB = S + 6 * BOX;     // [H2][W2]    jb
-    double* RJ = JB + BOX;        // [H2][W2]    RN(1/jb) (FASTDIV)
-    double* V = RJ + BOX;         // [4][H2][W2] vxs, vys, vxf, vyf
-    double* PJ = V + 4 * BOX;     // [H2][W2]    jb*h*p_bar_f
-    double* BR = PJ + BOX;        // [3][H2][W2] viscous brackets bx, by, bxy
-    double* FX = BR + 3 * BOX;    // [6][TY][TX+1] xi face fluxes
-    double* FY = FX + 6 * NFX;    // [6][TY+1][TX] eta face fluxes
+__global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ StageArgs A) {
+    extern __shared__ __align__(128) double sm[];
+    __shared__ unsigned long long bar;
+    double* S = sm + SM_S;
+    const double* G = sm + SM_G;
+    double* V = sm + SM_V;
+    double* PJ = sm + SM_PJ;
+    double* BR = sm + SM_BR;
+    double* FX = sm + SM_FX;
+    double* FY = sm + SM_FY;
 
     DevScalars* sc = A.sc;
     if (A.loop && *(volatile int*)&sc->done) return;
@@ -68,112 +117,127 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(StageArgs A) {
     const GridDesc& g = A.g;
     const Phys& P = A.ph;
     const int nx = g.nx, ny = g.ny, pitch = g.pitch;
-    const long long fs = g.fs;
     const int X0 = 3 + blockIdx.x * TX;
     const int Y0 = 3 + blockIdx.y * TY;
     const int bx0 = X0 - 2, by0 = Y0 - 2;
-    const double* __restrict__ geo = A.geo;
 
-    // ---- Phase 0: stage the state and jb of the radius-2 box ----------------
-    for (int k = threadIdx.x; k < BOX; k += NT) {
-        const int gx = bx0 + k % W2, gy = by0 + k / W2;
-        const bool in = gx < nx && gy < ny;
-        const long long o = static_cast<long long>(gy) * pitch + gx;
-#pragma unroll
-        for (int f = 0; f < 6; ++f) S[f * BOX + k] = in ? A.s[f * fs + o] : 0.0;
-        JB[k] = in ? ldg(geo + G_JB * fs + o) : 1.0;
+    // ---- Phase 0: one TMA transaction stages the radius-2 box of the 6 state
+    // fields and the 9 stencil geometry fields (OOB -> zeros, edge tiles only).
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        mbar_expect_tx(&bar, kTmaBytes);
+        // x coordinate + 1: the leading pad column of the device layout (tp_capi.cpp)
+        tma_load_3d(S, &A.tm_s, bx0 + 1, by0, 0, &bar);
+        tma_load_3d(sm + SM_G, &A.tm_g, bx0 + 1, by0, 0, &bar);
     }
-    __syncthreads();
+    const double dt = sc->dt;
+    // the Phase-3 cell of this thread: warm L2 with its per-cell geometry (and u^n)
+    const int p3x = X0 + (threadIdx.x % TX), p3y = Y0 + (threadIdx.x / TX);
+    const bool p3 = threadIdx.x < TX * TY && p3x <= nx - 4 && p3y <= ny - 4;
+    const long long o3 = static_cast<long long>(p3y) * pitch + p3x;
+    const double* __restrict__ geo = A.geo;
+    const long long fs = g.fs;
+    if (p3) {
+#pragma unroll
+        for (int f = G_NX; f <= G_RNZ; ++f) prefetch_l2(geo + f * fs + o3);
+        if (CORR) {
+#pragma unroll
+            for (int f = 0; f < 6; ++f) prefetch_l2(A.u0 + f * fs + o3);
+        }
+    }
+    __syncthreads();  // barrier init visible
+    mbar_wait(&bar, 0);
 
     // ---- Phase 1: xi faces, eta faces, cell fields -----------------------------
-    constexpr int NXP = ((NFX + 31) / 32) * 32;   // face lists padded to warp multiples
+    constexpr int NXP = ((NFX + 31) / 32) * 32;  // face lists padded to warp multiples
     constexpr int NYP = ((NFY + 31) / 32) * 32;
     constexpr int N1 = NXP + NYP + BOX;
     for (int it = threadIdx.x; it < N1; it += NT) {
         if (it < NXP) {
             if (it >= NFX) continue;
-            // xi face between box cells (fx+1, by) and (fx+2, by); stored at FX[ty][fx]
+            // xi face between box cells k and k+1 (row ty+2), stored at FX[ty][fx]
             const int fx = it % (TX + 1), ty = it / (TX + 1);
-            const int by = ty + 2;
-            const int gy = by0 + by, gxl = bx0 + fx + 1;
+            const int k = (ty + 2) * W2 + fx + 1;
             double L[6], R[6];
 #pragma unroll
             for (int f = 0; f < 6; ++f) {
-                const double* row = S + f * BOX + by * W2 + fx;
+                const double* row = S + f * BOX + k - 1;
                 const double c0 = row[0], c1 = row[1], c2 = row[2], c3 = row[3];
                 L[f] = edge_plus(c0, c1, c2);
                 R[f] = edge_minus(c1, c2, c3);
             }
-            const bool in = (gxl + 1) < nx && gy < ny;
-            const long long o = static_cast<long long>(gy) * pitch + gxl;
-            const double nZl = in ? ldg(geo + G_NZ * fs + o) : 1.0;
-            const double nZr = in ? ldg(geo + G_NZ * fs + o + 1) : 1.0;
-            const double a11l = in ? ldg(geo + G_A11 * fs + o) : 0.0;
-            const double a11r = in ? ldg(geo + G_A11 * fs + o + 1) : 0.0;
-            const double a12l = in ? ldg(geo + G_A12 * fs + o) : 0.0;
-            const double a12r = in ? ldg(geo + G_A12 * fs + o + 1) : 0.0;
             double out[6];
-            face_flux<FD, true>(L, R, JB[by * W2 + fx + 1], JB[by * W2 + fx + 2], nZl, nZr, a11l,
-                                a11r, a12l, a12r, P, out);
+            face_flux<FD, true>(L, R, G[G_JB * BOX + k], G[G_JB * BOX + k + 1], G[G_NZ * BOX + k],
+                                G[G_NZ * BOX + k + 1], G[G_A11 * BOX + k], G[G_A11 * BOX + k + 1],
+                                G[G_A12 * BOX + k], G[G_A12 * BOX + k + 1], G[G_RJBFX * BOX + k], P, out);
 #pragma unroll
-            for (int f = 0; f < 6; ++f) FX[f * NFX + ty * (TX + 1) + fx] = out[f];
+            for (int f = 0; f < 6; ++f) FX[f * NFX + it] = out[f];
         } else if (it < NXP + NYP) {
             const int jt = it - NXP;
             if (jt >= NFY) continue;
-            // eta face between box cells (bx, fy+1) and (bx, fy+2); stored at FY[fy][tx]
+            // eta face between box cells k and k+W2 (column tx+2), stored at FY[fy][tx]
             const int tx = jt % TX, fy = jt / TX;
-            const int bx = tx + 2;
-            const int gx = bx0 + bx, gyl = by0 + fy + 1;
+            const int k = (fy + 1) * W2 + tx + 2;
             double L[6], R[6];
 #pragma unroll
             for (int f = 0; f < 6; ++f) {
-                const double* col = S + f * BOX + fy * W2 + bx;
+                const double* col = S + f * BOX + k - W2;
                 const double c0 = col[0], c1 = col[W2], c2 = col[2 * W2], c3 = col[3 * W2];
                 L[f] = edge_plus(c0, c1, c2);
                 R[f] = edge_minus(c1, c2, c3);
             }
-            const bool in = gx < nx && (gyl + 1) < ny;
-            const long long o = static_cast<long long>(gyl) * pitch + gx;
-            const double nZl = in ? ldg(geo + G_NZ * fs + o) : 1.0;
-            const double nZr = in ? ldg(geo + G_NZ * fs + o + pitch) : 1.0;
-            const double a22l = in ? ldg(geo + G_A22 * fs + o) : 0.0;
-            const double a22r = in ? ldg(geo + G_A22 * fs + o + pitch) : 0.0;
-            const double a21l = in ? ldg(geo + G_A21 * fs + o) : 0.0;
-            const double a21r = in ? ldg(geo + G_A21 * fs + o + pitch) : 0.0;
             double out[6];
-            face_flux<FD, false>(L, R, JB[(fy + 1) * W2 + bx], JB[(fy + 2) * W2 + bx], nZl, nZr,
-                                 a22l, a22r, a21l, a21r, P, out);
+            face_flux<FD, false>(L, R, G[G_JB * BOX + k], G[G_JB * BOX + k + W2], G[G_NZ * BOX + k],
+                                 G[G_NZ * BOX + k + W2], G[G_A22 * BOX + k], G[G_A22 * BOX + k + W2],
+                                 G[G_A21 * BOX + k], G[G_A21 * BOX + k + W2], G[G_RJBFY * BOX + k], P,
+                                 out);
 #pragma unroll
-            for (int f = 0; f < 6; ++f) FY[f * NFY + fy * TX + tx] = out[f];
+            for (int f = 0; f < 6; ++f) FY[f * NFY + jt] = out[f];
         } else {
-            // cell fields (solver.cpp:172-184) on the box cell k
-            const int k = it - NXP - NYP;
-            const int bx = k % W2, by = k / W2;
-            const double jb = JB[k];
-            const Rcp rj = mkrcp<FD>(jb);
-            if (FD) RJ[k] = rj.r;
+            // cell fields (solver.cpp:172-184) on box cell k
             if (P.adv_only) continue;  // velocities/pjb feed sources and brackets only
-            const double hs = dv<FD>(S[0 * BOX + k], rj);
-            const double hf = dv<FD>(S[1 * BOX + k], rj);
+            const int k = it - NXP - NYP;
+            const double jb = G[G_JB * BOX + k];
+            const Rcp rj = mkrcp_const<FD>(jb, G[G_RJB * BOX + k]);
+            const double ws = S[0 * BOX + k], wf = S[1 * BOX + k];
+            const double qsx = S[2 * BOX + k], qsy = S[3 * BOX + k];
+            const double qfx = S[4 * BOX + k], qfy = S[5 * BOX + k];
+            bool ok = rj.ok;
+            double hs = dq<FD>(ws, rj, ok), hf = dq<FD>(wf, rj, ok);
+            double jsx = dq<FD>(qsx, rj, ok), jsy = dq<FD>(qsy, rj, ok);
+            double jfx = dq<FD>(qfx, rj, ok), jfy = dq<FD>(qfy, rj, ok);
+            if (!ok) {
+                dfix<FD>(hs, ws, rj);
+                dfix<FD>(hf, wf, rj);
+                dfix<FD>(jsx, qsx, rj);
+                dfix<FD>(jsy, qsy, rj);
+                dfix<FD>(jfx, qfx, rj);
+                dfix<FD>(jfy, qfy, rj);
+            }
             const double h = hs + hf;
             const double fsld = desing_factor<FD>(hs, P.eps_h);
             const double fflu = desing_factor<FD>(hf, P.eps_h);
-            V[0 * BOX + k] = dv<FD>(S[2 * BOX + k], rj) * fsld;
-            V[1 * BOX + k] = dv<FD>(S[3 * BOX + k], rj) * fsld;
-            V[2 * BOX + k] = dv<FD>(S[4 * BOX + k], rj) * fflu;
-            V[3 * BOX + k] = dv<FD>(S[5 * BOX + k], rj) * fflu;
-            if (bx >= 1 && bx <= TX + 2 && by >= 1 && by <= TY + 2) {
-                const int gx = bx0 + bx, gy = by0 + by;
-                const double nZ = (gx < nx && gy < ny)
-                                      ? ldg(geo + G_NZ * fs + static_cast<long long>(gy) * pitch + gx)
-                                      : 1.0;
-                PJ[k] = jb * h * (nZ * h * 0.5);  // solver.cpp:182
-            }
+            V[0 * BOX + k] = jsx * fsld;
+            V[1 * BOX + k] = jsy * fsld;
+            V[2 * BOX + k] = jfx * fflu;
+            V[3 * BOX + k] = jfy * fflu;
+            PJ[k] = jb * h * (G[G_NZ * BOX + k] * h * 0.5);  // solver.cpp:182
         }
     }
     __syncthreads();
 
     // ---- Phase 2: viscous brackets on the cross neighbours of the tile --------
+    // (and the per-cell fields of this thread's Phase-3 cell, now L2-warm)
+    double gc[9];
+    double u0c[6];
+    if (p3) {
+#pragma unroll
+        for (int f = 0; f < 9; ++f) gc[f] = __ldg(geo + (G_NX + f) * fs + o3);
+        if (CORR) {
+#pragma unroll
+            for (int f = 0; f < 6; ++f) u0c[f] = A.u0[f * fs + o3];
+        }
+    }
     const Rcp r2x = mkrcp_const<FD>(P.two_dxi, P.r_two_dxi);
     const Rcp r2y = mkrcp_const<FD>(P.two_deta, P.r_two_deta);
     if (!P.adv_only) {
@@ -190,24 +254,27 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(StageArgs A) {
                 by = (r < TX) ? 1 : TY + 2;
             }
             const int k = by * W2 + bx;
-            const int gx = bx0 + bx, gy = by0 + by;
-            const bool in = gx < nx && gy < ny;
-            const long long o = static_cast<long long>(gy) * pitch + gx;
-            const double jb = JB[k];
-            const double a11 = in ? ldg(geo + G_A11 * fs + o) : 0.0;
-            const double a12 = in ? ldg(geo + G_A12 * fs + o) : 0.0;
-            const double a21 = in ? ldg(geo + G_A21 * fs + o) : 0.0;
-            const double a22 = in ? ldg(geo + G_A22 * fs + o) : 0.0;
-            Rcp rj;
-            if (FD) rj = mkrcp_const<FD>(jb, RJ[k]); else rj = mkrcp<FD>(jb);
+            const double jb = G[G_JB * BOX + k];
+            const double a11 = G[G_A11 * BOX + k], a12 = G[G_A12 * BOX + k];
+            const double a21 = G[G_A21 * BOX + k], a22 = G[G_A22 * BOX + k];
+            const Rcp rj = mkrcp_const<FD>(jb, G[G_RJB * BOX + k]);
             // solver.cpp:197-205 + physics::viscous_brackets (physics.hpp:166-174)
-            const double h = dv<FD>(S[0 * BOX + k] + S[1 * BOX + k], rj);
             const double* vxf = V + 2 * BOX;
             const double* vyf = V + 3 * BOX;
-            const double gux = dv<FD>(vxf[k + 1] - vxf[k - 1], r2x);
-            const double guy = dv<FD>(vxf[k + W2] - vxf[k - W2], r2y);
-            const double gwx = dv<FD>(vyf[k + 1] - vyf[k - 1], r2x);
-            const double gwy = dv<FD>(vyf[k + W2] - vyf[k - W2], r2y);
+            const double n0 = S[0 * BOX + k] + S[1 * BOX + k];
+            const double n1 = vxf[k + 1] - vxf[k - 1], n2 = vxf[k + W2] - vxf[k - W2];
+            const double n3 = vyf[k + 1] - vyf[k - 1], n4 = vyf[k + W2] - vyf[k - W2];
+            bool ok = rj.ok && r2x.ok && r2y.ok;
+            double h = dq<FD>(n0, rj, ok);
+            double gux = dq<FD>(n1, r2x, ok), guy = dq<FD>(n2, r2y, ok);
+            double gwx = dq<FD>(n3, r2x, ok), gwy = dq<FD>(n4, r2y, ok);
+            if (!ok) {
+                dfix<FD>(h, n0, rj);
+                dfix<FD>(gux, n1, r2x);
+                dfix<FD>(guy, n2, r2y);
+                dfix<FD>(gwx, n3, r2x);
+                dfix<FD>(gwy, n4, r2y);
+            }
             const double jh = jb * h;
             BR[0 * BOX + k] = jh * (a11 * gux + a21 * guy);
             BR[1 * BOX + k] = jh * (a12 * gwx + a22 * gwy);
@@ -217,65 +284,101 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(StageArgs A) {
     __syncthreads();
 
     // ---- Phase 3: residual + update + cap + [average] + regularize + [finite, lambda]
-    const double dt = sc->dt;
     const Rcp rdx = mkrcp_const<FD>(P.dxi, P.r_dxi);
     const Rcp rdy = mkrcp_const<FD>(P.deta, P.r_deta);
     double lam_local = 0.0;
-    for (int k = threadIdx.x; k < TX * TY; k += NT) {
-        const int tx = k % TX, ty = k / TX;
-        const int X = X0 + tx, Y = Y0 + ty;
-        if (X > nx - 4 || Y > ny - 4) continue;
+    if (p3) {
+        const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
+        const int X = p3x, Y = p3y;
         const int bk = (ty + 2) * W2 + (tx + 2);
-        const long long o = static_cast<long long>(Y) * pitch + X;
+        const double nX = gc[0], nY = gc[1];
+        const double dXx = gc[2], dYx = gc[3], dZx = gc[4], dXy = gc[5], dYy = gc[6], dZy = gc[7];
+        const double nZ = G[G_NZ * BOX + bk];
+        const Rcp rnz = mkrcp_const<FD>(nZ, gc[8]);
+        const double jb = G[G_JB * BOX + bk];
+        const Rcp rj = mkrcp_const<FD>(jb, G[G_RJB * BOX + bk]);
 
-        double rhs[6];
+        // flux divergence (solver.cpp:396-399)
+        double dx[6], dy[6], nx_[6], ny_[6];
+        bool ok = rdx.ok && rdy.ok;
 #pragma unroll
         for (int f = 0; f < 6; ++f) {
             const double* fx = FX + f * NFX + ty * (TX + 1) + tx;
             const double* fy = FY + f * NFY + ty * TX + tx;
-            rhs[f] = dv<FD>(-(fx[1] - fx[0]), rdx) + dv<FD>(-(fy[TX] - fy[0]), rdy);  // :397-398
+            nx_[f] = -(fx[1] - fx[0]);
+            ny_[f] = -(fy[TX] - fy[0]);
+            dx[f] = dq<FD>(nx_[f], rdx, ok);
+            dy[f] = dq<FD>(ny_[f], rdy, ok);
         }
-
-        const double jb = JB[bk];
-        Rcp rj;
-        if (FD) rj = mkrcp_const<FD>(jb, RJ[bk]); else rj = mkrcp<FD>(jb);
-        double nX = 0, nY = 0, nZ = 1, a11 = 0, a12 = 0, a21 = 0, a22 = 0;
-        double dXx = 0, dYx = 0, dZx = 0, dXy = 0, dYy = 0, dZy = 0;
-        if (!P.adv_only || P.cap_on || CORR) nZ = ldg(geo + G_NZ * fs + o);
-        if (!P.adv_only || P.cap_on) {
-            nX = ldg(geo + G_NX * fs + o);
-            nY = ldg(geo + G_NY * fs + o);
-            dXx = ldg(geo + G_DNX_DXI * fs + o);
-            dYx = ldg(geo + G_DNY_DXI * fs + o);
-            dZx = ldg(geo + G_DNZ_DXI * fs + o);
-            dXy = ldg(geo + G_DNX_DETA * fs + o);
-            dYy = ldg(geo + G_DNY_DETA * fs + o);
-            dZy = ldg(geo + G_DNZ_DETA * fs + o);
+        if (!ok) {
+#pragma unroll
+            for (int f = 0; f < 6; ++f) {
+                dfix<FD>(dx[f], nx_[f], rdx);
+                dfix<FD>(dy[f], ny_[f], rdy);
+            }
         }
-        const Rcp rnz = mkrcp<FD>(nZ);
+        double rhs[6];
+#pragma unroll
+        for (int f = 0; f < 6; ++f) rhs[f] = dx[f] + dy[f];
 
         if (!P.adv_only) {
-            a11 = ldg(geo + G_A11 * fs + o);
-            a12 = ldg(geo + G_A12 * fs + o);
-            a21 = ldg(geo + G_A21 * fs + o);
-            a22 = ldg(geo + G_A22 * fs + o);
+            const double a11 = G[G_A11 * BOX + bk], a12 = G[G_A12 * BOX + bk];
+            const double a21 = G[G_A21 * BOX + bk], a22 = G[G_A22 * BOX + bk];
             // solver.cpp:406-445
-            const double hs = dv<FD>(S[0 * BOX + bk], rj);
-            const double hf = dv<FD>(S[1 * BOX + bk], rj);
-            const double h = hs + hf;
-            const Rcp rh = mkrcp<FD>(h);
-            const double phi_s = h < P.h_dry ? 0.0 : dv<FD>(hs, rh);
-            const double phi_f = h < P.h_dry ? 0.0 : dv<FD>(hf, rh);
+            const double ws = S[0 * BOX + bk], wf = S[1 * BOX + bk];
+            const double gpx = PJ[bk + 1] - PJ[bk - 1], gpy = PJ[bk + W2] - PJ[bk - W2];
+            const double* bvx = BR;
+            const double* bvy = BR + BOX;
+            const double* bxy = BR + 2 * BOX;
+            const double s1 = 2.0 * (bvx[bk + 1] - bvx[bk - 1]), s2 = bxy[bk + W2] - bxy[bk - W2];
+            const double s3 = 2.0 * (bvy[bk + W2] - bvy[bk - W2]), s4 = bxy[bk + 1] - bxy[bk - 1];
             const double vsx = V[0 * BOX + bk], vsy = V[1 * BOX + bk];
             const double vfx = V[2 * BOX + bk], vfy = V[3 * BOX + bk];
-            const double kap_s = curvature_accel<FD>(vsx, vsy, nX, nY, rnz, dXx, dYx, dZx, dXy, dYy, dZy);
-            const double kap_f = curvature_accel<FD>(vfx, vfy, nX, nY, rnz, dXx, dYx, dZx, dXy, dYy, dZy);
+            const double nzs = -(nX * vsx + nY * vsy), nzf = -(nX * vfx + nY * vfy);
+            const Rcp rNR = mkrcp_const<FD>(P.N_R, P.r_NR);
+            const Rcp reNR = mkrcp_const<FD>(P.eps_NR, P.r_eps_NR);
+            bool ok2 = rj.ok && rnz.ok && r2x.ok && r2y.ok && rNR.ok && reNR.ok;
+            double hs = dq<FD>(ws, rj, ok2), hf = dq<FD>(wf, rj, ok2);
+            double vzs = dq<FD>(nzs, rnz, ok2), vzf = dq<FD>(nzf, rnz, ok2);
+            double gPx = dq<FD>(gpx, r2x, ok2), gPy = dq<FD>(gpy, r2y, ok2);
+            double v1 = dq<FD>(s1, r2x, ok2), v2 = dq<FD>(s2, r2y, ok2);
+            double v3 = dq<FD>(s3, r2y, ok2), v4 = dq<FD>(s4, r2x, ok2);
+            if (!ok2) {
+                dfix<FD>(hs, ws, rj);
+                dfix<FD>(hf, wf, rj);
+                dfix<FD>(vzs, nzs, rnz);
+                dfix<FD>(vzf, nzf, rnz);
+                dfix<FD>(gPx, gpx, r2x);
+                dfix<FD>(gPy, gpy, r2y);
+                dfix<FD>(v1, s1, r2x);
+                dfix<FD>(v2, s2, r2y);
+                dfix<FD>(v3, s3, r2y);
+                dfix<FD>(v4, s4, r2x);
+            }
+            const double h = hs + hf;
+            double phi_s = 0.0, phi_f = 0.0, hsf_h = 0.0;
+            if (!(h <= 0.0)) {
+                const Rcp rh = mkrcp<FD>(h);
+                const double hsf = hs * hf;
+                bool okh = rh.ok;
+                double q1 = dq<FD>(hs, rh, okh), q2 = dq<FD>(hf, rh, okh), q3 = dq<FD>(hsf, rh, okh);
+                if (!okh) {
+                    dfix<FD>(q1, hs, rh);
+                    dfix<FD>(q2, hf, rh);
+                    dfix<FD>(q3, hsf, rh);
+                }
+                if (!(h < P.h_dry)) {  // phi = h < h_dry ? 0 : hs / h  (solver.cpp:410-411)
+                    phi_s = q1;
+                    phi_f = q2;
+                }
+                hsf_h = q3;
+            }
+            // physics::curvature_accel (physics.hpp:47-52) with vz from tangency
+            const double kap_s = ((vsx * dXx + vsy * dYx) + vzs * dZx) * vsx + ((vsx * dXy + vsy * dYy) + vzs * dZy) * vsy;
+            const double kap_f = ((vfx * dXx + vfy * dYx) + vzf * dZx) * vfx + ((vfx * dXy + vfy * dYy) + vzf * dZy) * vfy;
             // physics::hydrostatic_terms (physics.hpp:56-69)
             const double p_b_s = smax(0.0, hs * (nZ * P.oma - P.eps_chi * kap_s));
             const double p_b_f = smax(0.0, hf * (nZ - P.eps_chi * kap_f));
-            // gradient of jb*h*p_bar_f (solver.cpp:419-420)
-            const double gPx = dv<FD>(PJ[bk + 1] - PJ[bk - 1], r2x);
-            const double gPy = dv<FD>(PJ[bk + W2] - PJ[bk - W2], r2y);
             // solid: gravity + pressure gradient + drag (physics.hpp:98-155)
             const double sn_sx = jb * p_b_s * nX, sn_sy = jb * p_b_s * nY;
             const double Avx = a11 * gPx + a21 * gPy;
@@ -284,7 +387,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(StageArgs A) {
             const double sf_sx = fsp * Avx, sf_sy = fsp * Avy;
             double sv_sx = 0.0, sv_sy = 0.0, sv_fx = 0.0, sv_fy = 0.0;
             if (!(h <= 0.0)) {
-                const double common = jb * P.C_d * dv<FD>(hs * hf, rh);
+                const double common = jb * P.C_d * hsf_h;
                 const double cx = common * (vfx - vsx);
                 const double cy = common * (vfy - vsy);
                 sv_sx = P.alpha * cx;
@@ -294,18 +397,13 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(StageArgs A) {
             }
             // fluid: gravity + friction + pressure gradient + drag + viscous
             const double sn_fx = jb * p_b_f * nX, sn_fy = jb * p_b_f * nY;
-            const double coeff = dv<FD>(jb * hf * P.theta_b, mkrcp_const<FD>(P.eps_NR, P.r_eps_NR));
+            const double coeff = dv<FD>(jb * hf * P.theta_b, reNR);
             const double sd_fx = -coeff * vfx, sd_fy = -coeff * vfy;
             const double ephf = P.eps * phi_f;
             const double sf_fx = ephf * Avx, sf_fy = ephf * Avy;
-            const double visc = dv<FD>(ephf, mkrcp_const<FD>(P.N_R, P.r_NR));
-            const double* bvx = BR;
-            const double* bvy = BR + BOX;
-            const double* bxy = BR + 2 * BOX;
-            const double svis_x = visc * (dv<FD>(2.0 * (bvx[bk + 1] - bvx[bk - 1]), r2x) +
-                                          dv<FD>(bxy[bk + W2] - bxy[bk - W2], r2y));
-            const double svis_y = visc * (dv<FD>(2.0 * (bvy[bk + W2] - bvy[bk - W2]), r2y) +
-                                          dv<FD>(bxy[bk + 1] - bxy[bk - 1], r2x));
+            const double visc = dv<FD>(ephf, rNR);
+            const double svis_x = visc * (v1 + v2);
+            const double svis_y = visc * (v3 + v4);
             rhs[2] = rhs[2] + (sn_sx + sf_sx + sv_sx);
             rhs[3] = rhs[3] + (sn_sy + sf_sy + sv_sy);
             rhs[4] = rhs[4] + (sn_fx + sd_fx + sf_fx + sv_fx + svis_x);
@@ -321,12 +419,20 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(StageArgs A) {
         if (P.cap_on) {
             const double qx = un[2], qy = un[3];
             if (!(qx == 0.0 && qy == 0.0)) {
-                const double hs = dv<FD>(un[0], rj);
+                bool okc = rj.ok;
+                double hs = dq<FD>(un[0], rj, okc);
+                double jx = dq<FD>(qx, rj, okc), jy = dq<FD>(qy, rj, okc);
+                if (!okc) {
+                    dfix<FD>(hs, un[0], rj);
+                    dfix<FD>(jx, qx, rj);
+                    dfix<FD>(jy, qy, rj);
+                }
                 if (!(hs < P.h_dry)) {
                     const double fsld = desing_factor<FD>(hs, P.eps_h);
-                    const double vsx = dv<FD>(qx, rj) * fsld;
-                    const double vsy = dv<FD>(qy, rj) * fsld;
-                    const double kap = curvature_accel<FD>(vsx, vsy, nX, nY, rnz, dXx, dYx, dZx, dXy, dYy, dZy);
+                    const double vsx = jx * fsld;
+                    const double vsy = jy * fsld;
+                    const double vz = dv<FD>(-(nX * vsx + nY * vsy), rnz);
+                    const double kap = ((vsx * dXx + vsy * dYx) + vz * dZx) * vsx + ((vsx * dXy + vsy * dYy) + vz * dZy) * vsy;
                     const double p_b_s = smax(0.0, hs * (nZ * P.oma - P.eps_chi * kap));
                     const double rate = jb * p_b_s * P.tan_d;
                     const double qnorm = sqrt(qx * qx + qy * qy);
@@ -339,30 +445,39 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(StageArgs A) {
 
         if (CORR) {  // Heun average (solver.cpp:538-541)
 #pragma unroll
-            for (int f = 0; f < 6; ++f) un[f] = 0.5 * (A.u0[f * fs + o] + un[f]);
+            for (int f = 0; f < 6; ++f) un[f] = 0.5 * (u0c[f] + un[f]);
         }
 
         // regularize (solver.cpp:139-166), solid then fluid
-#pragma unroll
-        for (int p = 0; p < 2; ++p) {
-            double w = un[p];
-            double hp = dv<FD>(w, rj);
-            if (hp < 0.0) {
-                if (hp < -1e-12) {
-                    const unsigned long long key =
-                        (static_cast<unsigned long long>(CORR ? 1 : 0) << 62) |
-                        (static_cast<unsigned long long>(Y) << 32) |
-                        (static_cast<unsigned long long>(X) << 1) | static_cast<unsigned long long>(p);
-                    atomicMin(&sc->err_key, key);
-                    break;  // the reference throws here; leave the cell as computed
-                }
-                atomicAdd(&sc->audit[5 * p + 4], -w * P.cell_area);
-                un[p] = 0.0;
-                hp = 0.0;
+        {
+            bool okr = rj.ok;
+            double hp0 = dq<FD>(un[0], rj, okr), hp1 = dq<FD>(un[1], rj, okr);
+            if (!okr) {
+                dfix<FD>(hp0, un[0], rj);
+                dfix<FD>(hp1, un[1], rj);
             }
-            if (hp < P.h_dry) {
-                un[2 + 2 * p] = 0.0;
-                un[3 + 2 * p] = 0.0;
+            double hpv[2] = {hp0, hp1};
+#pragma unroll
+            for (int p = 0; p < 2; ++p) {
+                const double w = un[p];
+                double hp = hpv[p];
+                if (hp < 0.0) {
+                    if (hp < -1e-12) {
+                        const unsigned long long key =
+                            (static_cast<unsigned long long>(CORR ? 1 : 0) << 62) |
+                            (static_cast<unsigned long long>(Y) << 32) |
+                            (static_cast<unsigned long long>(X) << 1) | static_cast<unsigned long long>(p);
+                        atomicMin(&sc->err_key, key);
+                        break;  // the reference throws here; leave the cell as computed
+                    }
+                    atomicAdd(&sc->audit[5 * p + 4], -w * P.cell_area);
+                    un[p] = 0.0;
+                    hp = 0.0;
+                }
+                if (hp < P.h_dry) {
+                    un[2 + 2 * p] = 0.0;
+                    un[3 + 2 * p] = 0.0;
+                }
             }
         }
 
@@ -379,26 +494,36 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(StageArgs A) {
                 }
             }
             // lambda of the new state for the next compute_dt (solver.cpp:560-571)
-            const double hs = dv<FD>(un[0], rj);
-            const double hf = dv<FD>(un[1], rj);
+            bool okl = rj.ok;
+            double hs = dq<FD>(un[0], rj, okl), hf = dq<FD>(un[1], rj, okl);
+            double jsx = dq<FD>(un[2], rj, okl), jsy = dq<FD>(un[3], rj, okl);
+            double jfx = dq<FD>(un[4], rj, okl), jfy = dq<FD>(un[5], rj, okl);
+            if (!okl) {
+                dfix<FD>(hs, un[0], rj);
+                dfix<FD>(hf, un[1], rj);
+                dfix<FD>(jsx, un[2], rj);
+                dfix<FD>(jsy, un[3], rj);
+                dfix<FD>(jfx, un[4], rj);
+                dfix<FD>(jfy, un[5], rj);
+            }
             const double h = hs + hf;
             if (!(h < P.h_dry)) {
                 const double fsld = desing_factor<FD>(hs, P.eps_h);
                 const double fflu = desing_factor<FD>(hf, P.eps_h);
-                const double vsx = dv<FD>(un[2], rj) * fsld, vsy = dv<FD>(un[3], rj) * fsld;
-                const double vfx = dv<FD>(un[4], rj) * fflu, vfy = dv<FD>(un[5], rj) * fflu;
+                const double vsx = jsx * fsld, vsy = jsy * fsld;
+                const double vfx = jfx * fflu, vfy = jfy * fflu;
                 const double cel = sqrt(P.eps * nZ * h);
                 const double lx = smax(fabs(vsx), fabs(vfx)) + cel;
                 const double ly = smax(fabs(vsy), fabs(vfy)) + cel;
-                lam_local = smax(lam_local, smax(lx, ly));
+                lam_local = smax(lx, ly);
             }
         }
 
 #pragma unroll
-        for (int f = 0; f < 6; ++f) A.out[f * fs + o] = un[f];
+        for (int f = 0; f < 6; ++f) A.out[f * fs + o3] = un[f];
     }
 
-    // ---- boundary mass tally of this stage (solver.cpp:352-376), edge tiles only
+    // ---- boundary mass tally of this stage (solver.cpp:352-376), ring tiles only
     const bool w_edge = X0 == 3;
     const bool e_edge = (nx - 4) >= X0 && (nx - 4) < X0 + TX;
     const bool s_edge = g.has_south && Y0 == 3;
@@ -682,9 +807,7 @@ __global__ void __launch_bounds__(NT) regularize_kernel(GridDesc g, Phys P, doub
 // ---------------------------------------------------------------------------
 // host-side launch helpers (called from tp_capi.cpp)
 // ---------------------------------------------------------------------------
-size_t stage_smem_bytes() {
-    return sizeof(double) * (6 * BOX + BOX + BOX + 4 * BOX + BOX + 3 * BOX + 6 * NFX + 6 * NFY);
-}
+size_t stage_smem_bytes() { return sizeof(double) * SM_END; }
 
 template <bool FD, bool CORR>
 static cudaError_t launch_stage_t(const StageArgs& a, cudaStream_t st) {

@@ -2,9 +2,9 @@
 // No device code here: this header is included by tp_capi.cpp.
 #pragma once
 
+#include <cuda.h>
+
 #include <cstdint>
-
-
 
 namespace tpb {
 
@@ -29,11 +29,24 @@ struct Phys {
 };
 
 
-// Geometry field order = TerrainGeometry declaration order (terrain.hpp:59-63).
-enum GeoField {
-    G_NX = 0, G_NY, G_NZ, G_JB, G_A11, G_A12, G_A21, G_A22,
-    G_DNX_DXI, G_DNY_DXI, G_DNZ_DXI, G_DNX_DETA, G_DNY_DETA, G_DNZ_DETA, G_COUNT
+// Host/API geometry order = TerrainGeometry declaration order (terrain.hpp:59-63).
+enum RefGeoField {
+    R_NX = 0, R_NY, R_NZ, R_JB, R_A11, R_A12, R_A21, R_A22,
+    R_DNX_DXI, R_DNY_DXI, R_DNZ_DXI, R_DNX_DETA, R_DNY_DETA, R_DNZ_DETA, R_COUNT
 };
+// Device geometry layout: the reference's 14 fields regrouped so that the fields
+// every stencil point needs form one contiguous TMA box (the first NGBOX), plus
+// four host-derived reciprocals RN(1/x) of the geometric divisors (the shared
+// reciprocals of the FASTDIV division, see tp_math.cuh).
+enum GeoField {
+    G_JB = 0, G_RJB, G_NZ, G_A11, G_A12, G_A21, G_A22,
+    G_RJBFX,   // RN(1 / (0.5 * (jb(i,j) + jb(i+1,j))))  xi-face jbf (solver.cpp:242)
+    G_RJBFY,   // RN(1 / (0.5 * (jb(i,j) + jb(i,j+1))))  eta-face jbf
+    G_NX, G_NY, G_DNX_DXI, G_DNY_DXI, G_DNZ_DXI, G_DNX_DETA, G_DNY_DETA, G_DNZ_DETA,
+    G_RNZ,     // RN(1 / nZ)
+    G_COUNT
+};
+constexpr int NGBOX = 9;   // G_JB .. G_RJBFY staged per tile box by TMA
 // State field order = MixtureState::fields() (state.hpp:29).
 enum StateField { S_WS = 0, S_WF, S_QSX, S_QSY, S_QFX, S_QFY, S_COUNT };
 
@@ -84,6 +97,8 @@ constexpr int NFX = (TX + 1) * TY;
 constexpr int NFY = TX * (TY + 1);
 
 struct StageArgs {
+    CUtensorMap tm_s;                // TMA descriptor of the stage input state (6 fields)
+    CUtensorMap tm_g;                // TMA descriptor of the NGBOX box geometry fields
     GridDesc g;
     Phys ph;
     const double* __restrict__ s;    // stage input state (6 fields, ghosts filled)
