@@ -85,6 +85,87 @@ __device__ __forceinline__ void prefetch_l2(const void* p) {
     asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 
+// regularize + [check_finite + lambda] + store of one updated cell: the tail of
+// advance_step's stages (solver.cpp:139-166, :482-494, :556-573).
+template <bool FD, bool CORR>
+__device__ __forceinline__ void cell_epilogue(double (&un)[6], const Rcp& rj, double nZ, int X, int Y,
+                                              const Phys& P, DevScalars* sc, double& lam_local,
+                                              double* out, long long fs, long long o3) {
+    // regularize (solver.cpp:139-166), solid then fluid
+    {
+        bool okr = rj.ok;
+        double hp0 = dq<FD>(un[0], rj, okr), hp1 = dq<FD>(un[1], rj, okr);
+        if (!okr) {
+            dfix<FD>(hp0, un[0], rj);
+            dfix<FD>(hp1, un[1], rj);
+        }
+        double hpv[2] = {hp0, hp1};
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+            const double w = un[p];
+            double hp = hpv[p];
+            if (hp < 0.0) {
+                if (hp < -1e-12) {
+                    const unsigned long long key =
+                        (static_cast<unsigned long long>(CORR ? 1 : 0) << 62) |
+                        (static_cast<unsigned long long>(Y) << 32) |
+                        (static_cast<unsigned long long>(X) << 1) | static_cast<unsigned long long>(p);
+                    atomicMin(&sc->err_key, key);
+                    break;  // the reference throws here; leave the cell as computed
+                }
+                atomicAdd(&sc->audit[5 * p + 4], -w * P.cell_area);
+                un[p] = 0.0;
+                hp = 0.0;
+            }
+            if (hp < P.h_dry) {
+                un[2 + 2 * p] = 0.0;
+                un[3 + 2 * p] = 0.0;
+            }
+        }
+    }
+
+    if (CORR) {
+        // check_finite (solver.cpp:482-494)
+#pragma unroll
+        for (int f = 0; f < 6; ++f) {
+            if (!isfinite(un[f])) {
+                const unsigned long long key = (2ull << 62) |
+                                               (static_cast<unsigned long long>(f) << 56) |
+                                               (static_cast<unsigned long long>(Y) << 28) |
+                                               static_cast<unsigned long long>(X);
+                atomicMin(&sc->err_key, key);
+            }
+        }
+        // lambda of the new state for the next compute_dt (solver.cpp:560-571)
+        bool okl = rj.ok;
+        double hs = dq<FD>(un[0], rj, okl), hf = dq<FD>(un[1], rj, okl);
+        double jsx = dq<FD>(un[2], rj, okl), jsy = dq<FD>(un[3], rj, okl);
+        double jfx = dq<FD>(un[4], rj, okl), jfy = dq<FD>(un[5], rj, okl);
+        if (!okl) {
+            dfix<FD>(hs, un[0], rj);
+            dfix<FD>(hf, un[1], rj);
+            dfix<FD>(jsx, un[2], rj);
+            dfix<FD>(jsy, un[3], rj);
+            dfix<FD>(jfx, un[4], rj);
+            dfix<FD>(jfy, un[5], rj);
+        }
+        const double h = hs + hf;
+        if (!(h < P.h_dry)) {
+            const double fsld = desing_factor<FD>(hs, P.eps_h);
+            const double fflu = desing_factor<FD>(hf, P.eps_h);
+            const double vsx = jsx * fsld, vsy = jsy * fsld;
+            const double vfx = jfx * fflu, vfy = jfy * fflu;
+            const double cel = sqrt(P.eps * nZ * h);
+            const double lx = smax(fabs(vsx), fabs(vfx)) + cel;
+            const double ly = smax(fabs(vsy), fabs(vfy)) + cel;
+            lam_local = smax(lam_local, smax(lx, ly));
+        }
+    }
+
+#pragma unroll
+    for (int f = 0; f < 6; ++f) out[f * fs + o3] = un[f];
+}
+
 // shared-memory carve-up of the stage kernel (doubles)
 constexpr int SM_S = 0;                                   // [6][BOX] state box (TMA)
 constexpr int SM_G = ((6 * BOX * 8 + 127) / 128) * 16;    // [NGBOX][BOX] geometry box (TMA), 128B aligned
@@ -117,27 +198,37 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
     const GridDesc& g = A.g;
     const Phys& P = A.ph;
     const int nx = g.nx, ny = g.ny, pitch = g.pitch;
-    const int X0 = 3 + blockIdx.x * TX;
-    const int Y0 = 3 + blockIdx.y * TY;
-    const int bx0 = X0 - 2, by0 = Y0 - 2;
+    const double* __restrict__ geo = A.geo;
+    const long long fs = g.fs;
+    const int ntiles = A.ntx * A.nty;
+    const double dt = sc->dt;
 
-    // ---- Phase 0: one TMA transaction stages the radius-2 box of the 6 state
-    // fields and the 9 stencil geometry fields (OOB -> zeros, edge tiles only).
+    // Persistent tiles: block b walks tiles b, b+G, b+2G, ... (row-major, so the
+    // tiles in flight at any time are neighbours and share halos in L2).  The
+    // next tile's TMA is issued as soon as the current tile's staged boxes are
+    // dead (after Phase 2), so it lands while Phase 3 computes.
+    int tile = blockIdx.x;
     if (threadIdx.x == 0) {
         mbar_init(&bar, 1);
-        mbar_expect_tx(&bar, kTmaBytes);
-        // x coordinate + 1: the leading pad column of the device layout (tp_capi.cpp)
-        tma_load_3d(S, &A.tm_s, bx0 + 1, by0, 0, &bar);
-        tma_load_3d(sm + SM_G, &A.tm_g, bx0 + 1, by0, 0, &bar);
+        if (tile < ntiles) {
+            const int bx0 = 1 + (tile % A.ntx) * TX, by0 = 1 + (tile / A.ntx) * TY;
+            mbar_expect_tx(&bar, kTmaBytes);
+            // x coordinate + 1: the leading pad column of the device layout (tp_capi.cpp)
+            tma_load_3d(S, &A.tm_s, bx0 + 1, by0, 0, &bar);
+            tma_load_3d(sm + SM_G, &A.tm_g, bx0 + 1, by0, 0, &bar);
+        }
     }
-    const double dt = sc->dt;
-    // the Phase-3 cell of this thread: warm L2 with its per-cell geometry (and u^n)
+    __syncthreads();  // barrier init visible to all threads
+    double lam_local = 0.0;
+    for (unsigned iter = 0; tile < ntiles; tile += gridDim.x, ++iter) {
+    const int tix = tile % A.ntx, tiy = tile / A.ntx;
+    const int X0 = 3 + tix * TX;
+    const int Y0 = 3 + tiy * TY;
+    // the Phase-3 cell of this thread
     const int p3x = X0 + (threadIdx.x % TX), p3y = Y0 + (threadIdx.x / TX);
     const bool p3 = threadIdx.x < TX * TY && p3x <= nx - 4 && p3y <= ny - 4;
     const long long o3 = static_cast<long long>(p3y) * pitch + p3x;
-    const double* __restrict__ geo = A.geo;
-    const long long fs = g.fs;
-    if (p3) {
+    if (iter == 0 && p3) {  // later tiles were prefetched during the previous Phase 3
 #pragma unroll
         for (int f = G_NX; f <= G_RNZ; ++f) prefetch_l2(geo + f * fs + o3);
         if (CORR) {
@@ -145,8 +236,64 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
             for (int f = 0; f < 6; ++f) prefetch_l2(A.u0 + f * fs + o3);
         }
     }
-    __syncthreads();  // barrier init visible
-    mbar_wait(&bar, 0);
+    // next tile's boxes into S/G (call only once they are dead) + L2 warm-up of
+    // its per-cell fields for Phase 3
+    auto issue_next = [&]() {
+            const int nt = tile + gridDim.x;
+            if (nt < ntiles) {
+                const int bx0n = 1 + (nt % A.ntx) * TX, by0n = 1 + (nt / A.ntx) * TY;
+                if (threadIdx.x == 0) {
+                    mbar_expect_tx(&bar, kTmaBytes);
+                    tma_load_3d(S, &A.tm_s, bx0n + 1, by0n, 0, &bar);
+                    tma_load_3d(sm + SM_G, &A.tm_g, bx0n + 1, by0n, 0, &bar);
+                }
+                const int qx = bx0n + 2 + (threadIdx.x % TX), qy = by0n + 2 + (threadIdx.x / TX);
+                if (threadIdx.x < TX * TY && qx <= nx - 4 && qy <= ny - 4) {
+                    const long long oq = static_cast<long long>(qy) * pitch + qx;
+    #pragma unroll
+                    for (int f = G_NX; f <= G_RNZ; ++f) prefetch_l2(geo + f * fs + oq);
+                    if (CORR) {
+    #pragma unroll
+                        for (int f = 0; f < 6; ++f) prefetch_l2(A.u0 + f * fs + oq);
+                    }
+                }
+            }
+    };
+    mbar_wait(&bar, iter & 1u);
+
+    // ---- dry-tile fast path.  If the whole radius-2 state box is +0.0 the stage
+    // is a bitwise no-op on the tile (every flux is the dry-face 0.0, every source
+    // and divergence term a signed zero that cancels to +0.0, regularize keeps
+    // +0.0; traced term by term in DESIGN.md §3).  The predictor then stores
+    // +0.0; the corrector still averages with u^n (un = +0.0 before the average).
+    {
+        unsigned long long acc = 0ull;
+        for (int k = threadIdx.x; k < 6 * BOX; k += NT)
+            acc |= static_cast<unsigned long long>(__double_as_longlong(S[k]));
+        const int bk0 = (threadIdx.x / TX + 2) * W2 + (threadIdx.x % TX + 2);
+        const double jb0 = p3 ? G[G_JB * BOX + bk0] : 1.0;
+        const double rjb0 = p3 ? G[G_RJB * BOX + bk0] : 1.0;
+        const double nz0 = p3 ? G[G_NZ * BOX + bk0] : 1.0;
+        if (!__syncthreads_or(acc != 0ull)) {
+            issue_next();
+            if (p3) {
+                if (!CORR) {
+#pragma unroll
+                    for (int f = 0; f < 6; ++f) A.out[f * fs + o3] = 0.0;
+                } else {
+                    double un[6];
+#pragma unroll
+                    for (int f = 0; f < 6; ++f) un[f] = 0.5 * (A.u0[f * fs + o3] + 0.0);
+                    const Rcp rj0 = mkrcp_const<FD>(jb0, rjb0);
+                    cell_epilogue<FD, CORR>(un, rj0, nz0, p3x, p3y, P, sc, lam_local, A.out, fs, o3);
+                }
+            }
+            if ((tix == 0 || tix == A.ntx - 1 || tiy == 0 || tiy == A.nty - 1) && threadIdx.x < 4)
+                A.tally[4ll * tile + threadIdx.x] = 0.0;
+            continue;
+        }
+    }
+
 
     // ---- Phase 1: xi faces, eta faces, cell fields -----------------------------
     constexpr int NXP = ((NFX + 31) / 32) * 32;  // face lists padded to warp multiples
@@ -281,22 +428,38 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
             BR[2 * BOX + k] = jh * ((a12 * gux + a22 * guy) + (a11 * gwx + a21 * gwy));
         }
     }
+    // this thread's Phase-3 cell out of the staged boxes (they are recycled below)
+    double sc6[6], gjb = 1.0, grjb = 1.0, gnz = 1.0, ga11 = 0.0, ga12 = 0.0, ga21 = 0.0, ga22 = 0.0;
+    {
+        const int bk = (threadIdx.x / TX + 2) * W2 + (threadIdx.x % TX + 2);
+        if (p3) {
+#pragma unroll
+            for (int f = 0; f < 6; ++f) sc6[f] = S[f * BOX + bk];
+            gjb = G[G_JB * BOX + bk];
+            grjb = G[G_RJB * BOX + bk];
+            gnz = G[G_NZ * BOX + bk];
+            ga11 = G[G_A11 * BOX + bk];
+            ga12 = G[G_A12 * BOX + bk];
+            ga21 = G[G_A21 * BOX + bk];
+            ga22 = G[G_A22 * BOX + bk];
+        }
+    }
     __syncthreads();
+    issue_next();
 
     // ---- Phase 3: residual + update + cap + [average] + regularize + [finite, lambda]
     const Rcp rdx = mkrcp_const<FD>(P.dxi, P.r_dxi);
     const Rcp rdy = mkrcp_const<FD>(P.deta, P.r_deta);
-    double lam_local = 0.0;
     if (p3) {
         const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
         const int X = p3x, Y = p3y;
         const int bk = (ty + 2) * W2 + (tx + 2);
         const double nX = gc[0], nY = gc[1];
         const double dXx = gc[2], dYx = gc[3], dZx = gc[4], dXy = gc[5], dYy = gc[6], dZy = gc[7];
-        const double nZ = G[G_NZ * BOX + bk];
+        const double nZ = gnz;
         const Rcp rnz = mkrcp_const<FD>(nZ, gc[8]);
-        const double jb = G[G_JB * BOX + bk];
-        const Rcp rj = mkrcp_const<FD>(jb, G[G_RJB * BOX + bk]);
+        const double jb = gjb;
+        const Rcp rj = mkrcp_const<FD>(jb, grjb);
 
         // flux divergence (solver.cpp:396-399)
         double dx[6], dy[6], nx_[6], ny_[6];
@@ -322,10 +485,9 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
         for (int f = 0; f < 6; ++f) rhs[f] = dx[f] + dy[f];
 
         if (!P.adv_only) {
-            const double a11 = G[G_A11 * BOX + bk], a12 = G[G_A12 * BOX + bk];
-            const double a21 = G[G_A21 * BOX + bk], a22 = G[G_A22 * BOX + bk];
+            const double a11 = ga11, a12 = ga12, a21 = ga21, a22 = ga22;
             // solver.cpp:406-445
-            const double ws = S[0 * BOX + bk], wf = S[1 * BOX + bk];
+            const double ws = sc6[0], wf = sc6[1];
             const double gpx = PJ[bk + 1] - PJ[bk - 1], gpy = PJ[bk + W2] - PJ[bk - W2];
             const double* bvx = BR;
             const double* bvy = BR + BOX;
@@ -413,7 +575,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
         // stage update: predictor u = u0 + dt*R (:518), corrector u += dt*R (:531)
         double un[6];
 #pragma unroll
-        for (int f = 0; f < 6; ++f) un[f] = S[f * BOX + bk] + dt * rhs[f];
+        for (int f = 0; f < 6; ++f) un[f] = sc6[f] + dt * rhs[f];
 
         // Coulomb cap (solver.cpp:458-479) on the updated state
         if (P.cap_on) {
@@ -448,79 +610,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
             for (int f = 0; f < 6; ++f) un[f] = 0.5 * (u0c[f] + un[f]);
         }
 
-        // regularize (solver.cpp:139-166), solid then fluid
-        {
-            bool okr = rj.ok;
-            double hp0 = dq<FD>(un[0], rj, okr), hp1 = dq<FD>(un[1], rj, okr);
-            if (!okr) {
-                dfix<FD>(hp0, un[0], rj);
-                dfix<FD>(hp1, un[1], rj);
-            }
-            double hpv[2] = {hp0, hp1};
-#pragma unroll
-            for (int p = 0; p < 2; ++p) {
-                const double w = un[p];
-                double hp = hpv[p];
-                if (hp < 0.0) {
-                    if (hp < -1e-12) {
-                        const unsigned long long key =
-                            (static_cast<unsigned long long>(CORR ? 1 : 0) << 62) |
-                            (static_cast<unsigned long long>(Y) << 32) |
-                            (static_cast<unsigned long long>(X) << 1) | static_cast<unsigned long long>(p);
-                        atomicMin(&sc->err_key, key);
-                        break;  // the reference throws here; leave the cell as computed
-                    }
-                    atomicAdd(&sc->audit[5 * p + 4], -w * P.cell_area);
-                    un[p] = 0.0;
-                    hp = 0.0;
-                }
-                if (hp < P.h_dry) {
-                    un[2 + 2 * p] = 0.0;
-                    un[3 + 2 * p] = 0.0;
-                }
-            }
-        }
-
-        if (CORR) {
-            // check_finite (solver.cpp:482-494)
-#pragma unroll
-            for (int f = 0; f < 6; ++f) {
-                if (!isfinite(un[f])) {
-                    const unsigned long long key = (2ull << 62) |
-                                                   (static_cast<unsigned long long>(f) << 56) |
-                                                   (static_cast<unsigned long long>(Y) << 28) |
-                                                   static_cast<unsigned long long>(X);
-                    atomicMin(&sc->err_key, key);
-                }
-            }
-            // lambda of the new state for the next compute_dt (solver.cpp:560-571)
-            bool okl = rj.ok;
-            double hs = dq<FD>(un[0], rj, okl), hf = dq<FD>(un[1], rj, okl);
-            double jsx = dq<FD>(un[2], rj, okl), jsy = dq<FD>(un[3], rj, okl);
-            double jfx = dq<FD>(un[4], rj, okl), jfy = dq<FD>(un[5], rj, okl);
-            if (!okl) {
-                dfix<FD>(hs, un[0], rj);
-                dfix<FD>(hf, un[1], rj);
-                dfix<FD>(jsx, un[2], rj);
-                dfix<FD>(jsy, un[3], rj);
-                dfix<FD>(jfx, un[4], rj);
-                dfix<FD>(jfy, un[5], rj);
-            }
-            const double h = hs + hf;
-            if (!(h < P.h_dry)) {
-                const double fsld = desing_factor<FD>(hs, P.eps_h);
-                const double fflu = desing_factor<FD>(hf, P.eps_h);
-                const double vsx = jsx * fsld, vsy = jsy * fsld;
-                const double vfx = jfx * fflu, vfy = jfy * fflu;
-                const double cel = sqrt(P.eps * nZ * h);
-                const double lx = smax(fabs(vsx), fabs(vfx)) + cel;
-                const double ly = smax(fabs(vsy), fabs(vfy)) + cel;
-                lam_local = smax(lx, ly);
-            }
-        }
-
-#pragma unroll
-        for (int f = 0; f < 6; ++f) A.out[f * fs + o3] = un[f];
+        cell_epilogue<FD, CORR>(un, rj, nZ, X, Y, P, sc, lam_local, A.out, fs, o3);
     }
 
     // ---- boundary mass tally of this stage (solver.cpp:352-376), ring tiles only
@@ -528,8 +618,8 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
     const bool e_edge = (nx - 4) >= X0 && (nx - 4) < X0 + TX;
     const bool s_edge = g.has_south && Y0 == 3;
     const bool n_edge = g.has_north && (ny - 4) >= Y0 && (ny - 4) < Y0 + TY;
-    const bool ring = blockIdx.x == 0 || blockIdx.x == A.ntx - 1 || blockIdx.y == 0 ||
-                      blockIdx.y == A.nty - 1;  // every ring tile writes its slot (zeros if no edge)
+    const bool ring = tix == 0 || tix == A.ntx - 1 || tiy == 0 ||
+                      tiy == A.nty - 1;  // every ring tile writes its slot (zeros if no edge)
     if (ring && threadIdx.x < 2) {
         const int p = threadIdx.x;
         const double wdt = dt * 0.5;  // weight_dt = dt / 2.0 (solver.cpp:512, :526)
@@ -548,10 +638,12 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
             if (s_edge) add(-FY[p * NFY + 0 * TX + tx] * P.dxi * wdt);
             if (n_edge) add(FY[p * NFY + fyN * TX + tx] * P.dxi * wdt);
         }
-        double* t = A.tally + 4ll * (blockIdx.y * A.ntx + blockIdx.x);
+        double* t = A.tally + 4ll * tile;
         t[2 * p + 0] = in;
         t[2 * p + 1] = outf;
     }
+    __syncthreads();  // FX/FY/V/PJ/BR are rewritten by the next tile
+    }  // tile loop
 
     if (CORR) lam_block_max(lam_local, sc);
 }
@@ -809,9 +901,11 @@ __global__ void __launch_bounds__(NT) regularize_kernel(GridDesc g, Phys P, doub
 // ---------------------------------------------------------------------------
 size_t stage_smem_bytes() { return sizeof(double) * SM_END; }
 
+static int g_num_sms = 148;
 template <bool FD, bool CORR>
 static cudaError_t launch_stage_t(const StageArgs& a, cudaStream_t st) {
-    dim3 grid(a.ntx, a.nty);
+    const int ntiles = a.ntx * a.nty;
+    dim3 grid(ntiles < 2 * g_num_sms ? ntiles : 2 * g_num_sms);
     stage_kernel<FD, CORR><<<grid, NT, stage_smem_bytes(), st>>>(a);
     return cudaGetLastError();
 }
@@ -866,6 +960,9 @@ namespace tpb {
 cudaError_t init_kernels() {
     const int smem = static_cast<int>(stage_smem_bytes());
     cudaError_t e;
+    int dev = 0;
+    if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+    if ((e = cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
     if ((e = cudaFuncSetAttribute(stage_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) != cudaSuccess) return e;
     if ((e = cudaFuncSetAttribute(stage_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) != cudaSuccess) return e;
     if ((e = cudaFuncSetAttribute(stage_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) != cudaSuccess) return e;

@@ -128,3 +128,31 @@ def test_negative_thickness_error_matches(gpu, oracle_kind):
     with pytest.raises(NumericsError) as eg:
         sim.regularize()
     assert str(eg.value) == str(er.value)
+
+
+@pytest.mark.parametrize("name", ["c2", "wet", "c4"])
+def test_trajectory_other_terrains(gpu, oracle_kind, name):
+    """valley (mostly dry: exercises the dry-tile fast path), fully wet valley, seeded terrain."""
+    sc = {"c2": lambda: scenarios.c2_valley(160, 144), "wet": lambda: scenarios.wet_valley(128, 112),
+          "c4": lambda: scenarios.c4_terrain(120, 90)}[name]()
+    ref, sim = _pair(sc, oracle_kind)
+    tr, dts_r, _ = ref.steps(0.0, 1.0e9, 60, t_end=1.0e9)
+    tg, dts_g, _ = sim.steps(0.0, 1.0e9, 60, t_end=1.0e9, record_dts=True)
+    assert_bitwise(dts_g, dts_r, "dt sequence")
+    assert tg == tr
+    assert_bitwise(sim.state(), ref.state(), f"{name} state after 60 steps")
+
+
+def test_signed_zero_state(gpu, oracle_kind):
+    """-0.0 entries in dry cells must not take the all-(+0.0) dry-tile shortcut."""
+    sc = scenarios.c1_hill(64)
+    ref, sim = _pair(sc, oracle_kind)
+    s = ref.state()
+    s[2:, 3:20, 3:20] = -0.0
+    s[0, 5, 5] = -0.0
+    ref.set_state(s)
+    sim.set_state(s)
+    tr, dts_r, _ = ref.steps(0.0, 1.0e9, 20, t_end=1.0e9)
+    tg, dts_g, _ = sim.steps(0.0, 1.0e9, 20, t_end=1.0e9, record_dts=True)
+    assert_bitwise(dts_g, dts_r, "dt sequence")
+    assert_bitwise(sim.state(), ref.state(), "state with signed zeros")
