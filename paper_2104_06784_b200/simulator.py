@@ -184,6 +184,10 @@ class Simulator:
                                     C.byref(hit), _dp(dts) if record_dts else None))
         return tt.value, (dts[: n.value].copy() if record_dts else n.value), bool(hit.value)
 
+    def set_stream(self, cuda_stream_handle: int) -> None:
+        """Launch on an external CUDA stream (e.g. torch.cuda.Stream().cuda_stream)."""
+        self._check(self.L.tp_set_stream(self.h, C.c_void_p(cuda_stream_handle)))
+
     def kernel_launches(self) -> int:
         return int(self.L.tp_kernel_launches(self.h))
 
