@@ -232,6 +232,111 @@ class OracleSim:
         return out
 
 
+class OracleSlab:
+    """A row slab of the C restatement with the split-step interface of
+    paper_2104_06784_b200.distributed.CudaSlab (tests: gloo / in-process runs)."""
+
+    def __init__(self, scenario, rows, lanes: int = 0):
+        import torch
+        lib = _lib("port")
+        L = lib
+        vp, dp, ip = C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_int)
+        for name, res, args in [
+            ("orc_create_slab", C.c_int, [C.POINTER(_Params), C.c_int, C.c_int, C.c_double, C.c_double,
+                                          C.c_double, dp, C.c_int, C.c_int, C.POINTER(vp)]),
+            ("orc_halo_doubles", C.c_long, [vp]), ("orc_halo_pack", None, [vp, C.c_int, C.c_int, dp]),
+            ("orc_halo_unpack", None, [vp, C.c_int, C.c_int, dp]),
+            ("orc_step_begin", None, [vp, C.c_double, C.c_double, C.c_double]), ("orc_bc", None, [vp, C.c_int]),
+            ("orc_lambda_local", C.c_double, [vp]), ("orc_dt_from", None, [vp, C.c_double]),
+            ("orc_stage", C.c_int, [vp, C.c_int]), ("orc_step_end", C.c_int, [vp, dp, ip, dp])]:
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        self.L = L
+        cfg = scenario.config
+        p = _Params(cfg.params.delta_b, cfg.params.C_d, cfg.params.N_R, cfg.params.theta_b,
+                    cfg.params.phi_s0, cfg.params.alpha_rho, cfg.params.chi,
+                    cfg.scaling.L, cfg.scaling.H, cfg.scaling.g,
+                    cfg.t_end, cfg.dt_out, cfg.cfl, cfg.h_dry, cfg.eps_h, 1 if cfg.inflow else 0, lanes)
+        z = np.ascontiguousarray(scenario.z, dtype=np.float64)
+        h = C.c_void_p()
+        self.row0, self.row1 = rows
+        rc = L.orc_create_slab(C.byref(p), scenario.ncols, scenario.nrows, scenario.cellsize, 0.0, 0.0,
+                               _dp(z), self.row0, self.row1, C.byref(h))
+        self.h = h
+        if rc:
+            raise OracleError(rc, L.f["last_error"](h).decode())
+        if scenario.h0 is not None:
+            self._ck(L.f["set_initial_thickness"](h, _dp(np.ascontiguousarray(scenario.h0))))
+        if scenario.hydrograph is not None:
+            hg = scenario.hydrograph
+            ci = np.array([c[0] for c in hg.cells], dtype=np.int32)
+            cj = np.array([c[1] for c in hg.cells], dtype=np.int32)
+            sd = "".join(c[2] for c in hg.cells).encode()
+            smp = np.array(hg.samples, dtype=np.float64).reshape(-1, 4)
+            cols = [np.ascontiguousarray(smp[:, k]) for k in range(4)]
+            self._ck(L.f["set_hydrograph"](h, len(ci), ci.ctypes.data_as(ip), cj.ctypes.data_as(ip), sd,
+                                           len(smp), *[_dp(c) for c in cols]))
+        n = int(L.orc_halo_doubles(h))
+        self.send = [torch.zeros(n, dtype=torch.float64), torch.zeros(n, dtype=torch.float64)]
+        self.recv = [torch.zeros(n, dtype=torch.float64), torch.zeros(n, dtype=torch.float64)]
+        nx, ny, dxi, deta = C.c_int(), C.c_int(), C.c_double(), C.c_double()
+        L.f["dims"](h, C.byref(nx), C.byref(ny), C.byref(dxi), C.byref(deta))
+        self.nx, self.ny = nx.value, ny.value
+
+    def _ck(self, rc):
+        if rc:
+            raise OracleError(rc, self.L.f["last_error"](self.h).decode())
+
+    @staticmethod
+    def _tp(t):
+        return C.cast(t.data_ptr(), C.POINTER(C.c_double))
+
+    def pack(self, buf, side):
+        self.L.orc_halo_pack(self.h, buf, side, self._tp(self.send[side]))
+        return self.send[side]
+
+    def unpack(self, buf, side, src=None):
+        src = self.recv[side] if src is None else src
+        self.L.orc_halo_unpack(self.h, buf, side, self._tp(src.contiguous()))
+
+    def step_begin(self, t, t_next, t_end):
+        self.L.orc_step_begin(self.h, t, t_next, t_end)
+
+    def bc(self, buf):
+        self.L.orc_bc(self.h, buf)
+
+    def lambda_local(self):
+        return float(self.L.orc_lambda_local(self.h))
+
+    def dt_from(self, lam):
+        self.L.orc_dt_from(self.h, float(lam))
+
+    def stage(self, corrector):
+        self._ck(self.L.orc_stage(self.h, corrector))
+
+    def step_end(self):
+        t, hit, dt = C.c_double(), C.c_int(), C.c_double()
+        self._ck(self.L.orc_step_end(self.h, C.byref(t), C.byref(hit), C.byref(dt)))
+        return t.value, bool(hit.value), dt.value
+
+    def state(self):
+        out = np.empty((6, self.ny, self.nx))
+        self.L.f["get_state"](self.h, _dp(out))
+        return out
+
+    def audit(self):
+        a = np.empty(10)
+        self.L.f["get_audit"](self.h, _dp(a))
+        return a
+
+    def __del__(self):
+        try:
+            self.L.f["destroy"](self.h)
+        except Exception:
+            pass
+
+
 def reduce_max(values: np.ndarray, lanes: int = 0, kind: str = "ref") -> float:
     v = np.ascontiguousarray(values, dtype=np.float64)
     out = C.c_double()

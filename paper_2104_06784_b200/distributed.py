@@ -1,0 +1,282 @@
+"""Row-block (slab) decomposition of the time-stepping core across devices.
+
+SURVEY.md §8(e): the padded grid is split into contiguous row blocks (j is the
+slow index, field.hpp:23).  Each slab owns its rows plus two halo rows per side
+and exchanges them exactly where the reference refills ghosts:
+
+  1. after apply_boundaries(u, t)        (solver.cpp:639)  — rows of u^n
+  2. after apply_boundaries(u*, t + dt)  (solver.cpp:523)  — rows of u*
+
+plus one all-reduce(MAX) of the local wave-speed bound per step, which is exact
+and partition independent, so dt and every state value are bitwise those of the
+single-device run (tests/test_distributed_*.py check that).  Halo rows are
+exchanged at full padded width after the owner's W/E ghost fill, which keeps
+the reference's corner semantics; inflow cells are applied by the owning slab.
+
+Slab backends (same method set):
+  * CudaSlab — one tp_create_slab context (include/tpflow_b200.h) on one GPU,
+    buffers are CUDA tensors; halos move with NCCL send/recv (TorchComm) or
+    device copies (LocalComm, several slabs in one process).
+  * oracle.oracle.OracleSlab — the CPU checker's slab (tests only, gloo).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+
+def decompose(nrows: int, parts: int) -> List[tuple]:
+    """Balanced contiguous row blocks [row0, row1) (each >= 2 rows)."""
+    if parts < 1 or nrows < 2 * parts:
+        raise ValueError(f"cannot split {nrows} rows into {parts} slabs of >= 2 rows")
+    base, extra = divmod(nrows, parts)
+    out, r = [], 0
+    for k in range(parts):
+        n = base + (1 if k < extra else 0)
+        out.append((r, r + n))
+        r += n
+    return out
+
+
+class CudaSlab:
+    """One slab on one GPU, driven through the C ABI's split-step entry points."""
+
+    def __init__(self, scenario, rows: Sequence[int], device: int = 0, stream=None, fastdiv: bool = True):
+        import torch
+        from .simulator import Simulator
+        self.torch = torch
+        self.device = device
+        self.sim = Simulator.from_scenario(scenario, device=device, rows=tuple(rows), fastdiv=fastdiv)
+        self.L, self.h = self.sim.L, self.sim.h
+        self.stream = stream if stream is not None else torch.cuda.Stream(device=device)
+        self.sim.set_stream(self.stream.cuda_stream)
+        n = int(self.L.tp_halo_bytes(self.h)) // 8
+        mk = lambda: torch.empty(n, dtype=torch.float64, device=f"cuda:{device}")  # noqa: E731
+        self.send = [mk(), mk()]
+        self.recv = [mk(), mk()]
+        self.lam = torch.zeros(1, dtype=torch.float64, device=f"cuda:{device}")
+        self.row0, self.row1 = rows
+
+    def _ptr(self, t):
+        return C.c_void_p(t.data_ptr())
+
+    def pack(self, buf: int, side: int):
+        self.sim._check(self.L.tp_halo_pack(self.h, buf, side, self._ptr(self.send[side])))
+        return self.send[side]
+
+    def unpack(self, buf: int, side: int, src=None):
+        src = self.recv[side] if src is None else src
+        self.sim._check(self.L.tp_halo_unpack(self.h, buf, side, self._ptr(src)))
+
+    def step_begin(self, t: float, t_next: float, t_end: float):
+        self.sim._check(self.L.tp_step_begin(self.h, t, t_next, t_end))
+
+    def bc(self, buf: int):
+        self.sim._check(self.L.tp_bc(self.h, buf))
+
+    def lambda_local(self):
+        self.sim._check(self.L.tp_lambda_local(self.h, self._ptr(self.lam)))
+        return self.lam
+
+    def dt_from(self, lam):
+        self.sim._check(self.L.tp_dt_from(self.h, self._ptr(lam)))
+
+    def stage(self, corrector: int):
+        self.sim._check(self.L.tp_stage(self.h, corrector))
+
+    def step_end(self):
+        t, hit, dt = C.c_double(), C.c_int(), C.c_double()
+        self.sim._check(self.L.tp_step_end(self.h, C.byref(t), C.byref(hit), C.byref(dt)))
+        return t.value, bool(hit.value), dt.value
+
+    def state(self) -> np.ndarray:
+        return self.sim.state()
+
+    def audit(self) -> np.ndarray:
+        return self.sim.audit_array()
+
+    def synchronize(self):
+        self.stream.synchronize()
+
+
+class LocalComm:
+    """All slabs live in this process (e.g. several contexts on one GPU)."""
+
+    def exchange(self, slabs, buf: int):
+        for lo, hi in zip(slabs[:-1], slabs[1:]):
+            lo_n = lo.pack(buf, 1)       # lo's top interior rows -> hi's south halo
+            hi_s = hi.pack(buf, 0)       # hi's bottom interior rows -> lo's north halo
+            _sync_between(lo, hi)
+            _sync_between(hi, lo)
+            hi.unpack(buf, 0, lo_n)
+            lo.unpack(buf, 1, hi_s)
+            _sync_between(lo, hi)
+            _sync_between(hi, lo)
+
+    def allreduce_max(self, slabs, lams):
+        import torch
+        if isinstance(lams[0], torch.Tensor):
+            m = lams[0].clone()
+            for x in lams[1:]:
+                m = torch.maximum(m, x.to(m.device))
+            return [m.to(x.device) for x in lams]
+        m = max(lams)
+        return [m] * len(lams)
+
+    def allreduce_sum(self, arrs):
+        s = np.sum(np.stack(arrs), axis=0)
+        return s
+
+
+def _sync_between(a, b):
+    """Order b's stream after a's (device slabs); no-op on the CPU oracle."""
+    sa, sb = getattr(a, "stream", None), getattr(b, "stream", None)
+    if sa is not None and sb is not None and sa is not sb:
+        ev = a.torch.cuda.Event()
+        ev.record(sa)
+        sb.wait_event(ev)
+
+
+class TorchComm:
+    """One slab per rank; torch.distributed (NCCL on GPUs, gloo on CPU)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+
+    def exchange(self, slabs, buf: int):
+        dist = self.dist
+        (s,) = slabs
+        ops = []
+        if self.rank > 0:
+            ops.append(dist.P2POp(dist.isend, s.pack(buf, 0), self.rank - 1, self.group))
+            ops.append(dist.P2POp(dist.irecv, s.recv[0], self.rank - 1, self.group))
+        if self.rank < self.world - 1:
+            ops.append(dist.P2POp(dist.isend, s.pack(buf, 1), self.rank + 1, self.group))
+            ops.append(dist.P2POp(dist.irecv, s.recv[1], self.rank + 1, self.group))
+        if ops:
+            for r in dist.batch_isend_irecv(ops):
+                r.wait()
+        if self.rank > 0:
+            s.unpack(buf, 0)
+        if self.rank < self.world - 1:
+            s.unpack(buf, 1)
+
+    def allreduce_max(self, slabs, lams):
+        import torch
+        (lam,) = lams
+        t = lam if isinstance(lam, torch.Tensor) else torch.tensor([lam], dtype=torch.float64)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
+        return [t if isinstance(lam, torch.Tensor) else float(t.item())]
+
+    def allreduce_sum(self, arrs):
+        import torch
+        (a,) = arrs
+        t = torch.tensor(a, dtype=torch.float64)
+        if self.dist.get_backend(self.group) == "nccl":
+            t = t.cuda()
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
+        return t.cpu().numpy()
+
+
+class SlabRunner:
+    """Simulator::run's loop body (solver.cpp:637-649) over decomposed slabs."""
+
+    def __init__(self, slabs, comm):
+        self.slabs = list(slabs)
+        self.comm = comm
+
+    def step(self, t: float, t_next: float, t_end: float):
+        S, comm = self.slabs, self.comm
+        for s in S:
+            s.step_begin(t, t_next, t_end)
+            s.bc(0)                                      # apply_boundaries(u, t)
+        comm.exchange(S, 0)
+        lams = comm.allreduce_max(S, [s.lambda_local() for s in S])   # compute_dt
+        for s, lam in zip(S, lams):
+            s.dt_from(lam)
+            s.stage(0)                                   # predictor
+            s.bc(1)                                      # apply_boundaries(u*, t+dt)
+        comm.exchange(S, 1)
+        for s in S:
+            s.stage(1)                                   # corrector
+        res = [s.step_end() for s in S]
+        t_new, hit, dt = res[0]
+        assert all(r == res[0] for r in res), res       # dt is exact across slabs
+        return t_new, hit, dt
+
+    def steps(self, t: float, t_next: float, max_steps: int, t_end: Optional[float] = None):
+        t_end = t_next if t_end is None else t_end
+        dts, hit = [], False
+        while t < t_end and len(dts) < max_steps:
+            t, hit, dt = self.step(t, t_next, t_end)
+            dts.append(dt)
+            if hit:
+                break
+        return t, np.array(dts), hit
+
+    def audit(self) -> np.ndarray:
+        return self.comm.allreduce_sum([s.audit() for s in self.slabs]) if len(self.slabs) == 1 else \
+            np.sum([s.audit() for s in self.slabs], axis=0)
+
+
+def assemble(states: Sequence[np.ndarray]) -> np.ndarray:
+    """Interior rows of per-slab padded states -> the interior of the whole grid."""
+    return np.concatenate([s[:, 3:-3, 3:-3] for s in states], axis=1)
+
+
+# ---------------------------------------------------------------------------
+# bench.py --gpus N (torchrun): weak scaling, one 2048-row slab per rank
+# ---------------------------------------------------------------------------
+def bench_main(args, metric: str) -> None:
+    import json
+    import time
+    import torch
+    import torch.distributed as dist
+    from . import scenarios
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if not dist.is_initialized():
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    rows_per = args.nrows
+    sc = scenarios.SCENARIOS[args.config](args.ncols, rows_per * world) if args.config != "c1" \
+        else scenarios.c1_hill(args.ncols)
+    rows = decompose(sc.nrows, world)[rank]
+    stream = torch.cuda.Stream()
+    slab = CudaSlab(sc, rows, device=local, stream=stream)
+    runner = SlabRunner([slab], TorchComm())
+    with torch.cuda.stream(stream):
+        t, _, _ = runner.steps(0.0, 1e9, args.warmup, t_end=1e9)
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        t, dts, _ = runner.steps(t, 1e9, args.steps, t_end=1e9)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=f"cuda:{local}")
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms = float(ms.item())
+    cells = sc.ncols * sc.nrows
+    value = cells * args.steps / (ms / 1e3) / 1e9
+    if rank == 0:
+        out = {"metric": metric, "value": round(value, 4), "unit": "GCUPS", "n_gpus": world,
+               "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 5),
+               "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+               "data": "synthetic (scenarios.py)",
+               "config": {"workload": f"{sc.name} {sc.ncols}x{sc.nrows} (weak: {rows_per} rows per GPU), "
+                                      "row-block slabs, NCCL halo exchange + lambda all-reduce",
+                          "grid": [sc.ncols, sc.nrows], "parallelism": f"slab{world}",
+                          "l2": "inputs larger than L2"},
+               "gpu_launches": None}
+        print(json.dumps(out))
+    dist.barrier()

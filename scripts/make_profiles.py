@@ -1,0 +1,63 @@
+"""Summarise gpurun_out ncu captures into profiles/ (tracked)."""
+import csv, collections, json, subprocess, sys, os
+tag = sys.argv[1]
+out_dir = "profiles"
+def raw(rep):
+    txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(txt.splitlines()))
+    return rows[0], rows[1], rows[2:]
+lines = [f"# ncu summary, {tag}\n"]
+summary = {}
+for sfx, cfg in (("", "c2"), ("_wet", "wet")):
+    rep = f"gpurun_out/prof_{tag}{sfx}.ncu-rep"
+    if not os.path.exists(rep):
+        continue
+    hdr, units, data = raw(rep)
+    g = lambda r, k: r[hdr.index(k)] if k in hdr else ""
+    keys = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+            "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+            "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "smsp__issue_active.avg.pct_of_peak_sustained_active",
+            "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
+            "launch__occupancy_limit_registers", "launch__occupancy_limit_shared_mem", "smsp__inst_executed.sum",
+            "launch__grid_size", "launch__block_size"]
+    lines.append(f"\n## {cfg} 2048x2048 (bench.py --config {cfg}), `ncu --set full --clock-control none`\n")
+    lines.append("| metric | unit | " + " | ".join(g(r, "Kernel Name")[:40] for r in data) + " |")
+    lines.append("|---|---|" + "---|" * len(data))
+    for k in keys:
+        if k in hdr:
+            lines.append(f"| {k} | {units[hdr.index(k)]} | " + " | ".join(g(r, k) for r in data) + " |")
+    stalls = [h for h in hdr if h.startswith("smsp__average_warps_issue_stalled") and h.endswith("per_issue_active.ratio")]
+    top = sorted(stalls, key=lambda h: -float(data[0][hdr.index(h)] or 0))[:8]
+    lines.append("\nTop stall reasons (warps stalled per issue, pred/corr): " +
+                 ", ".join(f"{h.split('stalled_')[1].split('_per')[0]} {float(data[0][hdr.index(h)]):.2f}/{float(data[-1][hdr.index(h)]):.2f}" for h in top))
+    def tobytes(r, k):
+        v = float(g(r, k)); u = units[hdr.index(k)]
+        return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[u]
+    traffic = sum(tobytes(r, "dram__bytes_read.sum") + tobytes(r, "dram__bytes_write.sum") for r in data)
+    summary[cfg] = {"config": cfg, "grid": [2048, 2048], "dram_bytes_per_step": traffic,
+                    "alg_bytes_per_step": 464 * 2048 * 2048,
+                    "kernels": [g(r, "Kernel Name") for r in data]}
+    lines.append(f"\nDRAM traffic per step (pred+corr): {traffic/1e6:.1f} MB; algorithmic 464 B x 2048^2 = "
+                 f"{464*2048*2048/1e6:.1f} MB (ratio {traffic/(464*2048*2048):.3f}).\n")
+# launch list
+lc = f"gpurun_out/launches_{tag}.csv"
+if os.path.exists(lc):
+    rows = list(csv.reader(open(lc)))
+    hi = [i for i, r in enumerate(rows) if r and r[0] == "ID"][0]
+    hdr, data = rows[hi], rows[hi + 1:]
+    ki, vi = hdr.index("Kernel Name"), hdr.index("Metric Value")
+    agg = collections.defaultdict(list)
+    for r in data:
+        agg[r[ki].split("(")[0]].append(float(r[vi].replace(",", "")))
+    tot = sum(sum(v) for v in agg.values())
+    lines.append("\n## Launch list (`ncu --metrics gpu__time_duration.sum --clock-control none`, "
+                 "bench.py --steps 8 --warmup 3, cold-cache serialised: compare shares)\n")
+    lines.append("| kernel | launches | mean us | share |")
+    lines.append("|---|---|---|---|")
+    for k, v in sorted(agg.items(), key=lambda x: -sum(x[1])):
+        lines.append(f"| {k} | {len(v)} | {sum(v)/len(v)/1e3:.1f} | {100*sum(v)/tot:.1f}% |")
+open(f"{out_dir}/{tag}_ncu.md", "w").write("\n".join(lines) + "\n")
+if "c2" in summary:
+    d = summary["c2"]; d["wet"] = summary.get("wet"); d["source"] = f"profiles/{tag}_ncu.md"
+    json.dump(d, open(f"{out_dir}/ncu_stage_summary.json", "w"), indent=1)
+print("\n".join(lines))
