@@ -35,6 +35,8 @@ cudaError_t launch_post(const PostArgs& a, cudaStream_t st);
 cudaError_t launch_regularize(const GridDesc& g, const Phys& P, double* s, const double* geo,
                               DevScalars* sc, bool fastdiv, cudaStream_t st);
 cudaError_t init_kernels();
+cudaError_t init_pair_kernels();
+cudaError_t launch_stage_pair(const StageArgs& a, bool fastdiv, bool corr, cudaStream_t st);
 cudaError_t selftest_division(long long n, unsigned long long seed, unsigned long long* mismatches);
 }  // namespace tpb
 
@@ -123,6 +125,7 @@ struct tp_ctx {
     // options / flags
     bool fastdiv = true;
     int graph_steps = 16;
+    int kernel = 2;  // 2 = stage_kernel (one thread per face/cell), 3 = stage_pair_kernel (lane pairs)
     bool lam_valid = false;
     bool ghosts_in_B = false;
     bool inflow_active = false;
@@ -228,6 +231,10 @@ tpb::StageArgs stage_args(tp_ctx* c, bool corr, int loop) {
     return a;
 }
 
+cudaError_t launch_stage_sel(tp_ctx* c, const tpb::StageArgs& a, bool fastdiv, bool corr, cudaStream_t st) {
+    return c->kernel == 3 ? tpb::launch_stage_pair(a, fastdiv, corr, st) : tpb::launch_stage(a, fastdiv, corr, st);
+}
+
 void launch_bc(tp_ctx* c, int buf, int tsrc, double t, int loop) {
     tpb::BcArgs b{};
     b.g = c->g;
@@ -256,9 +263,9 @@ void launch_post(tp_ctx* c, int loop) {
 void enqueue_loop_step(tp_ctx* c) {
     launch_bc(c, 0, 1, 0.0, 1);                                     // apply_boundaries(u, t)
     ck(tpb::launch_dt(c->ph, c->dSc, 1, c->stream), "dt_kernel");   // compute_dt
-    ck(tpb::launch_stage(stage_args(c, false, 1), c->fastdiv, false, c->stream), "predictor");
+    ck(launch_stage_sel(c, stage_args(c, false, 1), c->fastdiv, false, c->stream), "predictor");
     launch_bc(c, 1, 2, 0.0, 1);                                     // apply_boundaries(u*, t+dt)
-    ck(tpb::launch_stage(stage_args(c, true, 1), c->fastdiv, true, c->stream), "corrector");
+    ck(launch_stage_sel(c, stage_args(c, true, 1), c->fastdiv, true, c->stream), "corrector");
     launch_post(c, 1);                                              // t += dt, audit, stop flag
 }
 
@@ -415,6 +422,7 @@ void create_impl(tp_ctx* c, const tp_params* p, const tp_dem* dem, int row0, int
     c->device = p->device;
     ck(cudaSetDevice(c->device), "cudaSetDevice");
     ck(tpb::init_kernels(), "init kernels");
+    ck(tpb::init_pair_kernels(), "init pair kernels");
     c->ncols = dem->ncols;
     c->nrows_g = dem->nrows;
     c->row0 = row0;
@@ -593,6 +601,10 @@ int tp_set_option(tp_ctx* c, const char* key, long value) {
         std::string k(key);
         if (k == "fastdiv") {
             c->fastdiv = value != 0;
+            drop_graphs(c);
+        } else if (k == "kernel") {
+            if (value != 2 && value != 3) throw ConfigErr{"kernel must be 2 or 3"};
+            c->kernel = static_cast<int>(value);
             drop_graphs(c);
         } else if (k == "graph_steps") {
             if (value < 1 || value > 4096) throw ConfigErr{"graph_steps must be in [1, 4096]"};
@@ -776,9 +788,9 @@ int tp_advance_step(tp_ctx* c, double dt_scaled, double t_scaled) {
     TP_GUARD(c, {
         // Simulator::advance_step (solver.cpp:496-545)
         write_ctrl(c, t_scaled, t_scaled, INFINITY, dt_scaled, LLONG_MAX);
-        ck(tpb::launch_stage(stage_args(c, false, 0), c->fastdiv, false, c->stream), "predictor");
+        ck(launch_stage_sel(c, stage_args(c, false, 0), c->fastdiv, false, c->stream), "predictor");
         launch_bc(c, 1, 2, 0.0, 0);
-        ck(tpb::launch_stage(stage_args(c, true, 0), c->fastdiv, true, c->stream), "corrector");
+        ck(launch_stage_sel(c, stage_args(c, true, 0), c->fastdiv, true, c->stream), "corrector");
         launch_post(c, 0);
         c->lam_valid = false;
         c->ghosts_in_B = true;
@@ -998,7 +1010,7 @@ int tp_dt_from(tp_ctx* c, const void* lam) {
 
 int tp_stage(tp_ctx* c, int corrector) {
     TP_GUARD(c, {
-        ck(tpb::launch_stage(stage_args(c, corrector != 0, 0), c->fastdiv, corrector != 0, c->stream),
+        ck(launch_stage_sel(c, stage_args(c, corrector != 0, 0), c->fastdiv, corrector != 0, c->stream),
            corrector ? "corrector" : "predictor");
         if (corrector) {
             c->lam_valid = true;  // lam_bits now holds the local lambda of u^{n+1}

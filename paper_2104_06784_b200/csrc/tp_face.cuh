@@ -61,10 +61,31 @@ __device__ __forceinline__ void face_flux(const double (&L)[6], const double (&R
         dfix<FD>(jL1, qnL1, rj);
         dfix<FD>(jR1, qnR1, rj);
     }
-    const double vnL0 = jL0 * desing_factor<FD>(smax(hL0, 0.0), P.eps_h);
-    const double vnR0 = jR0 * desing_factor<FD>(smax(hR0, 0.0), P.eps_h);
-    const double vnL1 = jL1 * desing_factor<FD>(smax(hL1, 0.0), P.eps_h);
-    const double vnR1 = jR1 * desing_factor<FD>(smax(hR1, 0.0), P.eps_h);
+    const double dL0 = smax(hL0, 0.0), dR0 = smax(hR0, 0.0);
+    const double dL1 = smax(hL1, 0.0), dR1 = smax(hR1, 0.0);
+    double fL0, fR0, fL1, fR1;
+    if (FD) {  // four desingularisation divisions, one shared slow-path branch
+        bool okf = true;
+        fL0 = desing_factor_g(dL0, P.eps_h, okf);
+        fR0 = desing_factor_g(dR0, P.eps_h, okf);
+        fL1 = desing_factor_g(dL1, P.eps_h, okf);
+        fR1 = desing_factor_g(dR1, P.eps_h, okf);
+        if (!okf) {
+            fL0 = desing_factor<FD>(dL0, P.eps_h);
+            fR0 = desing_factor<FD>(dR0, P.eps_h);
+            fL1 = desing_factor<FD>(dL1, P.eps_h);
+            fR1 = desing_factor<FD>(dR1, P.eps_h);
+        }
+    } else {
+        fL0 = desing_factor<FD>(dL0, P.eps_h);
+        fR0 = desing_factor<FD>(dR0, P.eps_h);
+        fL1 = desing_factor<FD>(dL1, P.eps_h);
+        fR1 = desing_factor<FD>(dR1, P.eps_h);
+    }
+    const double vnL0 = jL0 * fL0;
+    const double vnR0 = jR0 * fR0;
+    const double vnL1 = jL1 * fL1;
+    const double vnR1 = jR1 * fR1;
     double a = 0.0;
     a = smax(a, smax(fabs(vnL0) + celL, fabs(vnR0) + celR));
     a = smax(a, smax(fabs(vnL1) + celL, fabs(vnR1) + celR));

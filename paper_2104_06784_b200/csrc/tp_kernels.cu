@@ -22,68 +22,10 @@
 #include <cuda_runtime.h>
 
 #include "tp_face.cuh"
+#include "tp_stage_common.cuh"
 #include "tp_types.h"
 
 namespace tpb {
-
-__device__ __forceinline__ double ldg(const double* p) { return __ldg(p); }
-
-__device__ __forceinline__ void lam_block_max(double lam, DevScalars* sc) {
-    // lam >= 0 (or NaN, which reduce_max ignores: std::max(m, NaN) == m)
-    unsigned long long b = (lam == lam) ? static_cast<unsigned long long>(__double_as_longlong(lam)) : 0ull;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        unsigned long long x = __shfl_xor_sync(0xffffffffu, b, o);
-        b = x > b ? x : b;
-    }
-    __shared__ unsigned long long wmax[NT / 32];
-    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-    if (l == 0) wmax[w] = b;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned long long m = 0;
-        for (int k = 0; k < NT / 32; ++k) m = wmax[k] > m ? wmax[k] : m;
-        if (m) atomicMax(&sc->lam_bits, m);
-    }
-}
-
-// ---------------------------------------------------------------------------
-// TMA / mbarrier helpers (sm_90+ PTX, used here on sm_100a)
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-    return static_cast<unsigned>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, int x, int y, int z,
-                                            unsigned long long* bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<unsigned long long>(tm)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
-        : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@!p bra WAIT_%=;\n"
-        "}\n" ::"r"(smem_u32(bar)),
-        "r"(phase)
-        : "memory");
-}
-__device__ __forceinline__ void prefetch_l2(const void* p) {
-    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
-}
 
 // regularize + [check_finite + lambda] + store of one updated cell: the tail of
 // advance_step's stages (solver.cpp:139-166, :482-494, :556-573).
@@ -92,6 +34,7 @@ __device__ __forceinline__ void cell_epilogue(double (&un)[6], const Rcp& rj, do
                                               const Phys& P, DevScalars* sc, double& lam_local,
                                               double* out, long long fs, long long o3) {
     // regularize (solver.cpp:139-166), solid then fluid
+    double hpv[2];
     {
         bool okr = rj.ok;
         double hp0 = dq<FD>(un[0], rj, okr), hp1 = dq<FD>(un[1], rj, okr);
@@ -99,11 +42,12 @@ __device__ __forceinline__ void cell_epilogue(double (&un)[6], const Rcp& rj, do
             dfix<FD>(hp0, un[0], rj);
             dfix<FD>(hp1, un[1], rj);
         }
-        double hpv[2] = {hp0, hp1};
+        hpv[0] = hp0;
+        hpv[1] = hp1;
 #pragma unroll
         for (int p = 0; p < 2; ++p) {
             const double w = un[p];
-            double hp = hpv[p];
+            double& hp = hpv[p];
             if (hp < 0.0) {
                 if (hp < -1e-12) {
                     const unsigned long long key =
@@ -137,13 +81,12 @@ __device__ __forceinline__ void cell_epilogue(double (&un)[6], const Rcp& rj, do
             }
         }
         // lambda of the new state for the next compute_dt (solver.cpp:560-571)
+        // hs, hf: regularize's hp (exactly w_new / jb; 0.0 after a clip, as 0.0 / jb)
+        const double hs = hpv[0], hf = hpv[1];
         bool okl = rj.ok;
-        double hs = dq<FD>(un[0], rj, okl), hf = dq<FD>(un[1], rj, okl);
         double jsx = dq<FD>(un[2], rj, okl), jsy = dq<FD>(un[3], rj, okl);
         double jfx = dq<FD>(un[4], rj, okl), jfy = dq<FD>(un[5], rj, okl);
         if (!okl) {
-            dfix<FD>(hs, un[0], rj);
-            dfix<FD>(hf, un[1], rj);
             dfix<FD>(jsx, un[2], rj);
             dfix<FD>(jsy, un[3], rj);
             dfix<FD>(jfx, un[4], rj);
@@ -151,8 +94,8 @@ __device__ __forceinline__ void cell_epilogue(double (&un)[6], const Rcp& rj, do
         }
         const double h = hs + hf;
         if (!(h < P.h_dry)) {
-            const double fsld = desing_factor<FD>(hs, P.eps_h);
-            const double fflu = desing_factor<FD>(hf, P.eps_h);
+            double fsld, fflu;
+            desing_pair<FD>(hs, hf, P.eps_h, fsld, fflu);
             const double vsx = jsx * fsld, vsy = jsy * fsld;
             const double vfx = jfx * fflu, vfy = jfy * fflu;
             const double cel = sqrt(P.eps * nZ * h);
@@ -166,16 +109,6 @@ __device__ __forceinline__ void cell_epilogue(double (&un)[6], const Rcp& rj, do
     for (int f = 0; f < 6; ++f) out[f * fs + o3] = un[f];
 }
 
-// shared-memory carve-up of the stage kernel (doubles)
-constexpr int SM_S = 0;                                   // [6][BOX] state box (TMA)
-constexpr int SM_G = ((6 * BOX * 8 + 127) / 128) * 16;    // [NGBOX][BOX] geometry box (TMA), 128B aligned
-constexpr int SM_V = SM_G + NGBOX * BOX;                  // [4][BOX] cell velocities
-constexpr int SM_PJ = SM_V + 4 * BOX;                     // [BOX] jb*h*p_bar_f
-constexpr int SM_BR = SM_PJ + BOX;                        // [3][BOX] viscous brackets
-constexpr int SM_FX = SM_BR + 3 * BOX;                    // [6][NFX] xi face fluxes
-constexpr int SM_FY = SM_FX + 6 * NFX;                    // [6][NFY] eta face fluxes
-constexpr int SM_END = SM_FY + 6 * NFY;
-constexpr unsigned kTmaBytes = (6 + NGBOX) * BOX * 8;
 
 // ---------------------------------------------------------------------------
 // The fused stage kernel.
@@ -362,8 +295,8 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
                 dfix<FD>(jfy, qfy, rj);
             }
             const double h = hs + hf;
-            const double fsld = desing_factor<FD>(hs, P.eps_h);
-            const double fflu = desing_factor<FD>(hf, P.eps_h);
+            double fsld, fflu;
+            desing_pair<FD>(hs, hf, P.eps_h, fsld, fflu);
             V[0 * BOX + k] = jsx * fsld;
             V[1 * BOX + k] = jsy * fsld;
             V[2 * BOX + k] = jfx * fflu;
@@ -590,7 +523,14 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
                     dfix<FD>(jy, qy, rj);
                 }
                 if (!(hs < P.h_dry)) {
-                    const double fsld = desing_factor<FD>(hs, P.eps_h);
+                    double fsld;
+                    if (FD) {
+                        bool okf = true;
+                        fsld = desing_factor_g(hs, P.eps_h, okf);
+                        if (!okf) fsld = desing_factor<FD>(hs, P.eps_h);
+                    } else {
+                        fsld = desing_factor<FD>(hs, P.eps_h);
+                    }
                     const double vsx = jx * fsld;
                     const double vsy = jy * fsld;
                     const double vz = dv<FD>(-(nX * vsx + nY * vsy), rnz);
@@ -598,7 +538,16 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
                     const double p_b_s = smax(0.0, hs * (nZ * P.oma - P.eps_chi * kap));
                     const double rate = jb * p_b_s * P.tan_d;
                     const double qnorm = sqrt(qx * qx + qy * qy);
-                    const double factor = smax(0.0, 1.0 - dt * rate / qnorm);
+                    const double num = dt * rate;
+                    double frac;
+                    if (FD) {
+                        bool okq = true;
+                        frac = ddiv_fast(num, qnorm, okq);
+                        if (!okq) frac = num / qnorm;
+                    } else {
+                        frac = num / qnorm;
+                    }
+                    const double factor = smax(0.0, 1.0 - frac);  // 1.0 - dt * rate / qnorm
                     un[2] = qx * factor;
                     un[3] = qy * factor;
                 }
@@ -769,8 +718,8 @@ __global__ void __launch_bounds__(NT) lambda_kernel(GridDesc g, Phys P, const do
         const double hs = dv<FD>(s[0 * g.fs + o], rj);
         const double hf = dv<FD>(s[1 * g.fs + o], rj);
         const double h = hs + hf;
-        const double fsld = desing_factor<FD>(hs, P.eps_h);
-        const double fflu = desing_factor<FD>(hf, P.eps_h);
+        double fsld, fflu;
+        desing_pair<FD>(hs, hf, P.eps_h, fsld, fflu);
         const double vsx = dv<FD>(s[2 * g.fs + o], rj) * fsld;
         const double vsy = dv<FD>(s[3 * g.fs + o], rj) * fsld;
         const double vfx = dv<FD>(s[4 * g.fs + o], rj) * fflu;
@@ -1005,6 +954,17 @@ __global__ void selftest_div_kernel(long long n, unsigned long long seed, unsign
         const double q = dv<true>(a, r);
         const double ref = a / b;
         if (__double_as_longlong(q) != __double_as_longlong(ref)) ++local;
+        // nvcc's fast-path sequence with the shared slow-path branch
+        bool okd = true;
+        double q3 = ddiv_fast(a, b, okd);
+        if (!okd) q3 = a / b;
+        if (__double_as_longlong(q3) != __double_as_longlong(ref)) ++local;
+        // desingularisation factor, grouped vs single
+        const double hh = fabs(a) * 1e-3;
+        bool okg = true;
+        double fg = desing_factor_g(hh, 1e-6, okg);
+        if (!okg) fg = desing_factor<true>(hh, 1e-6);
+        if (__double_as_longlong(fg) != __double_as_longlong(desing_factor<false>(hh, 1e-6))) ++local;
     }
     if (local) atomicAdd(bad, local);
 }
