@@ -306,24 +306,101 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
     }
     __syncthreads();
 
-    // ---- Phase 2: viscous brackets on the cross neighbours of the tile --------
-    // (and the per-cell fields of this thread's Phase-3 cell, now L2-warm)
-    double gc[9];
-    double u0c[6];
-    if (p3) {
-#pragma unroll
-        for (int f = 0; f < 9; ++f) gc[f] = __ldg(geo + (G_NX + f) * fs + o3);
-        if (CORR) {
-#pragma unroll
-            for (int f = 0; f < 6; ++f) u0c[f] = A.u0[f * fs + o3];
-        }
-    }
+    // ---- Phase 2: (a) the cell-local source terms of this thread's Phase-3 cell
+    // (solver.cpp:406-445 minus the viscous divergence, which needs neighbours'
+    // brackets) and (b) the viscous brackets of the tile's cross neighbours, spread
+    // so that the 16 threads without a cell take the 62 extra brackets.
     const Rcp r2x = mkrcp_const<FD>(P.two_dxi, P.r_two_dxi);
     const Rcp r2y = mkrcp_const<FD>(P.two_deta, P.r_two_deta);
+    const Rcp rNR = mkrcp_const<FD>(P.N_R, P.r_NR);
+    // partial rhs sums in the reference's order: rhs[2] = div + ((sn + sf) + sv),
+    // rhs[4] = div + ((((sn + sd) + sf) + sv) + svis)  (solver.cpp:442-445)
+    double Ps2 = 0.0, Ps3 = 0.0, Pf4 = 0.0, Pf5 = 0.0, visc = 0.0;
+    if (p3 && !P.adv_only) {
+        const int bk = (threadIdx.x / TX + 2) * W2 + (threadIdx.x % TX + 2);
+        const double nX = __ldg(geo + G_NX * fs + o3), nY = __ldg(geo + G_NY * fs + o3);
+        const double dXx = __ldg(geo + G_DNX_DXI * fs + o3), dYx = __ldg(geo + G_DNY_DXI * fs + o3);
+        const double dZx = __ldg(geo + G_DNZ_DXI * fs + o3), dXy = __ldg(geo + G_DNX_DETA * fs + o3);
+        const double dYy = __ldg(geo + G_DNY_DETA * fs + o3), dZy = __ldg(geo + G_DNZ_DETA * fs + o3);
+        const double nZ = G[G_NZ * BOX + bk];
+        const Rcp rnz = mkrcp_const<FD>(nZ, __ldg(geo + G_RNZ * fs + o3));
+        const double jb = G[G_JB * BOX + bk];
+        const Rcp rj = mkrcp_const<FD>(jb, G[G_RJB * BOX + bk]);
+        const double a11 = G[G_A11 * BOX + bk], a12 = G[G_A12 * BOX + bk];
+        const double a21 = G[G_A21 * BOX + bk], a22 = G[G_A22 * BOX + bk];
+        const double ws = S[0 * BOX + bk], wf = S[1 * BOX + bk];
+        const double gpx = PJ[bk + 1] - PJ[bk - 1], gpy = PJ[bk + W2] - PJ[bk - W2];
+        const double vsx = V[0 * BOX + bk], vsy = V[1 * BOX + bk];
+        const double vfx = V[2 * BOX + bk], vfy = V[3 * BOX + bk];
+        const double nzs = -(nX * vsx + nY * vsy), nzf = -(nX * vfx + nY * vfy);
+        const Rcp reNR = mkrcp_const<FD>(P.eps_NR, P.r_eps_NR);
+        bool ok2 = rj.ok && rnz.ok && r2x.ok && r2y.ok;
+        double hs = dq<FD>(ws, rj, ok2), hf = dq<FD>(wf, rj, ok2);
+        double vzs = dq<FD>(nzs, rnz, ok2), vzf = dq<FD>(nzf, rnz, ok2);
+        double gPx = dq<FD>(gpx, r2x, ok2), gPy = dq<FD>(gpy, r2y, ok2);
+        if (!ok2) {
+            dfix<FD>(hs, ws, rj);
+            dfix<FD>(hf, wf, rj);
+            dfix<FD>(vzs, nzs, rnz);
+            dfix<FD>(vzf, nzf, rnz);
+            dfix<FD>(gPx, gpx, r2x);
+            dfix<FD>(gPy, gpy, r2y);
+        }
+        const double h = hs + hf;
+        double phi_s = 0.0, phi_f = 0.0, hsf_h = 0.0;
+        if (!(h <= 0.0)) {
+            const Rcp rh = mkrcp<FD>(h);
+            const double hsf = hs * hf;
+            bool okh = rh.ok;
+            double q1 = dq<FD>(hs, rh, okh), q2 = dq<FD>(hf, rh, okh), q3 = dq<FD>(hsf, rh, okh);
+            if (!okh) {
+                dfix<FD>(q1, hs, rh);
+                dfix<FD>(q2, hf, rh);
+                dfix<FD>(q3, hsf, rh);
+            }
+            if (!(h < P.h_dry)) {  // phi = h < h_dry ? 0 : hs / h  (solver.cpp:410-411)
+                phi_s = q1;
+                phi_f = q2;
+            }
+            hsf_h = q3;
+        }
+        // physics::curvature_accel (physics.hpp:47-52) with vz from tangency
+        const double kap_s = ((vsx * dXx + vsy * dYx) + vzs * dZx) * vsx + ((vsx * dXy + vsy * dYy) + vzs * dZy) * vsy;
+        const double kap_f = ((vfx * dXx + vfy * dYx) + vzf * dZx) * vfx + ((vfx * dXy + vfy * dYy) + vzf * dZy) * vfy;
+        // physics::hydrostatic_terms (physics.hpp:56-69)
+        const double p_b_s = smax(0.0, hs * (nZ * P.oma - P.eps_chi * kap_s));
+        const double p_b_f = smax(0.0, hf * (nZ - P.eps_chi * kap_f));
+        // solid: gravity + pressure gradient + drag (physics.hpp:98-155)
+        const double sn_sx = jb * p_b_s * nX, sn_sy = jb * p_b_s * nY;
+        const double Avx = a11 * gPx + a21 * gPy;
+        const double Avy = a12 * gPx + a22 * gPy;
+        const double fsp = P.neg_eps_alpha * phi_s;
+        double sv_sx = 0.0, sv_sy = 0.0, sv_fx = 0.0, sv_fy = 0.0;
+        if (!(h <= 0.0)) {
+            const double common = jb * P.C_d * hsf_h;
+            const double cx = common * (vfx - vsx);
+            const double cy = common * (vfy - vsy);
+            sv_sx = P.alpha * cx;
+            sv_sy = P.alpha * cy;
+            sv_fx = -cx;
+            sv_fy = -cy;
+        }
+        // fluid: gravity + friction + pressure gradient + drag (+ viscous in Phase 3)
+        const double sn_fx = jb * p_b_f * nX, sn_fy = jb * p_b_f * nY;
+        const double coeff = dv<FD>(jb * hf * P.theta_b, reNR);
+        const double ephf = P.eps * phi_f;
+        visc = dv<FD>(ephf, rNR);
+        Ps2 = sn_sx + fsp * Avx + sv_sx;
+        Ps3 = sn_sy + fsp * Avy + sv_sy;
+        Pf4 = sn_fx + -coeff * vfx + ephf * Avx + sv_fx;
+        Pf5 = sn_fy + -coeff * vfy + ephf * Avy + sv_fy;
+    }
     if (!P.adv_only) {
         constexpr int NB1 = (TX + 2) * TY;  // rows 2..TY+1, cols 1..TX+2
         constexpr int NB = NB1 + 2 * TX;    // + rows 1 and TY+2, cols 2..TX+1
-        for (int it = threadIdx.x; it < NB; it += NT) {
+        // threads with a Phase-3 cell: one bracket each; the rest stride over the remainder
+        const int stride = threadIdx.x < TX * TY ? NB : NT - TX * TY;
+        for (int it = threadIdx.x; it < NB; it += stride) {
             int bx, by;
             if (it < NB1) {
                 bx = 1 + it % (TX + 2);
@@ -362,7 +439,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
         }
     }
     // this thread's Phase-3 cell out of the staged boxes (they are recycled below)
-    double sc6[6], gjb = 1.0, grjb = 1.0, gnz = 1.0, ga11 = 0.0, ga12 = 0.0, ga21 = 0.0, ga22 = 0.0;
+    double sc6[6], gjb = 1.0, grjb = 1.0, gnz = 1.0;
     {
         const int bk = (threadIdx.x / TX + 2) * W2 + (threadIdx.x % TX + 2);
         if (p3) {
@@ -371,26 +448,20 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
             gjb = G[G_JB * BOX + bk];
             grjb = G[G_RJB * BOX + bk];
             gnz = G[G_NZ * BOX + bk];
-            ga11 = G[G_A11 * BOX + bk];
-            ga12 = G[G_A12 * BOX + bk];
-            ga21 = G[G_A21 * BOX + bk];
-            ga22 = G[G_A22 * BOX + bk];
         }
     }
     __syncthreads();
     issue_next();
 
-    // ---- Phase 3: residual + update + cap + [average] + regularize + [finite, lambda]
+    // ---- Phase 3: divergence + viscous source + update + cap + [average] +
+    //      regularize + [finite, lambda]
     const Rcp rdx = mkrcp_const<FD>(P.dxi, P.r_dxi);
     const Rcp rdy = mkrcp_const<FD>(P.deta, P.r_deta);
     if (p3) {
         const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
         const int X = p3x, Y = p3y;
         const int bk = (ty + 2) * W2 + (tx + 2);
-        const double nX = gc[0], nY = gc[1];
-        const double dXx = gc[2], dYx = gc[3], dZx = gc[4], dXy = gc[5], dYy = gc[6], dZy = gc[7];
         const double nZ = gnz;
-        const Rcp rnz = mkrcp_const<FD>(nZ, gc[8]);
         const double jb = gjb;
         const Rcp rj = mkrcp_const<FD>(jb, grjb);
 
@@ -418,91 +489,26 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
         for (int f = 0; f < 6; ++f) rhs[f] = dx[f] + dy[f];
 
         if (!P.adv_only) {
-            const double a11 = ga11, a12 = ga12, a21 = ga21, a22 = ga22;
-            // solver.cpp:406-445
-            const double ws = sc6[0], wf = sc6[1];
-            const double gpx = PJ[bk + 1] - PJ[bk - 1], gpy = PJ[bk + W2] - PJ[bk - W2];
             const double* bvx = BR;
             const double* bvy = BR + BOX;
             const double* bxy = BR + 2 * BOX;
             const double s1 = 2.0 * (bvx[bk + 1] - bvx[bk - 1]), s2 = bxy[bk + W2] - bxy[bk - W2];
             const double s3 = 2.0 * (bvy[bk + W2] - bvy[bk - W2]), s4 = bxy[bk + 1] - bxy[bk - 1];
-            const double vsx = V[0 * BOX + bk], vsy = V[1 * BOX + bk];
-            const double vfx = V[2 * BOX + bk], vfy = V[3 * BOX + bk];
-            const double nzs = -(nX * vsx + nY * vsy), nzf = -(nX * vfx + nY * vfy);
-            const Rcp rNR = mkrcp_const<FD>(P.N_R, P.r_NR);
-            const Rcp reNR = mkrcp_const<FD>(P.eps_NR, P.r_eps_NR);
-            bool ok2 = rj.ok && rnz.ok && r2x.ok && r2y.ok && rNR.ok && reNR.ok;
-            double hs = dq<FD>(ws, rj, ok2), hf = dq<FD>(wf, rj, ok2);
-            double vzs = dq<FD>(nzs, rnz, ok2), vzf = dq<FD>(nzf, rnz, ok2);
-            double gPx = dq<FD>(gpx, r2x, ok2), gPy = dq<FD>(gpy, r2y, ok2);
-            double v1 = dq<FD>(s1, r2x, ok2), v2 = dq<FD>(s2, r2y, ok2);
-            double v3 = dq<FD>(s3, r2y, ok2), v4 = dq<FD>(s4, r2x, ok2);
-            if (!ok2) {
-                dfix<FD>(hs, ws, rj);
-                dfix<FD>(hf, wf, rj);
-                dfix<FD>(vzs, nzs, rnz);
-                dfix<FD>(vzf, nzf, rnz);
-                dfix<FD>(gPx, gpx, r2x);
-                dfix<FD>(gPy, gpy, r2y);
+            bool ok3 = r2x.ok && r2y.ok;
+            double v1 = dq<FD>(s1, r2x, ok3), v2 = dq<FD>(s2, r2y, ok3);
+            double v3 = dq<FD>(s3, r2y, ok3), v4 = dq<FD>(s4, r2x, ok3);
+            if (!ok3) {
                 dfix<FD>(v1, s1, r2x);
                 dfix<FD>(v2, s2, r2y);
                 dfix<FD>(v3, s3, r2y);
                 dfix<FD>(v4, s4, r2x);
             }
-            const double h = hs + hf;
-            double phi_s = 0.0, phi_f = 0.0, hsf_h = 0.0;
-            if (!(h <= 0.0)) {
-                const Rcp rh = mkrcp<FD>(h);
-                const double hsf = hs * hf;
-                bool okh = rh.ok;
-                double q1 = dq<FD>(hs, rh, okh), q2 = dq<FD>(hf, rh, okh), q3 = dq<FD>(hsf, rh, okh);
-                if (!okh) {
-                    dfix<FD>(q1, hs, rh);
-                    dfix<FD>(q2, hf, rh);
-                    dfix<FD>(q3, hsf, rh);
-                }
-                if (!(h < P.h_dry)) {  // phi = h < h_dry ? 0 : hs / h  (solver.cpp:410-411)
-                    phi_s = q1;
-                    phi_f = q2;
-                }
-                hsf_h = q3;
-            }
-            // physics::curvature_accel (physics.hpp:47-52) with vz from tangency
-            const double kap_s = ((vsx * dXx + vsy * dYx) + vzs * dZx) * vsx + ((vsx * dXy + vsy * dYy) + vzs * dZy) * vsy;
-            const double kap_f = ((vfx * dXx + vfy * dYx) + vzf * dZx) * vfx + ((vfx * dXy + vfy * dYy) + vzf * dZy) * vfy;
-            // physics::hydrostatic_terms (physics.hpp:56-69)
-            const double p_b_s = smax(0.0, hs * (nZ * P.oma - P.eps_chi * kap_s));
-            const double p_b_f = smax(0.0, hf * (nZ - P.eps_chi * kap_f));
-            // solid: gravity + pressure gradient + drag (physics.hpp:98-155)
-            const double sn_sx = jb * p_b_s * nX, sn_sy = jb * p_b_s * nY;
-            const double Avx = a11 * gPx + a21 * gPy;
-            const double Avy = a12 * gPx + a22 * gPy;
-            const double fsp = P.neg_eps_alpha * phi_s;
-            const double sf_sx = fsp * Avx, sf_sy = fsp * Avy;
-            double sv_sx = 0.0, sv_sy = 0.0, sv_fx = 0.0, sv_fy = 0.0;
-            if (!(h <= 0.0)) {
-                const double common = jb * P.C_d * hsf_h;
-                const double cx = common * (vfx - vsx);
-                const double cy = common * (vfy - vsy);
-                sv_sx = P.alpha * cx;
-                sv_sy = P.alpha * cy;
-                sv_fx = -cx;
-                sv_fy = -cy;
-            }
-            // fluid: gravity + friction + pressure gradient + drag + viscous
-            const double sn_fx = jb * p_b_f * nX, sn_fy = jb * p_b_f * nY;
-            const double coeff = dv<FD>(jb * hf * P.theta_b, reNR);
-            const double sd_fx = -coeff * vfx, sd_fy = -coeff * vfy;
-            const double ephf = P.eps * phi_f;
-            const double sf_fx = ephf * Avx, sf_fy = ephf * Avy;
-            const double visc = dv<FD>(ephf, rNR);
             const double svis_x = visc * (v1 + v2);
             const double svis_y = visc * (v3 + v4);
-            rhs[2] = rhs[2] + (sn_sx + sf_sx + sv_sx);
-            rhs[3] = rhs[3] + (sn_sy + sf_sy + sv_sy);
-            rhs[4] = rhs[4] + (sn_fx + sd_fx + sf_fx + sv_fx + svis_x);
-            rhs[5] = rhs[5] + (sn_fy + sd_fy + sf_fy + sv_fy + svis_y);
+            rhs[2] = rhs[2] + Ps2;
+            rhs[3] = rhs[3] + Ps3;
+            rhs[4] = rhs[4] + (Pf4 + svis_x);
+            rhs[5] = rhs[5] + (Pf5 + svis_y);
         }
 
         // stage update: predictor u = u0 + dt*R (:518), corrector u += dt*R (:531)
@@ -514,6 +520,11 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
         if (P.cap_on) {
             const double qx = un[2], qy = un[3];
             if (!(qx == 0.0 && qy == 0.0)) {
+                const double nX = __ldg(geo + G_NX * fs + o3), nY = __ldg(geo + G_NY * fs + o3);
+                const double dXx = __ldg(geo + G_DNX_DXI * fs + o3), dYx = __ldg(geo + G_DNY_DXI * fs + o3);
+                const double dZx = __ldg(geo + G_DNZ_DXI * fs + o3), dXy = __ldg(geo + G_DNX_DETA * fs + o3);
+                const double dYy = __ldg(geo + G_DNY_DETA * fs + o3), dZy = __ldg(geo + G_DNZ_DETA * fs + o3);
+                const Rcp rnz = mkrcp_const<FD>(nZ, __ldg(geo + G_RNZ * fs + o3));
                 bool okc = rj.ok;
                 double hs = dq<FD>(un[0], rj, okc);
                 double jx = dq<FD>(qx, rj, okc), jy = dq<FD>(qy, rj, okc);
@@ -556,7 +567,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
 
         if (CORR) {  // Heun average (solver.cpp:538-541)
 #pragma unroll
-            for (int f = 0; f < 6; ++f) un[f] = 0.5 * (u0c[f] + un[f]);
+            for (int f = 0; f < 6; ++f) un[f] = 0.5 * (A.u0[f * fs + o3] + un[f]);
         }
 
         cell_epilogue<FD, CORR>(un, rj, nZ, X, Y, P, sc, lam_local, A.out, fs, o3);

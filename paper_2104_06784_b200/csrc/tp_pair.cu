@@ -20,8 +20,9 @@
 
 namespace tpb {
 
-constexpr int NTP = 256;  // threads per CTA of the pair kernel (128 lane pairs)
+constexpr int NTP = 512;  // threads per CTA of the pair kernel
 constexpr int NPAIR = NTP / 2;
+static_assert(NPAIR >= TX * TY, "Phase 3 maps one lane pair to each tile cell");
 
 __device__ __forceinline__ double pshfl(unsigned pm, double v) { return __shfl_xor_sync(pm, v, 1); }
 
