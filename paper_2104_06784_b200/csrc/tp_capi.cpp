@@ -70,14 +70,15 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 // 3-D tiled descriptor over [nfields][ny][pitch] doubles with the stage-kernel box
-CUtensorMap make_box_map(void* base, int nx, int ny, int pitch, long long fs, int nfields) {
+CUtensorMap make_box_map(void* base, int nx, int ny, int pitch, long long fs, int nfields, int bw = tpb::W2,
+                         int bh = tpb::H2, int bf = -1) {
     CUtensorMap m;
     cuuint64_t dims[3] = {static_cast<cuuint64_t>(nx), static_cast<cuuint64_t>(ny),
                           static_cast<cuuint64_t>(nfields)};
     cuuint64_t strides[2] = {static_cast<cuuint64_t>(pitch) * sizeof(double),
                              static_cast<cuuint64_t>(fs) * sizeof(double)};
-    cuuint32_t box[3] = {static_cast<cuuint32_t>(tpb::W2), static_cast<cuuint32_t>(tpb::H2),
-                         static_cast<cuuint32_t>(nfields)};
+    cuuint32_t box[3] = {static_cast<cuuint32_t>(bw), static_cast<cuuint32_t>(bh),
+                         static_cast<cuuint32_t>(bf < 0 ? nfields : bf)};
     cuuint32_t estr[3] = {1, 1, 1};
     CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, estr,
                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -136,7 +137,7 @@ struct tp_ctx {
     int graphK_steps = 0;
     long launches = 0;
     double t_next_last = 0.0;
-    CUtensorMap tmA{}, tmB{}, tmG{};
+    CUtensorMap tmA{}, tmB{}, tmG{}, tmC{};
 };
 
 namespace {
@@ -216,6 +217,7 @@ tpb::StageArgs stage_args(tp_ctx* c, bool corr, int loop) {
     tpb::StageArgs a{};
     a.tm_s = corr ? c->tmB : c->tmA;
     a.tm_g = c->tmG;
+    a.tm_c = c->tmC;
     a.g = c->g;
     a.ph = c->ph;
     a.s = corr ? c->dB : c->dA;
@@ -514,6 +516,8 @@ void create_impl(tp_ctx* c, const tp_params* p, const tp_dem* dem, int row0, int
     c->tmA = make_box_map(c->rawA, c->nx + 1, c->ny, c->pitch, c->fs, 6);
     c->tmB = make_box_map(c->rawB, c->nx + 1, c->ny, c->pitch, c->fs, 6);
     c->tmG = make_box_map(c->rawGeo, c->nx + 1, c->ny, c->pitch, c->fs, tpb::NGBOX);
+    c->tmC = make_box_map(c->rawGeo, c->nx + 1, c->ny, c->pitch, c->fs, tpb::G_COUNT, tpb::TX, tpb::TY,
+                          tpb::G_COUNT - tpb::NGBOX);
     DevScalars h{};
     h.lam_bits = 0;
     h.lam_cur = 0;

@@ -116,7 +116,9 @@ __device__ __forceinline__ void cell_epilogue(double (&un)[6], const Rcp& rj, do
 template <bool FD, bool CORR>
 __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ StageArgs A) {
     extern __shared__ __align__(128) double sm[];
-    __shared__ unsigned long long bar;
+    __shared__ unsigned long long bar;   // state + stencil-geometry boxes
+    __shared__ unsigned long long barc;  // per-cell geometry box
+    const double* Cg = sm + SM_C;        // [NGCELL][TY][TX]: nX, nY, dnX/dxi, dnY/dxi, dnZ/dxi, dnX/deta, dnY/deta, dnZ/deta, RN(1/nZ)
     double* S = sm + SM_S;
     const double* G = sm + SM_G;
     double* V = sm + SM_V;
@@ -141,14 +143,22 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
     // next tile's TMA is issued as soon as the current tile's staged boxes are
     // dead (after Phase 2), so it lands while Phase 3 computes.
     int tile = blockIdx.x;
+    auto issue_cell = [&](int t) {  // per-cell geometry of tile t (thread 0)
+        if (t < ntiles) {
+            mbar_expect_tx(&barc, kTmaCellBytes);
+            tma_load_3d(sm + SM_C, &A.tm_c, 3 + (t % A.ntx) * TX + 1, 3 + (t / A.ntx) * TY, G_NX, &barc);
+        }
+    };
     if (threadIdx.x == 0) {
         mbar_init(&bar, 1);
+        mbar_init(&barc, 1);
         if (tile < ntiles) {
             const int bx0 = 1 + (tile % A.ntx) * TX, by0 = 1 + (tile / A.ntx) * TY;
             mbar_expect_tx(&bar, kTmaBytes);
             // x coordinate + 1: the leading pad column of the device layout (tp_capi.cpp)
             tma_load_3d(S, &A.tm_s, bx0 + 1, by0, 0, &bar);
             tma_load_3d(sm + SM_G, &A.tm_g, bx0 + 1, by0, 0, &bar);
+            issue_cell(tile);
         }
     }
     __syncthreads();  // barrier init visible to all threads
@@ -162,8 +172,6 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
     const bool p3 = threadIdx.x < TX * TY && p3x <= nx - 4 && p3y <= ny - 4;
     const long long o3 = static_cast<long long>(p3y) * pitch + p3x;
     if (iter == 0 && p3) {  // later tiles were prefetched during the previous Phase 3
-#pragma unroll
-        for (int f = G_NX; f <= G_RNZ; ++f) prefetch_l2(geo + f * fs + o3);
         if (CORR) {
 #pragma unroll
             for (int f = 0; f < 6; ++f) prefetch_l2(A.u0 + f * fs + o3);
@@ -183,8 +191,6 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
                 const int qx = bx0n + 2 + (threadIdx.x % TX), qy = by0n + 2 + (threadIdx.x / TX);
                 if (threadIdx.x < TX * TY && qx <= nx - 4 && qy <= ny - 4) {
                     const long long oq = static_cast<long long>(qy) * pitch + qx;
-    #pragma unroll
-                    for (int f = G_NX; f <= G_RNZ; ++f) prefetch_l2(geo + f * fs + oq);
                     if (CORR) {
     #pragma unroll
                         for (int f = 0; f < 6; ++f) prefetch_l2(A.u0 + f * fs + oq);
@@ -209,6 +215,10 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
         const double nz0 = p3 ? G[G_NZ * BOX + bk0] : 1.0;
         if (!__syncthreads_or(acc != 0ull)) {
             issue_next();
+            if (threadIdx.x == 0) {  // retire this tile's cell box, stage the next one
+                mbar_wait(&barc, iter & 1u);
+                issue_cell(tile + gridDim.x);
+            }
             if (p3) {
                 if (!CORR) {
 #pragma unroll
@@ -316,14 +326,16 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
     // partial rhs sums in the reference's order: rhs[2] = div + ((sn + sf) + sv),
     // rhs[4] = div + ((((sn + sd) + sf) + sv) + svis)  (solver.cpp:442-445)
     double Ps2 = 0.0, Ps3 = 0.0, Pf4 = 0.0, Pf5 = 0.0, visc = 0.0;
+    mbar_wait(&barc, iter & 1u);
+    const int cidx = threadIdx.x;  // (ty*TX + tx) of this thread's Phase-3 cell
     if (p3 && !P.adv_only) {
         const int bk = (threadIdx.x / TX + 2) * W2 + (threadIdx.x % TX + 2);
-        const double nX = __ldg(geo + G_NX * fs + o3), nY = __ldg(geo + G_NY * fs + o3);
-        const double dXx = __ldg(geo + G_DNX_DXI * fs + o3), dYx = __ldg(geo + G_DNY_DXI * fs + o3);
-        const double dZx = __ldg(geo + G_DNZ_DXI * fs + o3), dXy = __ldg(geo + G_DNX_DETA * fs + o3);
-        const double dYy = __ldg(geo + G_DNY_DETA * fs + o3), dZy = __ldg(geo + G_DNZ_DETA * fs + o3);
+        const double nX = Cg[0 * TX * TY + cidx], nY = Cg[1 * TX * TY + cidx];
+        const double dXx = Cg[2 * TX * TY + cidx], dYx = Cg[3 * TX * TY + cidx];
+        const double dZx = Cg[4 * TX * TY + cidx], dXy = Cg[5 * TX * TY + cidx];
+        const double dYy = Cg[6 * TX * TY + cidx], dZy = Cg[7 * TX * TY + cidx];
         const double nZ = G[G_NZ * BOX + bk];
-        const Rcp rnz = mkrcp_const<FD>(nZ, __ldg(geo + G_RNZ * fs + o3));
+        const Rcp rnz = mkrcp_const<FD>(nZ, Cg[8 * TX * TY + cidx]);
         const double jb = G[G_JB * BOX + bk];
         const Rcp rj = mkrcp_const<FD>(jb, G[G_RJB * BOX + bk]);
         const double a11 = G[G_A11 * BOX + bk], a12 = G[G_A12 * BOX + bk];
@@ -520,11 +532,12 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
         if (P.cap_on) {
             const double qx = un[2], qy = un[3];
             if (!(qx == 0.0 && qy == 0.0)) {
-                const double nX = __ldg(geo + G_NX * fs + o3), nY = __ldg(geo + G_NY * fs + o3);
-                const double dXx = __ldg(geo + G_DNX_DXI * fs + o3), dYx = __ldg(geo + G_DNY_DXI * fs + o3);
-                const double dZx = __ldg(geo + G_DNZ_DXI * fs + o3), dXy = __ldg(geo + G_DNX_DETA * fs + o3);
-                const double dYy = __ldg(geo + G_DNY_DETA * fs + o3), dZy = __ldg(geo + G_DNZ_DETA * fs + o3);
-                const Rcp rnz = mkrcp_const<FD>(nZ, __ldg(geo + G_RNZ * fs + o3));
+                const int ci = threadIdx.x;
+                const double nX = Cg[0 * TX * TY + ci], nY = Cg[1 * TX * TY + ci];
+                const double dXx = Cg[2 * TX * TY + ci], dYx = Cg[3 * TX * TY + ci];
+                const double dZx = Cg[4 * TX * TY + ci], dXy = Cg[5 * TX * TY + ci];
+                const double dYy = Cg[6 * TX * TY + ci], dZy = Cg[7 * TX * TY + ci];
+                const Rcp rnz = mkrcp_const<FD>(nZ, Cg[8 * TX * TY + ci]);
                 bool okc = rj.ok;
                 double hs = dq<FD>(un[0], rj, okc);
                 double jx = dq<FD>(qx, rj, okc), jy = dq<FD>(qy, rj, okc);
@@ -602,7 +615,8 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
         t[2 * p + 0] = in;
         t[2 * p + 1] = outf;
     }
-    __syncthreads();  // FX/FY/V/PJ/BR are rewritten by the next tile
+    __syncthreads();  // FX/FY/V/PJ/BR/cell box are rewritten by the next tile
+    if (threadIdx.x == 0) issue_cell(tile + gridDim.x);
     }  // tile loop
 
     if (CORR) lam_block_max(lam_local, sc);

@@ -17,7 +17,11 @@ constexpr int SM_PJ = SM_V + 4 * BOX;                     // [BOX] jb*h*p_bar_f
 constexpr int SM_BR = SM_PJ + BOX;                        // [3][BOX] viscous brackets
 constexpr int SM_FX = SM_BR + 3 * BOX;                    // [6][NFX] xi face fluxes
 constexpr int SM_FY = SM_FX + 6 * NFX;                    // [6][NFY] eta face fluxes
-constexpr int SM_END = SM_FY + 6 * NFY;
+constexpr int SM_C = (((SM_FY + 6 * NFY) * 8 + 127) / 128) * 16;  // [NGCELL][TY][TX] per-cell geometry (TMA)
+constexpr int NGCELL = G_COUNT - NGBOX;                   // nX, nY, 6 x dn, RN(1/nZ)
+constexpr int SM_END = SM_C + NGCELL * TX * TY;
+constexpr unsigned kTmaCellBytes = NGCELL * TX * TY * 8;
+static_assert((SM_C * 8) % 128 == 0, "cell-geometry TMA box must be 128-byte aligned");
 constexpr unsigned kTmaBytes = (6 + NGBOX) * BOX * 8;
 
 __device__ __forceinline__ double ldg(const double* p) { return __ldg(p); }

@@ -21,9 +21,10 @@ for ln in dis:
 # phase boundaries from markers in the source
 marks = {}
 for i, l in enumerate(src, 1):
-    for key in ("Phase 1:", "Phase 2:", "Phase 3:", "boundary mass tally", "dry-tile fast path", "tile loop"):
+    for key in ("// ---- Phase 1:", "// ---- Phase 2:", "// ---- Phase 3:", "// ---- boundary mass tally",
+                "// ---- dry-tile fast path"):
         if key in l and key not in marks:
-            marks[key] = i
+            marks[key.replace("// ---- ", "")] = i
 start_kernel = [i for i, l in enumerate(src, 1) if "__global__ void __launch_bounds__(NT, 2) stage_kernel" in l][0]
 def phase(line):
     if line is None: return "?"
