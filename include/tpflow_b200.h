@@ -131,6 +131,9 @@ int tp_device_state(tp_ctx* c, int buf, void** ptr, long* pitch, long* field_str
 /* diagnostic: checks the FASTDIV division identity on n random operand pairs on
  * `device`; *mismatches = number of quotients differing from IEEE a/b (expect 0) */
 int tp_selftest_division(int device, long n, unsigned long long seed, unsigned long long* mismatches);
+/* diagnostic: out[k] = the device minmod limited_slope(a[k], b[k]) (solver.hpp:17-21)
+ * for n host operand pairs, so tests can compare it with the reference bit for bit */
+int tp_selftest_minmod(int device, long n, const double* a, const double* b, double* out);
 /* number of kernels launched by the last tp_steps call (graph replays included) */
 long tp_kernel_launches(const tp_ctx* c);
 

@@ -69,6 +69,7 @@ SIGNATURES = {
     "tp_device_state": (C.c_int, [_vp, C.c_int, C.POINTER(_vp), _lp, _lp]),
     "tp_kernel_launches": (C.c_long, [_vp]),
     "tp_selftest_division": (C.c_int, [C.c_int, C.c_long, C.c_ulonglong, C.POINTER(C.c_ulonglong)]),
+    "tp_selftest_minmod": (C.c_int, [C.c_int, C.c_long, _dp, _dp, _dp]),
 }
 
 

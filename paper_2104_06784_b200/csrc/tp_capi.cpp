@@ -38,6 +38,7 @@ cudaError_t init_kernels();
 cudaError_t init_pair_kernels();
 cudaError_t launch_stage_pair(const StageArgs& a, bool fastdiv, bool corr, cudaStream_t st);
 cudaError_t selftest_division(long long n, unsigned long long seed, unsigned long long* mismatches);
+cudaError_t selftest_minmod(long long n, const double* a, const double* b, double* out);
 }  // namespace tpb
 
 using tpb::DevScalars;
@@ -1063,6 +1064,12 @@ int tp_device_state(tp_ctx* c, int buf, void** ptr, long* pitch, long* field_str
 int tp_selftest_division(int device, long n, unsigned long long seed, unsigned long long* mismatches) {
     if (cudaSetDevice(device) != cudaSuccess) return TP_ERR_CUDA;
     return tpb::selftest_division(n, seed, mismatches) == cudaSuccess ? TP_OK : TP_ERR_CUDA;
+}
+
+int tp_selftest_minmod(int device, long n, const double* a, const double* b, double* out) {
+    if (n <= 0 || !a || !b || !out) return TP_ERR_INTERNAL;
+    if (cudaSetDevice(device) != cudaSuccess) return TP_ERR_CUDA;
+    return tpb::selftest_minmod(n, a, b, out) == cudaSuccess ? TP_OK : TP_ERR_CUDA;
 }
 
 long tp_kernel_launches(const tp_ctx* c) { return c ? c->launches : 0; }

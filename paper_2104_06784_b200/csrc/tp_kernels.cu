@@ -993,6 +993,23 @@ __global__ void selftest_div_kernel(long long n, unsigned long long seed, unsign
     }
     if (local) atomicAdd(bad, local);
 }
+// minmod (limited_slope) on device for n operand pairs; the caller compares with the
+// reference's branch structure on the host (tests/test_gpu_parity.py).
+__global__ void selftest_minmod_kernel(long long n, const double* a, const double* b, double* out) {
+    long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (i < n) out[i] = limited_slope(a[i], b[i]);
+}
+cudaError_t selftest_minmod(long long n, const double* a, const double* b, double* out) {
+    double* d = nullptr;
+    cudaError_t e = cudaMalloc(&d, 3 * n * sizeof(double) + 8);
+    if (e != cudaSuccess) return e;
+    cudaMemcpy(d, a, n * sizeof(double), cudaMemcpyHostToDevice);
+    cudaMemcpy(d + n, b, n * sizeof(double), cudaMemcpyHostToDevice);
+    selftest_minmod_kernel<<<static_cast<unsigned>((n + 255) / 256), 256>>>(n, d, d + n, d + 2 * n);
+    e = cudaMemcpy(out, d + 2 * n, n * sizeof(double), cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    return e;
+}
 cudaError_t selftest_division(long long n, unsigned long long seed, unsigned long long* mismatches) {
     unsigned long long* d = nullptr;
     cudaError_t e = cudaMalloc(&d, sizeof(unsigned long long));
