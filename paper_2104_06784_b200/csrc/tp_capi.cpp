@@ -35,8 +35,7 @@ cudaError_t launch_post(const PostArgs& a, cudaStream_t st);
 cudaError_t launch_regularize(const GridDesc& g, const Phys& P, double* s, const double* geo,
                               DevScalars* sc, bool fastdiv, cudaStream_t st);
 cudaError_t init_kernels();
-cudaError_t init_pair_kernels();
-cudaError_t launch_stage_pair(const StageArgs& a, bool fastdiv, bool corr, cudaStream_t st);
+cudaError_t launch_tiles(const TileArgs& a, cudaStream_t st);
 cudaError_t selftest_division(long long n, unsigned long long seed, unsigned long long* mismatches);
 cudaError_t selftest_minmod(long long n, const double* a, const double* b, double* out);
 }  // namespace tpb
@@ -127,7 +126,12 @@ struct tp_ctx {
     // options / flags
     bool fastdiv = true;
     int graph_steps = 16;
-    int kernel = 2;  // 2 = stage_kernel (one thread per face/cell), 3 = stage_pair_kernel (lane pairs)
+    bool skip_dry = true;  // list only tiles that are not bitwise no-ops (tiles_kernel)
+    unsigned char* dFlagA = nullptr;  // per-tile "interior has a nonzero bit" of A / B (1 = unknown)
+    unsigned char* dFlagB = nullptr;
+    int* dTiles = nullptr;            // active-tile list of the stage in flight + its count
+    int* dNact = nullptr;             // [2] list counts: predictor, corrector
+    int last_tiles_stage = 1;         // stage of the last tiles_kernel enqueued (0 pred, 1 corr)
     bool lam_valid = false;
     bool ghosts_in_B = false;
     bool inflow_active = false;
@@ -231,11 +235,50 @@ tpb::StageArgs stage_args(tp_ctx* c, bool corr, int loop) {
     a.nty = c->nty;
     a.loop = loop;
     a.use_sc_dt = 1;
+    a.tiles = c->dTiles;
+    a.ntiles_active = c->dNact + (corr ? 1 : 0);
+    a.flag_out = corr ? c->dFlagA : c->dFlagB;
     return a;
 }
 
+// Both stage launches go through here: the active-tile list (tiles_kernel), then the stage.
 cudaError_t launch_stage_sel(tp_ctx* c, const tpb::StageArgs& a, bool fastdiv, bool corr, cudaStream_t st) {
-    return c->kernel == 3 ? tpb::launch_stage_pair(a, fastdiv, corr, st) : tpb::launch_stage(a, fastdiv, corr, st);
+    tpb::TileArgs t{};
+    t.flag_in = corr ? c->dFlagB : c->dFlagA;
+    t.flag_out = corr ? c->dFlagA : c->dFlagB;
+    t.tiles = c->dTiles;
+    t.ntiles_active = c->dNact + (corr ? 1 : 0);
+    t.ntiles_reset = c->dNact + (corr ? 0 : 1);
+    t.tally = a.tally;
+    t.ntx = c->ntx;
+    t.nty = c->nty;
+    t.skip = c->skip_dry ? 1 : 0;
+    // ring boxes read ghost cells: only plain zero-gradient copies refreshed right before
+    // the stage (the device loop) keep the 3x3 flag rule exact
+    t.ring_ineligible = (c->inflow_active || !a.loop) ? 1 : 0;
+    t.south_ineligible = c->g.has_south ? 0 : 1;
+    t.north_ineligible = c->g.has_north ? 0 : 1;
+    t.loop = a.loop;
+    t.sc = c->dSc;
+    // each tiles_kernel zeroes the other stage's counter; two launches of one stage in a
+    // row (a bare tp_stage call) need an explicit reset
+    const int stage = corr ? 1 : 0;
+    if (c->last_tiles_stage == stage) {
+        cudaError_t e0 = cudaMemsetAsync(t.ntiles_active, 0, sizeof(int), st);
+        if (e0 != cudaSuccess) return e0;
+    }
+    c->last_tiles_stage = stage;
+    cudaError_t e = tpb::launch_tiles(t, st);
+    if (e != cudaSuccess) return e;
+    return tpb::launch_stage(a, fastdiv, corr, st);
+}
+
+// Conservative reset of the per-tile flags (after any write to a state buffer that is
+// not a stage kernel): every tile is listed until a stage recomputes its flag.
+void invalidate_flags(tp_ctx* c, bool a_buf, bool b_buf) {
+    const size_t n = static_cast<size_t>(c->ntx) * c->nty;
+    if (a_buf) ck(cudaMemsetAsync(c->dFlagA, 1, n, c->stream), "flags");
+    if (b_buf) ck(cudaMemsetAsync(c->dFlagB, 1, n, c->stream), "flags");
 }
 
 void launch_bc(tp_ctx* c, int buf, int tsrc, double t, int loop) {
@@ -274,18 +317,22 @@ void enqueue_loop_step(tp_ctx* c) {
 
 cudaGraphExec_t capture_steps(tp_ctx* c, int k) {
     cudaGraph_t graph = nullptr;
+    const int saved_stage = c->last_tiles_stage;
+    c->last_tiles_stage = 1;  // a replay always follows a corrector (tp_steps resets otherwise)
     ck(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal), "begin capture");
     try {
         for (int s = 0; s < k; ++s) enqueue_loop_step(c);
     } catch (...) {
         cudaStreamEndCapture(c->stream, &graph);
         if (graph) cudaGraphDestroy(graph);
+        c->last_tiles_stage = saved_stage;
         throw;
     }
     ck(cudaStreamEndCapture(c->stream, &graph), "end capture");
     cudaGraphExec_t exec = nullptr;
     ck(cudaGraphInstantiate(&exec, graph, 0), "graph instantiate");
     cudaGraphDestroy(graph);
+    c->last_tiles_stage = saved_stage;
     return exec;
 }
 
@@ -389,6 +436,7 @@ std::vector<double> host_state(tp_ctx* c) {
 
 void set_host_state(tp_ctx* c, const std::vector<double>& s) {
     upload_state(c, c->dA, s.data());
+    invalidate_flags(c, true, false);
     ck(cudaStreamSynchronize(c->stream), "sync");
     c->lam_valid = false;
     c->ghosts_in_B = false;
@@ -425,7 +473,6 @@ void create_impl(tp_ctx* c, const tp_params* p, const tp_dem* dem, int row0, int
     c->device = p->device;
     ck(cudaSetDevice(c->device), "cudaSetDevice");
     ck(tpb::init_kernels(), "init kernels");
-    ck(tpb::init_pair_kernels(), "init pair kernels");
     c->ncols = dem->ncols;
     c->nrows_g = dem->nrows;
     c->row0 = row0;
@@ -480,6 +527,13 @@ void create_impl(tp_ctx* c, const tp_params* p, const tp_dem* dem, int row0, int
     ck(cudaMemsetAsync(c->rawB, 0, sbytes, c->stream), "memset");
     ck(cudaMemsetAsync(c->dTallyP, 0, tb, c->stream), "memset");
     ck(cudaMemsetAsync(c->dTallyC, 0, tb, c->stream), "memset");
+    const size_t ntiles = static_cast<size_t>(c->ntx) * c->nty;
+    ck(cudaMalloc(&c->dFlagA, ntiles), "cudaMalloc flags");
+    ck(cudaMalloc(&c->dFlagB, ntiles), "cudaMalloc flags");
+    ck(cudaMalloc(&c->dTiles, sizeof(int) * ntiles), "cudaMalloc tiles");
+    ck(cudaMalloc(&c->dNact, 2 * sizeof(int)), "cudaMalloc tiles");
+    ck(cudaMemsetAsync(c->dNact, 0, 2 * sizeof(int), c->stream), "memset");
+    invalidate_flags(c, true, true);
     {
         // device geometry layout (tp_types.h GeoField): the 14 reference fields
         // regrouped + RN(1/jb), RN(1/nZ) and the face RN(1/jbf) of the whole grid
@@ -569,6 +623,10 @@ void tp_destroy(tp_ctx* c) {
     cudaFree(c->dSide);
     cudaFree(c->dSamples);
     cudaFree(c->dDts);
+    cudaFree(c->dFlagA);
+    cudaFree(c->dFlagB);
+    cudaFree(c->dTiles);
+    cudaFree(c->dNact);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
     delete c;
 }
@@ -607,9 +665,8 @@ int tp_set_option(tp_ctx* c, const char* key, long value) {
         if (k == "fastdiv") {
             c->fastdiv = value != 0;
             drop_graphs(c);
-        } else if (k == "kernel") {
-            if (value != 2 && value != 3) throw ConfigErr{"kernel must be 2 or 3"};
-            c->kernel = static_cast<int>(value);
+        } else if (k == "skip_dry") {
+            c->skip_dry = value != 0;
             drop_graphs(c);
         } else if (k == "graph_steps") {
             if (value < 1 || value > 4096) throw ConfigErr{"graph_steps must be in [1, 4096]"};
@@ -761,6 +818,7 @@ int tp_get_state(tp_ctx* c, double* out) {
 int tp_set_state(tp_ctx* c, const double* in) {
     TP_GUARD(c, {
         upload_state(c, c->dA, in);
+        invalidate_flags(c, true, false);
         ck(cudaStreamSynchronize(c->stream), "sync");
         c->lam_valid = false;
         c->ghosts_in_B = false;
@@ -808,6 +866,7 @@ int tp_regularize(tp_ctx* c) {
         sync_ghosts(c);
         ck(tpb::launch_regularize(c->g, c->ph, c->dA, c->dGeo, c->dSc, c->fastdiv, c->stream),
            "regularize_kernel");
+        invalidate_flags(c, true, false);
         c->lam_valid = false;
         check_error(c, c->dA);
     })
@@ -849,12 +908,15 @@ int tp_steps(tp_ctx* c, double t_next, double t_end, long max_steps, double* t, 
             c->graph1 = capture_steps(c, 1);
             c->graphK_steps = c->graph_steps;
         }
+        if (c->last_tiles_stage == 0)  // the graphs start with a predictor list
+            ck(cudaMemsetAsync(c->dNact, 0, sizeof(int), c->stream), "memset");
+        c->last_tiles_stage = 1;
         long long done_steps = 0;
         DevScalars h{};
         for (;;) {
             const bool big = (max_steps - done_steps) >= c->graph_steps;
             ck(cudaGraphLaunch(big ? c->graphK : c->graph1, c->stream), "graph launch");
-            c->launches += 6L * (big ? c->graph_steps : 1);
+            c->launches += 8L * (big ? c->graph_steps : 1);
             h = read_scalars(c);
             done_steps = h.steps;
             if (h.done) break;
@@ -1055,6 +1117,11 @@ int tp_synchronize(tp_ctx* c) { TP_GUARD(c, ck(cudaStreamSynchronize(c->stream),
 
 int tp_device_state(tp_ctx* c, int buf, void** ptr, long* pitch, long* field_stride) {
     if (!c) return TP_ERR_INTERNAL;
+    try {
+        invalidate_flags(c, buf == 0, buf != 0);  // the caller may write through the pointer
+    } catch (...) {
+        return TP_ERR_CUDA;
+    }
     *ptr = buf ? c->dB : c->dA;
     *pitch = c->pitch;
     *field_stride = static_cast<long>(c->fs);

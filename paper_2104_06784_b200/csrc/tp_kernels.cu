@@ -30,7 +30,7 @@ namespace tpb {
 // regularize + [check_finite + lambda] + store of one updated cell: the tail of
 // advance_step's stages (solver.cpp:139-166, :482-494, :556-573).
 template <bool FD, bool CORR>
-__device__ __forceinline__ void cell_epilogue(double (&un)[6], const Rcp& rj, double nZ, int X, int Y,
+__device__ __forceinline__ unsigned long long cell_epilogue(double (&un)[6], const Rcp& rj, double nZ, int X, int Y,
                                               const Phys& P, DevScalars* sc, double& lam_local,
                                               double* out, long long fs, long long o3) {
     // regularize (solver.cpp:139-166), solid then fluid
@@ -105,8 +105,13 @@ __device__ __forceinline__ void cell_epilogue(double (&un)[6], const Rcp& rj, do
         }
     }
 
+    unsigned long long bits = 0ull;
 #pragma unroll
-    for (int f = 0; f < 6; ++f) out[f * fs + o3] = un[f];
+    for (int f = 0; f < 6; ++f) {
+        out[f * fs + o3] = un[f];
+        bits |= static_cast<unsigned long long>(__double_as_longlong(un[f]));
+    }
+    return bits;  // feeds the tile's output flag
 }
 
 
@@ -118,6 +123,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
     extern __shared__ __align__(128) double sm[];
     __shared__ unsigned long long bar;   // state + stencil-geometry boxes
     __shared__ unsigned long long barc;  // per-cell geometry box
+    __shared__ int s_tile;               // list entry of the next tile (read by thread 0 at issue time)
     const double* Cg = sm + SM_C;        // [NGCELL][TY][TX]: nX, nY, dnX/dxi, dnY/dxi, dnZ/dxi, dnX/deta, dnY/deta, dnZ/deta, RN(1/nZ)
     double* S = sm + SM_S;
     const double* G = sm + SM_G;
@@ -136,34 +142,40 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
     const double* __restrict__ geo = A.geo;
     const long long fs = g.fs;
     const int ntiles = A.ntx * A.nty;
+    const int nact = *A.ntiles_active;  // active-tile list of this stage (tiles_kernel)
     const double dt = sc->dt;
 
     // Persistent tiles: block b walks tiles b, b+G, b+2G, ... (row-major, so the
     // tiles in flight at any time are neighbours and share halos in L2).  The
     // next tile's TMA is issued as soon as the current tile's staged boxes are
     // dead (after Phase 2), so it lands while Phase 3 computes.
-    int tile = blockIdx.x;
-    auto issue_cell = [&](int t) {  // per-cell geometry of tile t (thread 0)
-        if (t < ntiles) {
+    auto issue_cell = [&](int li) {  // per-cell geometry of list entry li (thread 0)
+        if (li < nact) {
+            const int t = A.tiles[li];
             mbar_expect_tx(&barc, kTmaCellBytes);
             tma_load_3d(sm + SM_C, &A.tm_c, 3 + (t % A.ntx) * TX + 1, 3 + (t / A.ntx) * TY, G_NX, &barc);
         }
     };
+    (void)ntiles;
     if (threadIdx.x == 0) {
         mbar_init(&bar, 1);
         mbar_init(&barc, 1);
-        if (tile < ntiles) {
+        if (static_cast<int>(blockIdx.x) < nact) {
+            const int tile = A.tiles[blockIdx.x];
+            s_tile = tile;
             const int bx0 = 1 + (tile % A.ntx) * TX, by0 = 1 + (tile / A.ntx) * TY;
             mbar_expect_tx(&bar, kTmaBytes);
             // x coordinate + 1: the leading pad column of the device layout (tp_capi.cpp)
             tma_load_3d(S, &A.tm_s, bx0 + 1, by0, 0, &bar);
             tma_load_3d(sm + SM_G, &A.tm_g, bx0 + 1, by0, 0, &bar);
-            issue_cell(tile);
+            issue_cell(blockIdx.x);
         }
     }
     __syncthreads();  // barrier init visible to all threads
     double lam_local = 0.0;
-    for (unsigned iter = 0; tile < ntiles; tile += gridDim.x, ++iter) {
+    unsigned iter = 0;
+    for (int li = blockIdx.x; li < nact; li += gridDim.x, ++iter) {
+    const int tile = s_tile;  // written by thread 0 before the previous end-of-tile barrier
     const int tix = tile % A.ntx, tiy = tile / A.ntx;
     const int X0 = 3 + tix * TX;
     const int Y0 = 3 + tiy * TY;
@@ -171,32 +183,24 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
     const int p3x = X0 + (threadIdx.x % TX), p3y = Y0 + (threadIdx.x / TX);
     const bool p3 = threadIdx.x < TX * TY && p3x <= nx - 4 && p3y <= ny - 4;
     const long long o3 = static_cast<long long>(p3y) * pitch + p3x;
-    if (iter == 0 && p3) {  // later tiles were prefetched during the previous Phase 3
-        if (CORR) {
+    // u^n of this thread's cell is read in Phase 3: warm L2 now (corrector)
+    if (CORR && p3) {
 #pragma unroll
-            for (int f = 0; f < 6; ++f) prefetch_l2(A.u0 + f * fs + o3);
-        }
+        for (int f = 0; f < 6; ++f) prefetch_l2(A.u0 + f * fs + o3);
     }
-    // next tile's boxes into S/G (call only once they are dead) + L2 warm-up of
-    // its per-cell fields for Phase 3
+    // thread 0 fetches the next list entry now; it is consumed at issue time
+    const int nli = li + gridDim.x;
+    const int next_tile = (threadIdx.x == 0 && nli < nact) ? A.tiles[nli] : 0;
+    // next tile's boxes into S/G (call only once they are dead)
     auto issue_next = [&]() {
-            const int nt = tile + gridDim.x;
-            if (nt < ntiles) {
-                const int bx0n = 1 + (nt % A.ntx) * TX, by0n = 1 + (nt / A.ntx) * TY;
-                if (threadIdx.x == 0) {
-                    mbar_expect_tx(&bar, kTmaBytes);
-                    tma_load_3d(S, &A.tm_s, bx0n + 1, by0n, 0, &bar);
-                    tma_load_3d(sm + SM_G, &A.tm_g, bx0n + 1, by0n, 0, &bar);
-                }
-                const int qx = bx0n + 2 + (threadIdx.x % TX), qy = by0n + 2 + (threadIdx.x / TX);
-                if (threadIdx.x < TX * TY && qx <= nx - 4 && qy <= ny - 4) {
-                    const long long oq = static_cast<long long>(qy) * pitch + qx;
-                    if (CORR) {
-    #pragma unroll
-                        for (int f = 0; f < 6; ++f) prefetch_l2(A.u0 + f * fs + oq);
-                    }
-                }
-            }
+        if (threadIdx.x == 0 && nli < nact) {
+            const int nt = next_tile;
+            s_tile = nt;
+            const int bx0n = 1 + (nt % A.ntx) * TX, by0n = 1 + (nt / A.ntx) * TY;
+            mbar_expect_tx(&bar, kTmaBytes);
+            tma_load_3d(S, &A.tm_s, bx0n + 1, by0n, 0, &bar);
+            tma_load_3d(sm + SM_G, &A.tm_g, bx0n + 1, by0n, 0, &bar);
+        }
     };
     mbar_wait(&bar, iter & 1u);
 
@@ -217,8 +221,9 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
             issue_next();
             if (threadIdx.x == 0) {  // retire this tile's cell box, stage the next one
                 mbar_wait(&barc, iter & 1u);
-                issue_cell(tile + gridDim.x);
+                issue_cell(li + gridDim.x);
             }
+            unsigned long long obits = 0ull;
             if (p3) {
                 if (!CORR) {
 #pragma unroll
@@ -228,11 +233,14 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
 #pragma unroll
                     for (int f = 0; f < 6; ++f) un[f] = 0.5 * (A.u0[f * fs + o3] + 0.0);
                     const Rcp rj0 = mkrcp_const<FD>(jb0, rjb0);
-                    cell_epilogue<FD, CORR>(un, rj0, nz0, p3x, p3y, P, sc, lam_local, A.out, fs, o3);
+                    obits = cell_epilogue<FD, CORR>(un, rj0, nz0, p3x, p3y, P, sc, lam_local, A.out, fs, o3);
                 }
             }
             if ((tix == 0 || tix == A.ntx - 1 || tiy == 0 || tiy == A.nty - 1) && threadIdx.x < 4)
                 A.tally[4ll * tile + threadIdx.x] = 0.0;
+            // (the barrier also publishes s_tile, written in issue_next)
+            const int nzo = __syncthreads_or(obits != 0ull);
+            if (threadIdx.x == 0) A.flag_out[tile] = nzo ? 1 : 0;
             continue;
         }
     }
@@ -469,6 +477,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
     //      regularize + [finite, lambda]
     const Rcp rdx = mkrcp_const<FD>(P.dxi, P.r_dxi);
     const Rcp rdy = mkrcp_const<FD>(P.deta, P.r_deta);
+    unsigned long long obits = 0ull;
     if (p3) {
         const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
         const int X = p3x, Y = p3y;
@@ -583,7 +592,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
             for (int f = 0; f < 6; ++f) un[f] = 0.5 * (A.u0[f * fs + o3] + un[f]);
         }
 
-        cell_epilogue<FD, CORR>(un, rj, nZ, X, Y, P, sc, lam_local, A.out, fs, o3);
+        obits = cell_epilogue<FD, CORR>(un, rj, nZ, X, Y, P, sc, lam_local, A.out, fs, o3);
     }
 
     // ---- boundary mass tally of this stage (solver.cpp:352-376), ring tiles only
@@ -615,11 +624,57 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
         t[2 * p + 0] = in;
         t[2 * p + 1] = outf;
     }
-    __syncthreads();  // FX/FY/V/PJ/BR/cell box are rewritten by the next tile
-    if (threadIdx.x == 0) issue_cell(tile + gridDim.x);
+    // FX/FY/V/PJ/BR/cell box are rewritten by the next tile; the barrier also
+    // reduces the tile's output flag
+    const int nzo = __syncthreads_or(obits != 0ull);
+    if (threadIdx.x == 0) {
+        A.flag_out[tile] = nzo ? 1 : 0;
+        issue_cell(li + gridDim.x);
+    }
     }  // tile loop
 
     if (CORR) lam_block_max(lam_local, sc);
+}
+
+// ---------------------------------------------------------------------------
+// Active-tile list of one stage (see TileArgs).  One thread per tile; the list is
+// appended warp by warp, so it stays row-major within each warp's 32 tiles.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(NT) tiles_kernel(TileArgs a) {
+    if (a.loop && *(volatile int*)&a.sc->done) return;
+    const int ntiles = a.ntx * a.nty;
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    bool active = false;
+    if (t < ntiles) {
+        const int tx = t % a.ntx, ty = t / a.ntx;
+        const bool ring = tx == 0 || tx == a.ntx - 1 || ty == 0 || ty == a.nty - 1;
+        bool skip = a.skip && a.flag_out[t] == 0;
+        if (ring && a.ring_ineligible) skip = false;
+        if (ty == 0 && a.south_ineligible) skip = false;
+        if (ty == a.nty - 1 && a.north_ineligible) skip = false;
+        for (int dy = -1; dy <= 1 && skip; ++dy) {
+            const int y = ty + dy;
+            if (y < 0 || y >= a.nty) continue;
+            for (int dx = -1; dx <= 1; ++dx) {
+                const int x = tx + dx;
+                if (x >= 0 && x < a.ntx && a.flag_in[y * a.ntx + x]) skip = false;
+            }
+        }
+        active = !skip;
+        if (skip && ring) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) a.tally[4ll * t + q] = 0.0;
+        }
+    }
+    // the other stage's counter was consumed by the stage before this one and is
+    // appended to only after this stage: reset it here (saves a memset node)
+    if (t == 0) *a.ntiles_reset = 0;
+    const unsigned m = __ballot_sync(0xffffffffu, active);
+    const int lane = threadIdx.x & 31;
+    int base = 0;
+    if (lane == 0 && m) base = atomicAdd(a.ntiles_active, __popc(m));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (active) a.tiles[base + __popc(m & ((1u << lane) - 1u))] = t;
 }
 
 // ---------------------------------------------------------------------------
@@ -878,9 +933,15 @@ size_t stage_smem_bytes() { return sizeof(double) * SM_END; }
 static int g_num_sms = 148;
 template <bool FD, bool CORR>
 static cudaError_t launch_stage_t(const StageArgs& a, cudaStream_t st) {
-    const int ntiles = a.ntx * a.nty;
+    const int ntiles = a.ntx * a.nty;  // upper bound of the active list
     dim3 grid(ntiles < 2 * g_num_sms ? ntiles : 2 * g_num_sms);
     stage_kernel<FD, CORR><<<grid, NT, stage_smem_bytes(), st>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_tiles(const TileArgs& a, cudaStream_t st) {
+    const int n = a.ntx * a.nty;
+    tiles_kernel<<<(n + NT - 1) / NT, NT, 0, st>>>(a);
     return cudaGetLastError();
 }
 

@@ -111,6 +111,30 @@ struct StageArgs {
     int ntx, nty;
     int loop;                        // 1 = obey sc->done (device-resident loop)
     int use_sc_dt;                   // read dt from sc (always 1 in practice)
+    // active-tile list of this stage (TileArgs below); tiles not listed are bitwise no-ops
+    const int* __restrict__ tiles;   // [ntiles] tile indices, count in *ntiles_active
+    const int* ntiles_active;
+    unsigned char* flag_out;         // per-tile "output interior has a nonzero bit" of `out`
+};
+
+// Dry-tile classification before a stage.  flag_in: per-tile flags of the stage's input
+// buffer (the radius-2 box reads interior cells of the 3x3 tile neighbourhood only);
+// flag_out: flags of its output buffer.  A tile whose 3x3 input neighbourhood and whose
+// own output are all +0.0 bits is a bitwise no-op: it is left off the
+// list (its ring tally slot is zeroed here).  Flags are conservative: 1 = unknown.
+struct TileArgs {
+    const unsigned char* flag_in;
+    const unsigned char* flag_out;
+    int* tiles;
+    int* ntiles_active;   // this stage's counter (zeroed by the other stage's tiles_kernel)
+    int* ntiles_reset;    // the other stage's counter
+    double* tally;
+    int ntx, nty;
+    int skip;             // 0 = list every tile
+    int ring_ineligible;  // 1 = ring tiles read non-copy ghosts (Mode-II inflow): never skip them
+    int south_ineligible, north_ineligible;  // slab edges next to halo rows: never skip
+    int loop;
+    DevScalars* sc;
 };
 
 struct BcArgs {

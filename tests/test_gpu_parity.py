@@ -193,14 +193,14 @@ def test_signed_zero_state(gpu, oracle_kind):
 
 @pytest.mark.parametrize("make", [lambda: scenarios.c1_hill(96), lambda: scenarios.wet_valley(96, 80),
                                   lambda: scenarios.c3_channel(96, 48, t_end=30.0, dt_out=0.5)])
-def test_pair_kernel_variant_bitwise(gpu, oracle_kind, make):
-    """option kernel=3 (stage_pair_kernel, lane-pair split) is bit-identical too."""
+def test_full_tile_list_bitwise(gpu, oracle_kind, make):
+    """option skip_dry=0 (every tile listed, no dry-tile skipping) is bit-identical too."""
     sc = make()
     ref, sim = _pair(sc, oracle_kind)
-    sim.set_option("kernel", 3)
+    sim.set_option("skip_dry", 0)
     t_next = 0.5 / sc.config.scaling.t_unit() if sc.config.inflow else 1e9
     tr, dts_r, _ = ref.steps(0.0, t_next, 80, t_end=1e9)
     tg, dts_g, _ = sim.steps(0.0, t_next, 80, t_end=1e9, record_dts=True)
     assert_bitwise(dts_g, dts_r, "dt sequence")
-    assert_bitwise(sim.state(), ref.state(), "pair-kernel state")
+    assert_bitwise(sim.state(), ref.state(), "full-list state")
     np.testing.assert_allclose(sim.audit_array(), ref.audit(), rtol=1e-12, atol=1e-300)
