@@ -14,6 +14,8 @@ import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libtpflow_b200.so")
+# development override (e.g. the `make timing` probe build); the product path is LIB_PATH
+LIB_PATH = os.environ.get("TPFLOW_B200_LIB", LIB_PATH)
 CSRC = os.path.join(HERE, "csrc")
 
 
@@ -70,6 +72,7 @@ SIGNATURES = {
     "tp_kernel_launches": (C.c_long, [_vp]),
     "tp_selftest_division": (C.c_int, [C.c_int, C.c_long, C.c_ulonglong, C.POINTER(C.c_ulonglong)]),
     "tp_selftest_minmod": (C.c_int, [C.c_int, C.c_long, _dp, _dp, _dp]),
+    "tp_debug_phase_cycles": (C.c_int, [C.POINTER(C.c_ulonglong), C.c_int]),
 }
 
 

@@ -38,6 +38,7 @@ cudaError_t init_kernels();
 cudaError_t launch_tiles(const TileArgs& a, cudaStream_t st);
 cudaError_t selftest_division(long long n, unsigned long long seed, unsigned long long* mismatches);
 cudaError_t selftest_minmod(long long n, const double* a, const double* b, double* out);
+cudaError_t phase_cycles(unsigned long long* out, int reset);
 }  // namespace tpb
 
 using tpb::DevScalars;
@@ -1137,6 +1138,10 @@ int tp_selftest_minmod(int device, long n, const double* a, const double* b, dou
     if (n <= 0 || !a || !b || !out) return TP_ERR_INTERNAL;
     if (cudaSetDevice(device) != cudaSuccess) return TP_ERR_CUDA;
     return tpb::selftest_minmod(n, a, b, out) == cudaSuccess ? TP_OK : TP_ERR_CUDA;
+}
+
+int tp_debug_phase_cycles(unsigned long long* out, int reset) {
+    return tpb::phase_cycles(out, reset) == cudaSuccess ? TP_OK : TP_ERR_CUDA;
 }
 
 long tp_kernel_launches(const tp_ctx* c) { return c ? c->launches : 0; }

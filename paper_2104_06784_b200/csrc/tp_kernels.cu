@@ -27,6 +27,31 @@
 
 namespace tpb {
 
+// Development probe (make timing): per-warp clock accumulation of the stage kernel's
+// phases and barrier waits; compiled out of the product build.
+#ifdef TP_PHASE_TIMING
+__device__ unsigned long long g_phase_cycles[2][14];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define TPROBE_DECL unsigned long long tp_acc[11] = {0}; long long tp_last = clock64(); \
+    const long long tp_c0 = tp_last; const unsigned long long tp_g0 = gtimer();
+#define TPROBE(k) do { const long long _n = clock64(); tp_acc[k] += _n - tp_last; tp_last = _n; } while (0)
+#define TPROBE_FLUSH(corr)                                                          \
+    if ((threadIdx.x & 31) == 0) {                                                  \
+        for (int _k = 0; _k < 11; ++_k) atomicAdd(&g_phase_cycles[corr][_k], tp_acc[_k]); \
+        atomicAdd(&g_phase_cycles[corr][11], 1ull);                                 \
+        atomicAdd(&g_phase_cycles[corr][12], static_cast<unsigned long long>(clock64() - tp_c0)); \
+        atomicAdd(&g_phase_cycles[corr][13], gtimer() - tp_g0);                    \
+    }
+#else
+#define TPROBE_DECL
+#define TPROBE(k) do { } while (0)
+#define TPROBE_FLUSH(corr)
+#endif
+
 // regularize + [check_finite + lambda] + store of one updated cell: the tail of
 // advance_step's stages (solver.cpp:139-166, :482-494, :556-573).
 template <bool FD, bool CORR>
@@ -149,11 +174,12 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
     // tiles in flight at any time are neighbours and share halos in L2).  The
     // next tile's TMA is issued as soon as the current tile's staged boxes are
     // dead (after Phase 2), so it lands while Phase 3 computes.
+    // list entries are packed (tile row << 16) | tile column (tiles_kernel)
     auto issue_cell = [&](int li) {  // per-cell geometry of list entry li (thread 0)
         if (li < nact) {
-            const int t = A.tiles[li];
+            const int e = A.tiles[li];
             mbar_expect_tx(&barc, kTmaCellBytes);
-            tma_load_3d(sm + SM_C, &A.tm_c, 3 + (t % A.ntx) * TX + 1, 3 + (t / A.ntx) * TY, G_NX, &barc);
+            tma_load_3d(sm + SM_C, &A.tm_c, 3 + (e & 0xffff) * TX + 1, 3 + (e >> 16) * TY, G_NX, &barc);
         }
     };
     (void)ntiles;
@@ -161,9 +187,9 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
         mbar_init(&bar, 1);
         mbar_init(&barc, 1);
         if (static_cast<int>(blockIdx.x) < nact) {
-            const int tile = A.tiles[blockIdx.x];
-            s_tile = tile;
-            const int bx0 = 1 + (tile % A.ntx) * TX, by0 = 1 + (tile / A.ntx) * TY;
+            const int e = A.tiles[blockIdx.x];
+            s_tile = e;
+            const int bx0 = 1 + (e & 0xffff) * TX, by0 = 1 + (e >> 16) * TY;
             mbar_expect_tx(&bar, kTmaBytes);
             // x coordinate + 1: the leading pad column of the device layout (tp_capi.cpp)
             tma_load_3d(S, &A.tm_s, bx0 + 1, by0, 0, &bar);
@@ -174,9 +200,11 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
     __syncthreads();  // barrier init visible to all threads
     double lam_local = 0.0;
     unsigned iter = 0;
+    TPROBE_DECL
     for (int li = blockIdx.x; li < nact; li += gridDim.x, ++iter) {
-    const int tile = s_tile;  // written by thread 0 before the previous end-of-tile barrier
-    const int tix = tile % A.ntx, tiy = tile / A.ntx;
+    const int entry = s_tile;  // written by thread 0 before the previous end-of-tile barrier
+    const int tix = entry & 0xffff, tiy = entry >> 16;
+    const int tile = tiy * A.ntx + tix;
     const int X0 = 3 + tix * TX;
     const int Y0 = 3 + tiy * TY;
     // the Phase-3 cell of this thread
@@ -190,61 +218,25 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
     }
     // thread 0 fetches the next list entry now; it is consumed at issue time
     const int nli = li + gridDim.x;
-    const int next_tile = (threadIdx.x == 0 && nli < nact) ? A.tiles[nli] : 0;
+    const int next_entry = (threadIdx.x == 0 && nli < nact) ? A.tiles[nli] : 0;
     // next tile's boxes into S/G (call only once they are dead)
     auto issue_next = [&]() {
         if (threadIdx.x == 0 && nli < nact) {
-            const int nt = next_tile;
-            s_tile = nt;
-            const int bx0n = 1 + (nt % A.ntx) * TX, by0n = 1 + (nt / A.ntx) * TY;
+            const int e = next_entry;
+            s_tile = e;
+            const int bx0n = 1 + (e & 0xffff) * TX, by0n = 1 + (e >> 16) * TY;
             mbar_expect_tx(&bar, kTmaBytes);
             tma_load_3d(S, &A.tm_s, bx0n + 1, by0n, 0, &bar);
             tma_load_3d(sm + SM_G, &A.tm_g, bx0n + 1, by0n, 0, &bar);
         }
     };
+    TPROBE(0);  // loop-top bookkeeping
     mbar_wait(&bar, iter & 1u);
-
-    // ---- dry-tile fast path.  If the whole radius-2 state box is +0.0 the stage
-    // is a bitwise no-op on the tile (every flux is the dry-face 0.0, every source
-    // and divergence term a signed zero that cancels to +0.0, regularize keeps
-    // +0.0; traced term by term in DESIGN.md §3).  The predictor then stores
-    // +0.0; the corrector still averages with u^n (un = +0.0 before the average).
-    {
-        unsigned long long acc = 0ull;
-        for (int k = threadIdx.x; k < 6 * BOX; k += NT)
-            acc |= static_cast<unsigned long long>(__double_as_longlong(S[k]));
-        const int bk0 = (threadIdx.x / TX + 2) * W2 + (threadIdx.x % TX + 2);
-        const double jb0 = p3 ? G[G_JB * BOX + bk0] : 1.0;
-        const double rjb0 = p3 ? G[G_RJB * BOX + bk0] : 1.0;
-        const double nz0 = p3 ? G[G_NZ * BOX + bk0] : 1.0;
-        if (!__syncthreads_or(acc != 0ull)) {
-            issue_next();
-            if (threadIdx.x == 0) {  // retire this tile's cell box, stage the next one
-                mbar_wait(&barc, iter & 1u);
-                issue_cell(li + gridDim.x);
-            }
-            unsigned long long obits = 0ull;
-            if (p3) {
-                if (!CORR) {
-#pragma unroll
-                    for (int f = 0; f < 6; ++f) A.out[f * fs + o3] = 0.0;
-                } else {
-                    double un[6];
-#pragma unroll
-                    for (int f = 0; f < 6; ++f) un[f] = 0.5 * (A.u0[f * fs + o3] + 0.0);
-                    const Rcp rj0 = mkrcp_const<FD>(jb0, rjb0);
-                    obits = cell_epilogue<FD, CORR>(un, rj0, nz0, p3x, p3y, P, sc, lam_local, A.out, fs, o3);
-                }
-            }
-            if ((tix == 0 || tix == A.ntx - 1 || tiy == 0 || tiy == A.nty - 1) && threadIdx.x < 4)
-                A.tally[4ll * tile + threadIdx.x] = 0.0;
-            // (the barrier also publishes s_tile, written in issue_next)
-            const int nzo = __syncthreads_or(obits != 0ull);
-            if (threadIdx.x == 0) A.flag_out[tile] = nzo ? 1 : 0;
-            continue;
-        }
-    }
-
+    TPROBE(1);  // wait for the state/geometry boxes
+    TPROBE(2);
+    TPROBE(3);
+    // (tiles whose radius-2 box is all +0.0 are bitwise no-ops; they are
+    // left off the list by tiles_kernel, and a listed dry tile computes the same +0.0)
 
     // ---- Phase 1: xi faces, eta faces, cell fields -----------------------------
     constexpr int NXP = ((NFX + 31) / 32) * 32;  // face lists padded to warp multiples
@@ -322,7 +314,9 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
             PJ[k] = jb * h * (G[G_NZ * BOX + k] * h * 0.5);  // solver.cpp:182
         }
     }
+    TPROBE(4);  // Phase 1 work
     __syncthreads();
+    TPROBE(5);  // Phase 1 barrier
 
     // ---- Phase 2: (a) the cell-local source terms of this thread's Phase-3 cell
     // (solver.cpp:406-445 minus the viscous divergence, which needs neighbours'
@@ -335,6 +329,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
     // rhs[4] = div + ((((sn + sd) + sf) + sv) + svis)  (solver.cpp:442-445)
     double Ps2 = 0.0, Ps3 = 0.0, Pf4 = 0.0, Pf5 = 0.0, visc = 0.0;
     mbar_wait(&barc, iter & 1u);
+    TPROBE(6);  // cell-geometry box wait
     const int cidx = threadIdx.x;  // (ty*TX + tx) of this thread's Phase-3 cell
     if (p3 && !P.adv_only) {
         const int bk = (threadIdx.x / TX + 2) * W2 + (threadIdx.x % TX + 2);
@@ -470,7 +465,9 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
             gnz = G[G_NZ * BOX + bk];
         }
     }
+    TPROBE(7);  // Phase 2 work
     __syncthreads();
+    TPROBE(8);  // Phase 2 barrier
     issue_next();
 
     // ---- Phase 3: divergence + viscous source + update + cap + [average] +
@@ -626,12 +623,15 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
     }
     // FX/FY/V/PJ/BR/cell box are rewritten by the next tile; the barrier also
     // reduces the tile's output flag
+    TPROBE(9);  // Phase 3 work + tally
     const int nzo = __syncthreads_or(obits != 0ull);
+    TPROBE(10);  // Phase 3 barrier
     if (threadIdx.x == 0) {
         A.flag_out[tile] = nzo ? 1 : 0;
         issue_cell(li + gridDim.x);
     }
     }  // tile loop
+    TPROBE_FLUSH(CORR ? 1 : 0)
 
     if (CORR) lam_block_max(lam_local, sc);
 }
@@ -674,7 +674,7 @@ __global__ void __launch_bounds__(NT) tiles_kernel(TileArgs a) {
     int base = 0;
     if (lane == 0 && m) base = atomicAdd(a.ntiles_active, __popc(m));
     base = __shfl_sync(0xffffffffu, base, 0);
-    if (active) a.tiles[base + __popc(m & ((1u << lane) - 1u))] = t;
+    if (active) a.tiles[base + __popc(m & ((1u << lane) - 1u))] = ((t / a.ntx) << 16) | (t % a.ntx);
 }
 
 // ---------------------------------------------------------------------------
@@ -1071,6 +1071,22 @@ cudaError_t selftest_minmod(long long n, const double* a, const double* b, doubl
     cudaFree(d);
     return e;
 }
+// phase-timing probe readout (zeros unless built with TP_PHASE_TIMING)
+cudaError_t phase_cycles(unsigned long long* out, int reset) {
+#ifdef TP_PHASE_TIMING
+    cudaError_t e = cudaMemcpyFromSymbol(out, g_phase_cycles, sizeof(g_phase_cycles));
+    if (e == cudaSuccess && reset) {
+        static const unsigned long long z[2][14] = {};
+        e = cudaMemcpyToSymbol(g_phase_cycles, z, sizeof(z));
+    }
+    return e;
+#else
+    (void)reset;
+    for (int k = 0; k < 28; ++k) out[k] = 0;
+    return cudaSuccess;
+#endif
+}
+
 cudaError_t selftest_division(long long n, unsigned long long seed, unsigned long long* mismatches) {
     unsigned long long* d = nullptr;
     cudaError_t e = cudaMalloc(&d, sizeof(unsigned long long));

@@ -112,7 +112,7 @@ struct StageArgs {
     int loop;                        // 1 = obey sc->done (device-resident loop)
     int use_sc_dt;                   // read dt from sc (always 1 in practice)
     // active-tile list of this stage (TileArgs below); tiles not listed are bitwise no-ops
-    const int* __restrict__ tiles;   // [ntiles] tile indices, count in *ntiles_active
+    const int* __restrict__ tiles;   // [ntiles] entries (tile row << 16) | tile column, count in *ntiles_active
     const int* ntiles_active;
     unsigned char* flag_out;         // per-tile "output interior has a nonzero bit" of `out`
 };
