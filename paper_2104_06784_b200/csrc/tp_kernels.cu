@@ -239,54 +239,47 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
     // left off the list by tiles_kernel, and a listed dry tile computes the same +0.0)
 
     // ---- Phase 1: xi faces, eta faces, cell fields -----------------------------
-    constexpr int NXP = ((NFX + 31) / 32) * 32;  // face lists padded to warp multiples
-    constexpr int NYP = ((NFY + 31) / 32) * 32;
-    constexpr int N1 = NXP + NYP + BOX;
-    for (int it = threadIdx.x; it < N1; it += NT) {
-        if (it < NXP) {
-            if (it >= NFX) continue;
-            // xi face between box cells k and k+1 (row ty+2), stored at FX[ty][fx]
-            const int fx = it % (TX + 1), ty = it / (TX + 1);
-            const int k = (ty + 2) * W2 + fx + 1;
-            double L[6], R[6];
+    // faces: thread t owns xi face t and eta face t, written as one straight-line
+    // block so the two independent dependency chains interleave (ILP)
+    {
+        const int it = threadIdx.x;
+        const bool hx = it < NFX, hy = it < NFY;
+        const int fx = it % (TX + 1), tyx = it / (TX + 1);
+        const int kx = hx ? (tyx + 2) * W2 + fx + 1 : 2 * W2 + 2;  // xi face between kx and kx+1
+        const int txy = it % TX, fy = it / TX;
+        const int ky = hy ? (fy + 1) * W2 + txy + 2 : 2 * W2 + 2;  // eta face between ky and ky+W2
+        double Lx[6], Rx[6], Ly[6], Ry[6];
 #pragma unroll
-            for (int f = 0; f < 6; ++f) {
-                const double* row = S + f * BOX + k - 1;
-                const double c0 = row[0], c1 = row[1], c2 = row[2], c3 = row[3];
-                L[f] = edge_plus(c0, c1, c2);
-                R[f] = edge_minus(c1, c2, c3);
-            }
-            double out[6];
-            face_flux<FD, true>(L, R, G[G_JB * BOX + k], G[G_JB * BOX + k + 1], G[G_NZ * BOX + k],
-                                G[G_NZ * BOX + k + 1], G[G_A11 * BOX + k], G[G_A11 * BOX + k + 1],
-                                G[G_A12 * BOX + k], G[G_A12 * BOX + k + 1], G[G_RJBFX * BOX + k], P, out);
+        for (int f = 0; f < 6; ++f) {
+            const double* row = S + f * BOX + kx - 1;
+            const double c0 = row[0], c1 = row[1], c2 = row[2], c3 = row[3];
+            Lx[f] = edge_plus(c0, c1, c2);
+            Rx[f] = edge_minus(c1, c2, c3);
+            const double* col = S + f * BOX + ky - W2;
+            const double d0 = col[0], d1 = col[W2], d2 = col[2 * W2], d3 = col[3 * W2];
+            Ly[f] = edge_plus(d0, d1, d2);
+            Ry[f] = edge_minus(d1, d2, d3);
+        }
+        double ox[6], oy[6];
+        face_flux<FD, true>(Lx, Rx, G[G_JB * BOX + kx], G[G_JB * BOX + kx + 1], G[G_NZ * BOX + kx],
+                            G[G_NZ * BOX + kx + 1], G[G_A11 * BOX + kx], G[G_A11 * BOX + kx + 1],
+                            G[G_A12 * BOX + kx], G[G_A12 * BOX + kx + 1], G[G_RJBFX * BOX + kx], P, ox);
+        face_flux<FD, false>(Ly, Ry, G[G_JB * BOX + ky], G[G_JB * BOX + ky + W2], G[G_NZ * BOX + ky],
+                             G[G_NZ * BOX + ky + W2], G[G_A22 * BOX + ky], G[G_A22 * BOX + ky + W2],
+                             G[G_A21 * BOX + ky], G[G_A21 * BOX + ky + W2], G[G_RJBFY * BOX + ky], P, oy);
+        if (hx) {
 #pragma unroll
-            for (int f = 0; f < 6; ++f) FX[f * NFX + it] = out[f];
-        } else if (it < NXP + NYP) {
-            const int jt = it - NXP;
-            if (jt >= NFY) continue;
-            // eta face between box cells k and k+W2 (column tx+2), stored at FY[fy][tx]
-            const int tx = jt % TX, fy = jt / TX;
-            const int k = (fy + 1) * W2 + tx + 2;
-            double L[6], R[6];
+            for (int f = 0; f < 6; ++f) FX[f * NFX + it] = ox[f];
+        }
+        if (hy) {
 #pragma unroll
-            for (int f = 0; f < 6; ++f) {
-                const double* col = S + f * BOX + k - W2;
-                const double c0 = col[0], c1 = col[W2], c2 = col[2 * W2], c3 = col[3 * W2];
-                L[f] = edge_plus(c0, c1, c2);
-                R[f] = edge_minus(c1, c2, c3);
-            }
-            double out[6];
-            face_flux<FD, false>(L, R, G[G_JB * BOX + k], G[G_JB * BOX + k + W2], G[G_NZ * BOX + k],
-                                 G[G_NZ * BOX + k + W2], G[G_A22 * BOX + k], G[G_A22 * BOX + k + W2],
-                                 G[G_A21 * BOX + k], G[G_A21 * BOX + k + W2], G[G_RJBFY * BOX + k], P,
-                                 out);
-#pragma unroll
-            for (int f = 0; f < 6; ++f) FY[f * NFY + jt] = out[f];
-        } else {
+            for (int f = 0; f < 6; ++f) FY[f * NFY + it] = oy[f];
+        }
+    }
+    for (int k = threadIdx.x; k < BOX; k += NT) {
+        {
             // cell fields (solver.cpp:172-184) on box cell k
             if (P.adv_only) continue;  // velocities/pjb feed sources and brackets only
-            const int k = it - NXP - NYP;
             const double jb = G[G_JB * BOX + k];
             const Rcp rj = mkrcp_const<FD>(jb, G[G_RJB * BOX + k]);
             const double ws = S[0 * BOX + k], wf = S[1 * BOX + k];
