@@ -134,8 +134,8 @@ int tp_selftest_division(int device, long n, unsigned long long seed, unsigned l
 /* diagnostic: out[k] = the device minmod limited_slope(a[k], b[k]) (solver.hpp:17-21)
  * for n host operand pairs, so tests can compare it with the reference bit for bit */
 int tp_selftest_minmod(int device, long n, const double* a, const double* b, double* out);
-/* development probe: per-phase warp cycles of the stage kernels [2][14] (pred, corr;
- * slot 11 counts warps, 12/13 sum warp lifetimes in cycles / ns); all zero unless the library was built with `make timing` */
+/* development probe: per-phase warp cycles of the stage kernels [2][19] (pred, corr;
+ * slot 16 counts warps, 17/18 sum warp lifetimes in cycles / ns); all zero unless the library was built with `make timing` */
 int tp_debug_phase_cycles(unsigned long long* out, int reset);
 /* number of kernels launched by the last tp_steps call (graph replays included) */
 long tp_kernel_launches(const tp_ctx* c);

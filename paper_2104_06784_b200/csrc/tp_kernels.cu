@@ -30,21 +30,21 @@ namespace tpb {
 // Development probe (make timing): per-warp clock accumulation of the stage kernel's
 // phases and barrier waits; compiled out of the product build.
 #ifdef TP_PHASE_TIMING
-__device__ unsigned long long g_phase_cycles[2][14];
+__device__ unsigned long long g_phase_cycles[2][19];
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
-#define TPROBE_DECL unsigned long long tp_acc[11] = {0}; long long tp_last = clock64(); \
+#define TPROBE_DECL unsigned long long tp_acc[16] = {0}; long long tp_last = clock64(); \
     const long long tp_c0 = tp_last; const unsigned long long tp_g0 = gtimer();
 #define TPROBE(k) do { const long long _n = clock64(); tp_acc[k] += _n - tp_last; tp_last = _n; } while (0)
 #define TPROBE_FLUSH(corr)                                                          \
     if ((threadIdx.x & 31) == 0) {                                                  \
-        for (int _k = 0; _k < 11; ++_k) atomicAdd(&g_phase_cycles[corr][_k], tp_acc[_k]); \
-        atomicAdd(&g_phase_cycles[corr][11], 1ull);                                 \
-        atomicAdd(&g_phase_cycles[corr][12], static_cast<unsigned long long>(clock64() - tp_c0)); \
-        atomicAdd(&g_phase_cycles[corr][13], gtimer() - tp_g0);                    \
+        for (int _k = 0; _k < 16; ++_k) atomicAdd(&g_phase_cycles[corr][_k], tp_acc[_k]); \
+        atomicAdd(&g_phase_cycles[corr][16], 1ull);                                 \
+        atomicAdd(&g_phase_cycles[corr][17], static_cast<unsigned long long>(clock64() - tp_c0)); \
+        atomicAdd(&g_phase_cycles[corr][18], gtimer() - tp_g0);                    \
     }
 #else
 #define TPROBE_DECL
@@ -527,6 +527,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
 #pragma unroll
         for (int f = 0; f < 6; ++f) un[f] = sc6[f] + dt * rhs[f];
 
+        TPROBE(11);  // phase 3: divergence + viscous + update
         // Coulomb cap (solver.cpp:458-479) on the updated state
         if (P.cap_on) {
             const double qx = un[2], qy = un[3];
@@ -577,12 +578,15 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
             }
         }
 
+        TPROBE(12);  // phase 3: Coulomb cap
         if (CORR) {  // Heun average (solver.cpp:538-541)
 #pragma unroll
             for (int f = 0; f < 6; ++f) un[f] = 0.5 * (A.u0[f * fs + o3] + un[f]);
         }
 
+        TPROBE(13);  // phase 3: Heun average
         obits = cell_epilogue<FD, CORR>(un, rj, nZ, X, Y, P, sc, lam_local, A.out, fs, o3);
+        TPROBE(14);  // phase 3: regularize, finite, lambda, stores
     }
 
     // ---- boundary mass tally of this stage (solver.cpp:352-376), ring tiles only
@@ -1069,13 +1073,13 @@ cudaError_t phase_cycles(unsigned long long* out, int reset) {
 #ifdef TP_PHASE_TIMING
     cudaError_t e = cudaMemcpyFromSymbol(out, g_phase_cycles, sizeof(g_phase_cycles));
     if (e == cudaSuccess && reset) {
-        static const unsigned long long z[2][14] = {};
+        static const unsigned long long z[2][19] = {};
         e = cudaMemcpyToSymbol(g_phase_cycles, z, sizeof(z));
     }
     return e;
 #else
     (void)reset;
-    for (int k = 0; k < 28; ++k) out[k] = 0;
+    for (int k = 0; k < 38; ++k) out[k] = 0;
     return cudaSuccess;
 #endif
 }

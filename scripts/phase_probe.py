@@ -12,7 +12,7 @@ steps = int(sys.argv[3]) if len(sys.argv) > 3 else 20
 sc = scenarios.SCENARIOS[name](n, n) if name != "c1" else scenarios.c1_hill(n)
 sim = Simulator.from_scenario(sc)
 L = _lib.lib()
-buf = (C.c_ulonglong * 28)()
+buf = (C.c_ulonglong * 38)()
 sim.steps(0.0, 1e9, 8, t_end=1e9)
 sim.synchronize()
 L.tp_debug_phase_cycles(buf, 1)
@@ -20,12 +20,13 @@ sim.steps(0.0, 1e9, steps, t_end=1e9)
 sim.synchronize()
 L.tp_debug_phase_cycles(buf, 0)
 names = ["loop top", "wait S/G TMA", "dry scan", "dry barrier", "phase1 work", "phase1 barrier",
-         "wait cell TMA", "phase2 work", "phase2 barrier", "phase3 work", "phase3 barrier"]
+         "wait cell TMA", "phase2 work", "phase2 barrier", "phase3 tail", "phase3 barrier",
+         "p3 div+visc+upd", "p3 cap", "p3 heun", "p3 epilogue", "-"]
 for st, label in ((0, "predictor"), (1, "corrector")):
-    v = list(buf[14 * st: 14 * st + 14])
-    tot = sum(v[:11])
-    w = max(v[11], 1)
-    print(f"{label}: warps {v[11]}  total {tot / w:.0f} cycles/warp; warp lifetime {v[12] / w:.0f} cycles, "
-          f"{v[13] / w / 1e3:.1f} us (globaltimer)")
-    for k in range(11):
+    v = list(buf[19 * st: 19 * st + 19])
+    tot = sum(v[:16])
+    w = max(v[16], 1)
+    print(f"{label}: warps {v[16]}  total {tot / w:.0f} cycles/warp; warp lifetime {v[17] / w:.0f} cycles, "
+          f"{v[18] / w / 1e3:.1f} us (globaltimer)")
+    for k in range(15):
         print(f"   {names[k]:16s} {100 * v[k] / tot:5.1f}%")
