@@ -6,7 +6,7 @@ tmp = tempfile.mkdtemp()
 subprocess.run(["cuobjdump", "-xelf", "all", so], cwd=tmp, capture_output=True)
 cub = [c for c in glob.glob(tmp + "/*.cubin") if "tp_kernels" in c][0]
 dis = subprocess.run(["nvdisasm", "-gi", "-c", cub], capture_output=True, text=True).stdout.split("\n")
-src = open("/root/repo/paper_2104_06784_b200/csrc/tp_kernels.cu").read().split("\n")
+src = open(os.environ.get("TP_KSRC", "/root/repo/paper_2104_06784_b200/csrc/tp_kernels.cu")).read().split("\n")
 func = None; cur = None; mp = collections.defaultdict(dict)
 for ln in dis:
     m = re.match(r'\s*\.text\.(\S+):', ln)
@@ -21,16 +21,14 @@ for ln in dis:
 # phase boundaries from markers in the source
 marks = {}
 for i, l in enumerate(src, 1):
-    for key in ("// ---- Phase 1:", "// ---- Phase 2:", "// ---- Phase 3:", "// ---- boundary mass tally",
-                "// ---- dry-tile fast path"):
+    for key in ("// ---- Phase 1:", "// ---- Phase 2:", "// ---- Phase 3:", "// ---- boundary mass tally"):
         if key in l and key not in marks:
             marks[key.replace("// ---- ", "")] = i
 start_kernel = [i for i, l in enumerate(src, 1) if "__global__ void __launch_bounds__(NT, 2) stage_kernel" in l][0]
 def phase(line):
     if line is None: return "?"
     if line < start_kernel: return "epilogue/helpers"
-    if line < marks["dry-tile fast path"]: return "prologue/TMA"
-    if line < marks["Phase 1:"]: return "dry-check"
+    if line < marks["Phase 1:"]: return "prologue/TMA"
     if line < marks["Phase 2:"]: return "phase1 faces+cells"
     if line < marks["Phase 3:"]: return "phase2 brackets"
     if line < marks["boundary mass tally"]: return "phase3 sources/update"
