@@ -136,38 +136,38 @@ def cpu_reference(config, ncols, nrows, steps, lanes, timeout=600):
     raise RuntimeError("CPU reference failed: " + err)
 
 
-def time_stages(sim, torch, stream, n=4):
-    """Per-stage kernel time with CUDA events on the launching stream (roofline leg)."""
+def time_stages(sim, n=4):
+    """Per-stage kernel time: CUDA events recorded on the launching stream right around
+    each stage kernel (tp_stage_timed), median over n device-loop-equivalent steps."""
     import ctypes as C
     L = sim.L
     h = sim.h
-    lam = torch.zeros(1, dtype=torch.float64, device="cuda")
-    tp, tc = [], []
+    lam = C.c_double(0.0)
+    tp, tc, ap, ac = [], [], [], []
     t = C.c_double(0.0)
     hit = C.c_int()
     dtv = C.c_double()
+    ms = C.c_float()
     tcur = sim._bench_t
-    with torch.cuda.stream(stream):
-        for _ in range(n):
-            sim._check(L.tp_step_begin(h, tcur, 1e9, 1e9))
-            sim._check(L.tp_bc(h, 0))
-            sim._check(L.tp_lambda_local(h, C.c_void_p(lam.data_ptr())))
-            sim._check(L.tp_dt_from(h, C.c_void_p(lam.data_ptr())))
-            e0, e1, e2, e3 = (torch.cuda.Event(enable_timing=True) for _ in range(4))
-            e0.record(stream)
-            sim._check(L.tp_stage(h, 0))
-            e1.record(stream)
-            sim._check(L.tp_bc(h, 1))
-            e2.record(stream)
-            sim._check(L.tp_stage(h, 1))
-            e3.record(stream)
-            sim._check(L.tp_step_end(h, C.byref(t), C.byref(hit), C.byref(dtv)))
-            stream.synchronize()
-            tp.append(e0.elapsed_time(e1))
-            tc.append(e2.elapsed_time(e3))
-            tcur = t.value
+    import torch
+    lam_dev = torch.zeros(1, dtype=torch.float64, device="cuda")
+    for _ in range(n):
+        sim._check(L.tp_step_begin(h, tcur, 1e9, 1e9))
+        sim._check(L.tp_bc(h, 0))
+        sim._check(L.tp_lambda_local(h, C.c_void_p(lam_dev.data_ptr())))
+        sim._check(L.tp_dt_from(h, C.c_void_p(lam_dev.data_ptr())))
+        sim._check(L.tp_stage_timed(h, 0, C.byref(ms)))
+        tp.append(ms.value)
+        sim._check(L.tp_bc(h, 1))
+        sim._check(L.tp_stage_timed(h, 1, C.byref(ms)))
+        tc.append(ms.value)
+        p_, c_, _ = sim.active_tiles()
+        ap.append(p_)
+        ac.append(c_)
+        sim._check(L.tp_step_end(h, C.byref(t), C.byref(hit), C.byref(dtv)))
+        tcur = t.value
     sim._bench_t = tcur
-    return statistics.median(tp), statistics.median(tc)
+    return statistics.median(tp), statistics.median(tc), statistics.median(ap), statistics.median(ac)
 
 
 def ncu_traffic():
@@ -211,14 +211,20 @@ def run_b200(args):
         torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
     launches = sim.kernel_launches()
+    act_p, act_c, ntiles = sim.active_tiles()
     assert n == args.steps, (n, args.steps)
     value = cells * args.steps / (ms / 1e3) / 1e9
 
     # roofline leg: the two stage kernels (the dominant kernel of the step)
     sim._bench_t = t
-    t_pred, t_corr = time_stages(sim, torch, stream, n=args.roofline_reps)
+    t_pred, t_corr, tp_p, tp_c = time_stages(sim, n=args.roofline_reps)
     peak, peak_src = load_peaks()
     achieved = ALG_BYTES_PER_CELL_UPDATE * cells / ((t_pred + t_corr) / 1e3) / 1e9
+    # the same bytes restricted to the tiles the kernels actually processed (dry tiles whose
+    # stage is a bitwise no-op are skipped): the kernel's own bandwidth
+    frac_p, frac_c = tp_p / ntiles, tp_c / ntiles
+    achieved_proc = (ALG_BYTES_PRED * cells * frac_p + ALG_BYTES_CORR * cells * frac_c) / \
+        ((t_pred + t_corr) / 1e3) / 1e9
     traffic = None
     nt = ncu_traffic()
     if nt and nt.get("grid") == [sc.ncols, sc.nrows] and nt.get("config") == args.config:
@@ -229,6 +235,9 @@ def run_b200(args):
                 "alg_bytes_per_launch": ALG_BYTES_PER_CELL_UPDATE * cells,
                 "kernel_ms_per_step": round(t_pred + t_corr, 4), "pred_ms": round(t_pred, 4),
                 "corr_ms": round(t_corr, 4), "peak_source": peak_src,
+                "processed_tile_frac": [round(frac_p, 4), round(frac_c, 4)],
+                "achieved_processed_tiles": round(achieved_proc, 1),
+                "frac_processed_tiles": round(achieved_proc / peak, 4),
                 "step_frac": round(achieved * (t_pred + t_corr) / (ms / args.steps) / peak, 4)}
 
     # e2e leg: through the C ABI with HOST (pinned) buffers, copies inside the timed region
@@ -272,6 +281,7 @@ def run_b200(args):
                    "l2": "inputs larger than L2 (state 2x%.0f MB + geometry %.0f MB > 126 MB)"
                          % (nbytes / 1e6, 18 * sim.ny * sim.nx * 8 / 1e6),
                    "parallelism": "single device", "graph_steps": args.graph_steps,
+                   "active_tiles_last_step": [act_p, act_c, ntiles],
                    "hbm_roofline_gcups": round(peak / ALG_BYTES_PER_CELL_UPDATE, 3),
                    "hbm_frac_of_step": round(value / (peak / ALG_BYTES_PER_CELL_UPDATE), 4),
                    "setup_seconds": round(setup_s, 2)},

@@ -121,6 +121,9 @@ int tp_bc(tp_ctx* c, int buf);                         /* buf 0 at t, buf 1 at t
 int tp_lambda_local(tp_ctx* c, void* dst_device);      /* local lambda_max (1 double) -> dst */
 int tp_dt_from(tp_ctx* c, const void* lam_device);     /* dt from an all-reduced lambda */
 int tp_stage(tp_ctx* c, int corrector);                /* predictor u^n -> u*, corrector */
+/* tp_stage with CUDA events recorded on the context stream right around the stage
+ * kernel (after its tile-list kernel); *ms = that kernel's device time */
+int tp_stage_timed(tp_ctx* c, int corrector, float* ms);
 int tp_step_end(tp_ctx* c, double* t, int* hit, double* dt); /* fold audit, advance t, sync */
 
 /* interop: the CUDA stream the context launches on (default: its own stream) */
@@ -134,6 +137,9 @@ int tp_selftest_division(int device, long n, unsigned long long seed, unsigned l
 /* diagnostic: out[k] = the device minmod limited_slope(a[k], b[k]) (solver.hpp:17-21)
  * for n host operand pairs, so tests can compare it with the reference bit for bit */
 int tp_selftest_minmod(int device, long n, const double* a, const double* b, double* out);
+/* tiles listed by the last predictor / corrector launch (dry tiles whose stage is a
+ * bitwise no-op are skipped) and the number of tiles of the grid */
+int tp_active_tiles(tp_ctx* c, int* pred, int* corr, int* total);
 /* development probe: per-phase warp cycles of the stage kernels [2][19] (pred, corr;
  * slot 16 counts warps, 17/18 sum warp lifetimes in cycles / ns); all zero unless the library was built with `make timing` */
 int tp_debug_phase_cycles(unsigned long long* out, int reset);

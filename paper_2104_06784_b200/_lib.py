@@ -65,6 +65,7 @@ SIGNATURES = {
     "tp_lambda_local": (C.c_int, [_vp, _vp]),
     "tp_dt_from": (C.c_int, [_vp, _vp]),
     "tp_stage": (C.c_int, [_vp, C.c_int]),
+    "tp_stage_timed": (C.c_int, [_vp, C.c_int, C.POINTER(C.c_float)]),
     "tp_step_end": (C.c_int, [_vp, _dp, _ip, _dp]),
     "tp_set_stream": (C.c_int, [_vp, _vp]),
     "tp_synchronize": (C.c_int, [_vp]),
@@ -72,6 +73,7 @@ SIGNATURES = {
     "tp_kernel_launches": (C.c_long, [_vp]),
     "tp_selftest_division": (C.c_int, [C.c_int, C.c_long, C.c_ulonglong, C.POINTER(C.c_ulonglong)]),
     "tp_selftest_minmod": (C.c_int, [C.c_int, C.c_long, _dp, _dp, _dp]),
+    "tp_active_tiles": (C.c_int, [_vp, _ip, _ip, _ip]),
     "tp_debug_phase_cycles": (C.c_int, [C.POINTER(C.c_ulonglong), C.c_int]),
 }
 

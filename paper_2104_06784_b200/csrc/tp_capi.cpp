@@ -131,7 +131,7 @@ struct tp_ctx {
     unsigned char* dFlagA = nullptr;  // per-tile "interior has a nonzero bit" of A / B (1 = unknown)
     unsigned char* dFlagB = nullptr;
     int* dTiles = nullptr;            // active-tile list of the stage in flight + its count
-    int* dNact = nullptr;             // [2] list counts: predictor, corrector
+    int* dNact = nullptr;             // [4] list counts: predictor, corrector; last-launch stats
     int last_tiles_stage = 1;         // stage of the last tiles_kernel enqueued (0 pred, 1 corr)
     bool lam_valid = false;
     bool ghosts_in_B = false;
@@ -239,11 +239,13 @@ tpb::StageArgs stage_args(tp_ctx* c, bool corr, int loop) {
     a.tiles = c->dTiles;
     a.ntiles_active = c->dNact + (corr ? 1 : 0);
     a.flag_out = corr ? c->dFlagA : c->dFlagB;
+    a.nact_stat = c->dNact + 2;
     return a;
 }
 
 // Both stage launches go through here: the active-tile list (tiles_kernel), then the stage.
-cudaError_t launch_stage_sel(tp_ctx* c, const tpb::StageArgs& a, bool fastdiv, bool corr, cudaStream_t st) {
+cudaError_t launch_stage_sel(tp_ctx* c, const tpb::StageArgs& a, bool fastdiv, bool corr, cudaStream_t st,
+                             cudaEvent_t ev0 = nullptr, cudaEvent_t ev1 = nullptr) {
     tpb::TileArgs t{};
     t.flag_in = corr ? c->dFlagB : c->dFlagA;
     t.flag_out = corr ? c->dFlagA : c->dFlagB;
@@ -271,7 +273,10 @@ cudaError_t launch_stage_sel(tp_ctx* c, const tpb::StageArgs& a, bool fastdiv, b
     c->last_tiles_stage = stage;
     cudaError_t e = tpb::launch_tiles(t, st);
     if (e != cudaSuccess) return e;
-    return tpb::launch_stage(a, fastdiv, corr, st);
+    if (ev0 && (e = cudaEventRecord(ev0, st)) != cudaSuccess) return e;
+    e = tpb::launch_stage(a, fastdiv, corr, st);
+    if (e == cudaSuccess && ev1) e = cudaEventRecord(ev1, st);
+    return e;
 }
 
 // Conservative reset of the per-tile flags (after any write to a state buffer that is
@@ -532,8 +537,8 @@ void create_impl(tp_ctx* c, const tp_params* p, const tp_dem* dem, int row0, int
     ck(cudaMalloc(&c->dFlagA, ntiles), "cudaMalloc flags");
     ck(cudaMalloc(&c->dFlagB, ntiles), "cudaMalloc flags");
     ck(cudaMalloc(&c->dTiles, sizeof(int) * ntiles), "cudaMalloc tiles");
-    ck(cudaMalloc(&c->dNact, 2 * sizeof(int)), "cudaMalloc tiles");
-    ck(cudaMemsetAsync(c->dNact, 0, 2 * sizeof(int), c->stream), "memset");
+    ck(cudaMalloc(&c->dNact, 4 * sizeof(int)), "cudaMalloc tiles");
+    ck(cudaMemsetAsync(c->dNact, 0, 4 * sizeof(int), c->stream), "memset");
     invalidate_flags(c, true, true);
     {
         // device geometry layout (tp_types.h GeoField): the 14 reference fields
@@ -1087,6 +1092,25 @@ int tp_stage(tp_ctx* c, int corrector) {
     })
 }
 
+int tp_stage_timed(tp_ctx* c, int corrector, float* ms) {
+    TP_GUARD(c, {
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        ck(cudaEventCreate(&e0), "event");
+        ck(cudaEventCreate(&e1), "event");
+        cudaError_t e = launch_stage_sel(c, stage_args(c, corrector != 0, 0), c->fastdiv, corrector != 0,
+                                         c->stream, e0, e1);
+        if (e == cudaSuccess) e = cudaEventSynchronize(e1);
+        if (e == cudaSuccess) e = cudaEventElapsedTime(ms, e0, e1);
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        ck(e, corrector ? "corrector" : "predictor");
+        if (corrector) {
+            c->lam_valid = true;
+            c->ghosts_in_B = true;
+        }
+    })
+}
+
 int tp_step_end(tp_ctx* c, double* t, int* hit, double* dt) {
     TP_GUARD(c, {
         // clear a stale done flag so post_kernel runs its loop bookkeeping
@@ -1138,6 +1162,17 @@ int tp_selftest_minmod(int device, long n, const double* a, const double* b, dou
     if (n <= 0 || !a || !b || !out) return TP_ERR_INTERNAL;
     if (cudaSetDevice(device) != cudaSuccess) return TP_ERR_CUDA;
     return tpb::selftest_minmod(n, a, b, out) == cudaSuccess ? TP_OK : TP_ERR_CUDA;
+}
+
+int tp_active_tiles(tp_ctx* c, int* pred, int* corr, int* total) {
+    TP_GUARD(c, {
+        int n[2] = {0, 0};
+        ck(cudaMemcpyAsync(n, c->dNact + 2, sizeof(n), cudaMemcpyDeviceToHost, c->stream), "tiles D2H");
+        ck(cudaStreamSynchronize(c->stream), "sync");
+        *pred = n[0];
+        *corr = n[1];
+        *total = c->ntx * c->nty;
+    })
 }
 
 int tp_debug_phase_cycles(unsigned long long* out, int reset) {

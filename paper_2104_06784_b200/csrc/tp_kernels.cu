@@ -168,6 +168,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
     const long long fs = g.fs;
     const int ntiles = A.ntx * A.nty;
     const int nact = *A.ntiles_active;  // active-tile list of this stage (tiles_kernel)
+    if (blockIdx.x == 0 && threadIdx.x == 0) A.nact_stat[CORR ? 1 : 0] = nact;  // diagnostics
     const double dt = sc->dt;
 
     // Persistent tiles: block b walks tiles b, b+G, b+2G, ... (row-major, so the

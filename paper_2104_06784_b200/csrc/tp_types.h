@@ -115,6 +115,7 @@ struct StageArgs {
     const int* __restrict__ tiles;   // [ntiles] entries (tile row << 16) | tile column, count in *ntiles_active
     const int* ntiles_active;
     unsigned char* flag_out;         // per-tile "output interior has a nonzero bit" of `out`
+    int* nact_stat;                  // [2] list length of the last predictor / corrector launch
 };
 
 // Dry-tile classification before a stage.  flag_in: per-tile flags of the stage's input

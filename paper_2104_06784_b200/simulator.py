@@ -191,6 +191,12 @@ class Simulator:
     def kernel_launches(self) -> int:
         return int(self.L.tp_kernel_launches(self.h))
 
+    def active_tiles(self) -> tuple:
+        """(predictor, corrector) tiles processed by the last step, and the grid's tile count."""
+        p, c, t = C.c_int(), C.c_int(), C.c_int()
+        self._check(self.L.tp_active_tiles(self.h, C.byref(p), C.byref(c), C.byref(t)))
+        return p.value, c.value, t.value
+
     def synchronize(self) -> None:
         self._check(self.L.tp_synchronize(self.h))
 
