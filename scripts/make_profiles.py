@@ -8,8 +8,8 @@ def raw(rep):
     return rows[0], rows[1], rows[2:]
 lines = [f"# ncu summary, {tag}\n"]
 summary = {}
-for sfx, cfg in (("", "c2"), ("_wet", "wet")):
-    rep = f"gpurun_out/prof_{tag}{sfx}.ncu-rep"
+for cfg in ("c2", "wet"):
+    rep = f"gpurun_out/prof_{tag}_{cfg}.ncu-rep"
     if not os.path.exists(rep):
         continue
     hdr, units, data = raw(rep)
