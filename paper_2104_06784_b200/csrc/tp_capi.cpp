@@ -36,6 +36,8 @@ cudaError_t launch_regularize(const GridDesc& g, const Phys& P, double* s, const
                               DevScalars* sc, bool fastdiv, cudaStream_t st);
 cudaError_t init_kernels();
 cudaError_t launch_tiles(const TileArgs& a, cudaStream_t st);
+cudaError_t launch_pre(const PreArgs& a, cudaStream_t st);
+int bc_blocks(const GridDesc& g);
 cudaError_t selftest_division(long long n, unsigned long long seed, unsigned long long* mismatches);
 cudaError_t selftest_minmod(long long n, const double* a, const double* b, double* out);
 cudaError_t phase_cycles(unsigned long long* out, int reset);
@@ -243,9 +245,7 @@ tpb::StageArgs stage_args(tp_ctx* c, bool corr, int loop) {
     return a;
 }
 
-// Both stage launches go through here: the active-tile list (tiles_kernel), then the stage.
-cudaError_t launch_stage_sel(tp_ctx* c, const tpb::StageArgs& a, bool fastdiv, bool corr, cudaStream_t st,
-                             cudaEvent_t ev0 = nullptr, cudaEvent_t ev1 = nullptr) {
+tpb::TileArgs tile_args(tp_ctx* c, const tpb::StageArgs& a, bool corr) {
     tpb::TileArgs t{};
     t.flag_in = corr ? c->dFlagB : c->dFlagA;
     t.flag_out = corr ? c->dFlagA : c->dFlagB;
@@ -263,6 +263,13 @@ cudaError_t launch_stage_sel(tp_ctx* c, const tpb::StageArgs& a, bool fastdiv, b
     t.north_ineligible = c->g.has_north ? 0 : 1;
     t.loop = a.loop;
     t.sc = c->dSc;
+    return t;
+}
+
+// Stage launches outside the fused device loop: the active-tile list (tiles_kernel), then the stage.
+cudaError_t launch_stage_sel(tp_ctx* c, const tpb::StageArgs& a, bool fastdiv, bool corr, cudaStream_t st,
+                             cudaEvent_t ev0 = nullptr, cudaEvent_t ev1 = nullptr) {
+    const tpb::TileArgs t = tile_args(c, a, corr);
     // each tiles_kernel zeroes the other stage's counter; two launches of one stage in a
     // row (a bare tp_stage call) need an explicit reset
     const int stage = corr ? 1 : 0;
@@ -311,14 +318,30 @@ void launch_post(tp_ctx* c, int loop) {
     ck(tpb::launch_post(a, c->stream), "post_kernel");
 }
 
-// one whole step of the device loop: 6 kernels
+// one whole step of the device loop: 5 kernels
+//   pre(bc(u,t) + predictor list + compute_dt) -> predictor -> pre(bc(u*,t+dt) + corrector list)
+//   -> corrector -> post(t += dt, audit, stop flag)
 void enqueue_loop_step(tp_ctx* c) {
-    launch_bc(c, 0, 1, 0.0, 1);                                     // apply_boundaries(u, t)
-    ck(tpb::launch_dt(c->ph, c->dSc, 1, c->stream), "dt_kernel");   // compute_dt
-    ck(launch_stage_sel(c, stage_args(c, false, 1), c->fastdiv, false, c->stream), "predictor");
-    launch_bc(c, 1, 2, 0.0, 1);                                     // apply_boundaries(u*, t+dt)
-    ck(launch_stage_sel(c, stage_args(c, true, 1), c->fastdiv, true, c->stream), "corrector");
-    launch_post(c, 1);                                              // t += dt, audit, stop flag
+    for (int corr = 0; corr < 2; ++corr) {
+        const tpb::StageArgs sa = stage_args(c, corr != 0, 1);
+        tpb::PreArgs p{};
+        p.bc.g = c->g;
+        p.bc.s = corr ? c->dB : c->dA;
+        p.bc.geo = c->dGeo;
+        p.bc.inflow = inflow_desc(c);
+        p.bc.sc = c->dSc;
+        p.bc.t = 0.0;
+        p.bc.tsrc = corr ? 2 : 1;
+        p.bc.loop = 1;
+        p.t = tile_args(c, sa, corr != 0);
+        p.P = c->ph;
+        p.nb_bc = tpb::bc_blocks(c->g);
+        p.with_dt = corr ? 0 : 1;
+        ck(tpb::launch_pre(p, c->stream), corr ? "pre (corrector)" : "pre (predictor)");
+        c->last_tiles_stage = corr;
+        ck(tpb::launch_stage(sa, c->fastdiv, corr != 0, c->stream), corr ? "corrector" : "predictor");
+    }
+    launch_post(c, 1);
 }
 
 cudaGraphExec_t capture_steps(tp_ctx* c, int k) {
@@ -922,7 +945,7 @@ int tp_steps(tp_ctx* c, double t_next, double t_end, long max_steps, double* t, 
         for (;;) {
             const bool big = (max_steps - done_steps) >= c->graph_steps;
             ck(cudaGraphLaunch(big ? c->graphK : c->graph1, c->stream), "graph launch");
-            c->launches += 8L * (big ? c->graph_steps : 1);
+            c->launches += 5L * (big ? c->graph_steps : 1);
             h = read_scalars(c);
             done_steps = h.steps;
             if (h.done) break;

@@ -638,10 +638,9 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
 // Active-tile list of one stage (see TileArgs).  One thread per tile; the list is
 // appended warp by warp, so it stays row-major within each warp's 32 tiles.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(NT) tiles_kernel(TileArgs a) {
-    if (a.loop && *(volatile int*)&a.sc->done) return;
+__device__ __forceinline__ void tiles_body(const TileArgs& a, int block) {
     const int ntiles = a.ntx * a.nty;
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const int t = block * blockDim.x + threadIdx.x;
     bool active = false;
     if (t < ntiles) {
         const int tx = t % a.ntx, ty = t / a.ntx;
@@ -673,6 +672,11 @@ __global__ void __launch_bounds__(NT) tiles_kernel(TileArgs a) {
     if (lane == 0 && m) base = atomicAdd(a.ntiles_active, __popc(m));
     base = __shfl_sync(0xffffffffu, base, 0);
     if (active) a.tiles[base + __popc(m & ((1u << lane) - 1u))] = ((t / a.ntx) << 16) | (t % a.ntx);
+}
+
+__global__ void __launch_bounds__(NT) tiles_kernel(TileArgs a) {
+    if (a.loop && *(volatile int*)&a.sc->done) return;
+    tiles_body(a, blockIdx.x);
 }
 
 // ---------------------------------------------------------------------------
@@ -719,11 +723,10 @@ __device__ void hydro_at(const Inflow& in, double t, double& h, double& phi, dou
     h = s[4 * (n - 1) + 1]; phi = s[4 * (n - 1) + 2]; speed = s[4 * (n - 1) + 3];
 }
 
-__global__ void bc_kernel(BcArgs a) {
-    if (a.loop && *(volatile int*)&a.sc->done) return;
+__device__ __forceinline__ void bc_body(const BcArgs& a, int block) {
     const GridDesc& g = a.g;
     const int n = ghost_band_count(g);
-    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    const int idx = block * blockDim.x + threadIdx.x;
     if (idx >= n) return;
     int i, j;
     ghost_band_cell(g, idx, i, j);
@@ -765,6 +768,11 @@ __global__ void bc_kernel(BcArgs a) {
     }
 #pragma unroll
     for (int f = 0; f < 6; ++f) a.s[f * g.fs + o] = v[f];
+}
+
+__global__ void __launch_bounds__(NT) bc_kernel(BcArgs a) {
+    if (a.loop && *(volatile int*)&a.sc->done) return;
+    bc_body(a, blockIdx.x);
 }
 
 // Copy the ghost band of src into dst (the reference's u_ keeps the ghosts of
@@ -813,7 +821,7 @@ __global__ void __launch_bounds__(NT) lambda_kernel(GridDesc g, Phys P, const do
 }
 
 // compute_dt's tail (solver.cpp:575-579) and exact_hit (:641).  One thread.
-__global__ void dt_kernel(Phys P, DevScalars* sc, int loop) {
+__device__ __forceinline__ void dt_body(const Phys& P, DevScalars* sc, int loop) {
     if (loop) {
         if (sc->done) return;
         if (!(sc->t < sc->t_end) || sc->steps >= sc->max_steps) { sc->done = 1; return; }
@@ -830,6 +838,24 @@ __global__ void dt_kernel(Phys P, DevScalars* sc, int loop) {
     sc->dt = dt;
     sc->hit = dt == sc->t_next - sc->t;
     sc->lam_bits = 0ull;
+}
+
+__global__ void dt_kernel(Phys P, DevScalars* sc, int loop) { dt_body(P, sc, loop); }
+
+// One launch before each stage of the device loop: apply_boundaries on the stage input
+// (blocks [0, nb_bc)), the stage's active-tile list (the next nb_tiles blocks) and,
+// before the predictor, compute_dt's tail (block 0, thread 0).  Every block derives the
+// loop's stop condition from values no block of this launch writes, so all agree.
+__global__ void __launch_bounds__(NT) pre_kernel(const __grid_constant__ PreArgs a) {
+    const DevScalars* sc = a.t.sc;
+    const bool stop = *(volatile const int*)&sc->done || !(sc->t < sc->t_end) || sc->steps >= sc->max_steps;
+    if (stop) {
+        if (a.with_dt && blockIdx.x == 0 && threadIdx.x == 0) a.t.sc->done = 1;
+        return;
+    }
+    if (a.with_dt && blockIdx.x == 0 && threadIdx.x == 0) dt_body(a.P, a.t.sc, 0);
+    if (static_cast<int>(blockIdx.x) < a.nb_bc) bc_body(a.bc, blockIdx.x);
+    else tiles_body(a.t, blockIdx.x - a.nb_bc);
 }
 
 // After the corrector: fold the two stage tallies into the audit (predictor then
@@ -937,6 +963,17 @@ static cudaError_t launch_stage_t(const StageArgs& a, cudaStream_t st) {
     return cudaGetLastError();
 }
 
+cudaError_t launch_pre(const PreArgs& a, cudaStream_t st) {
+    const int n = a.t.ntx * a.t.nty;
+    pre_kernel<<<a.nb_bc + (n + NT - 1) / NT, NT, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+int bc_blocks(const GridDesc& g) {
+    const int n = (g.has_south ? 3 * g.nx : 0) + (g.has_north ? 3 * g.nx : 0) + 6 * (g.ny - 6);
+    return (n + NT - 1) / NT;
+}
+
 cudaError_t launch_tiles(const TileArgs& a, cudaStream_t st) {
     const int n = a.ntx * a.nty;
     tiles_kernel<<<(n + NT - 1) / NT, NT, 0, st>>>(a);
@@ -949,8 +986,7 @@ cudaError_t launch_stage(const StageArgs& a, bool fastdiv, bool corr, cudaStream
 }
 
 cudaError_t launch_bc(const BcArgs& a, cudaStream_t st) {
-    const int n = (a.g.has_south ? 3 * a.g.nx : 0) + (a.g.has_north ? 3 * a.g.nx : 0) + 6 * (a.g.ny - 6);
-    bc_kernel<<<(n + 255) / 256, 256, 0, st>>>(a);
+    bc_kernel<<<bc_blocks(a.g), NT, 0, st>>>(a);
     return cudaGetLastError();
 }
 

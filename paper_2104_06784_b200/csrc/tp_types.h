@@ -149,6 +149,15 @@ struct BcArgs {
     int loop;
 };
 
+// bc + tile list (+ dt before the predictor) of one device-loop stage in one launch
+struct PreArgs {
+    BcArgs bc;
+    TileArgs t;
+    Phys P;
+    int nb_bc;    // blocks of the ghost band (bc_body); the tile blocks follow
+    int with_dt;  // predictor: compute_dt's tail in block 0
+};
+
 struct PostArgs {
     DevScalars* sc;
     const double* tally_pred;
