@@ -130,8 +130,8 @@ struct tp_ctx {
     bool fastdiv = true;
     int graph_steps = 16;
     bool skip_dry = true;  // list only tiles that are not bitwise no-ops (tiles_kernel)
-    unsigned char* dFlagA = nullptr;  // per-tile "interior has a nonzero bit" of A / B (1 = unknown)
-    unsigned char* dFlagB = nullptr;
+    unsigned short* dFlagA = nullptr;  // per-tile TileFlag bits of A / B (all set = unknown)
+    unsigned short* dFlagB = nullptr;
     int* dTiles = nullptr;            // active-tile list of the stage in flight + its count
     int* dNact = nullptr;             // [4] list counts: predictor, corrector; last-launch stats
     int last_tiles_stage = 1;         // stage of the last tiles_kernel enqueued (0 pred, 1 corr)
@@ -290,8 +290,8 @@ cudaError_t launch_stage_sel(tp_ctx* c, const tpb::StageArgs& a, bool fastdiv, b
 // not a stage kernel): every tile is listed until a stage recomputes its flag.
 void invalidate_flags(tp_ctx* c, bool a_buf, bool b_buf) {
     const size_t n = static_cast<size_t>(c->ntx) * c->nty;
-    if (a_buf) ck(cudaMemsetAsync(c->dFlagA, 1, n, c->stream), "flags");
-    if (b_buf) ck(cudaMemsetAsync(c->dFlagB, 1, n, c->stream), "flags");
+    if (a_buf) ck(cudaMemsetAsync(c->dFlagA, 0xff, n * sizeof(unsigned short), c->stream), "flags");
+    if (b_buf) ck(cudaMemsetAsync(c->dFlagB, 0xff, n * sizeof(unsigned short), c->stream), "flags");
 }
 
 void launch_bc(tp_ctx* c, int buf, int tsrc, double t, int loop) {
@@ -557,8 +557,8 @@ void create_impl(tp_ctx* c, const tp_params* p, const tp_dem* dem, int row0, int
     ck(cudaMemsetAsync(c->dTallyP, 0, tb, c->stream), "memset");
     ck(cudaMemsetAsync(c->dTallyC, 0, tb, c->stream), "memset");
     const size_t ntiles = static_cast<size_t>(c->ntx) * c->nty;
-    ck(cudaMalloc(&c->dFlagA, ntiles), "cudaMalloc flags");
-    ck(cudaMalloc(&c->dFlagB, ntiles), "cudaMalloc flags");
+    ck(cudaMalloc(&c->dFlagA, ntiles * sizeof(unsigned short)), "cudaMalloc flags");
+    ck(cudaMalloc(&c->dFlagB, ntiles * sizeof(unsigned short)), "cudaMalloc flags");
     ck(cudaMalloc(&c->dTiles, sizeof(int) * ntiles), "cudaMalloc tiles");
     ck(cudaMalloc(&c->dNact, 4 * sizeof(int)), "cudaMalloc tiles");
     ck(cudaMemsetAsync(c->dNact, 0, 4 * sizeof(int), c->stream), "memset");

@@ -52,6 +52,16 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #define TPROBE_FLUSH(corr)
 #endif
 
+// Output-flag bits of one tile (TileFlag in tp_types.h) touched by the cell at tile
+// coordinates (cx, cy): the interior, the 2-cell edge bands and the 2x2 corners a
+// neighbouring tile's radius-2 box reads.
+__device__ __forceinline__ unsigned cell_flag_bits(int cx, int cy) {
+    const bool w = cx < 2, e = cx >= TX - 2, s = cy < 2, n = cy >= TY - 2;
+    return TF_ANY | (w ? TF_W : 0u) | (e ? TF_E : 0u) | (s ? TF_S : 0u) | (n ? TF_N : 0u) |
+           ((w && s) ? TF_SW : 0u) | ((e && s) ? TF_SE : 0u) | ((w && n) ? TF_NW : 0u) |
+           ((e && n) ? TF_NE : 0u);
+}
+
 // regularize + [check_finite + lambda] + store of one updated cell: the tail of
 // advance_step's stages (solver.cpp:139-166, :482-494, :556-573).
 template <bool FD, bool CORR>
@@ -149,6 +159,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
     __shared__ unsigned long long bar;   // state + stencil-geometry boxes
     __shared__ unsigned long long barc;  // per-cell geometry box
     __shared__ int s_tile;               // list entry of the next tile (read by thread 0 at issue time)
+    __shared__ unsigned s_flags;         // output-flag bits of the tile in flight
     const double* Cg = sm + SM_C;        // [NGCELL][TY][TX]: nX, nY, dnX/dxi, dnY/dxi, dnZ/dxi, dnX/deta, dnY/deta, dnZ/deta, RN(1/nZ)
     double* S = sm + SM_S;
     const double* G = sm + SM_G;
@@ -198,6 +209,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
             issue_cell(blockIdx.x);
         }
     }
+    if (threadIdx.x == 0) s_flags = 0u;
     __syncthreads();  // barrier init visible to all threads
     double lam_local = 0.0;
     unsigned iter = 0;
@@ -619,13 +631,19 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
         t[2 * p + 0] = in;
         t[2 * p + 1] = outf;
     }
-    // FX/FY/V/PJ/BR/cell box are rewritten by the next tile; the barrier also
-    // reduces the tile's output flag
+    // the tile's output flags: warp OR, one shared atomic per warp; the end-of-tile
+    // barrier (FX/FY/V/PJ/BR/cell box are rewritten by the next tile) publishes them
+    {
+        const unsigned fb = (p3 && obits != 0ull) ? cell_flag_bits(threadIdx.x % TX, threadIdx.x / TX) : 0u;
+        const unsigned wf = __reduce_or_sync(0xffffffffu, fb);
+        if ((threadIdx.x & 31) == 0 && wf) atomicOr(&s_flags, wf);
+    }
     TPROBE(9);  // Phase 3 work + tally
-    const int nzo = __syncthreads_or(obits != 0ull);
+    __syncthreads();
     TPROBE(10);  // Phase 3 barrier
     if (threadIdx.x == 0) {
-        A.flag_out[tile] = nzo ? 1 : 0;
+        A.flag_out[tile] = static_cast<unsigned short>(s_flags);
+        s_flags = 0u;  // next write after at least one more barrier
         issue_cell(li + gridDim.x);
     }
     }  // tile loop
@@ -649,13 +667,21 @@ __device__ __forceinline__ void tiles_body(const TileArgs& a, int block) {
         if (ring && a.ring_ineligible) skip = false;
         if (ty == 0 && a.south_ineligible) skip = false;
         if (ty == a.nty - 1 && a.north_ineligible) skip = false;
-        for (int dy = -1; dy <= 1 && skip; ++dy) {
-            const int y = ty + dy;
-            if (y < 0 || y >= a.nty) continue;
-            for (int dx = -1; dx <= 1; ++dx) {
-                const int x = tx + dx;
-                if (x >= 0 && x < a.ntx && a.flag_in[y * a.ntx + x]) skip = false;
-            }
+        if (skip) {
+            // the radius-2 box reads this tile's interior, the facing 2-cell band of each
+            // edge neighbour and the facing 2x2 corner of each diagonal neighbour
+            const unsigned short* F = a.flag_in;
+            const bool xl = tx > 0, xr = tx < a.ntx - 1, yl = ty > 0, yr = ty < a.nty - 1;
+            unsigned need = F[t] & TF_ANY;
+            if (xl) need |= F[t - 1] & TF_E;
+            if (xr) need |= F[t + 1] & TF_W;
+            if (yl) need |= F[t - a.ntx] & TF_N;
+            if (yr) need |= F[t + a.ntx] & TF_S;
+            if (xl && yl) need |= F[t - a.ntx - 1] & TF_NE;
+            if (xr && yl) need |= F[t - a.ntx + 1] & TF_NW;
+            if (xl && yr) need |= F[t + a.ntx - 1] & TF_SE;
+            if (xr && yr) need |= F[t + a.ntx + 1] & TF_SW;
+            skip = need == 0u;
         }
         active = !skip;
         if (skip && ring) {

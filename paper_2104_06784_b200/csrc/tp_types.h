@@ -114,18 +114,26 @@ struct StageArgs {
     // active-tile list of this stage (TileArgs below); tiles not listed are bitwise no-ops
     const int* __restrict__ tiles;   // [ntiles] entries (tile row << 16) | tile column, count in *ntiles_active
     const int* ntiles_active;
-    unsigned char* flag_out;         // per-tile "output interior has a nonzero bit" of `out`
+    unsigned short* flag_out;        // per-tile TileFlag bits of `out` (nonzero bits per region)
     int* nact_stat;                  // [2] list length of the last predictor / corrector launch
 };
 
+// Per-tile output flags: which regions of the tile's interior hold a value with a nonzero
+// bit (the 2-cell bands and 2x2 corners are what a neighbour's radius-2 box reads).
+enum TileFlag : unsigned {
+    TF_ANY = 1u, TF_W = 2u, TF_E = 4u, TF_S = 8u, TF_N = 16u,
+    TF_SW = 32u, TF_SE = 64u, TF_NW = 128u, TF_NE = 256u, TF_ALL = 0xffffu
+};
+
 // Dry-tile classification before a stage.  flag_in: per-tile flags of the stage's input
-// buffer (the radius-2 box reads interior cells of the 3x3 tile neighbourhood only);
-// flag_out: flags of its output buffer.  A tile whose 3x3 input neighbourhood and whose
-// own output are all +0.0 bits is a bitwise no-op: it is left off the
-// list (its ring tally slot is zeroed here).  Flags are conservative: 1 = unknown.
+// buffer (the radius-2 box reads interior cells of the tile and the facing bands/corners
+// of its 8 neighbours only); flag_out: flags of its output buffer.  A tile whose box
+// and whose own output are all +0.0 bits is a bitwise no-op: it is left
+// off the list (its ring tally slot is zeroed here).  Flags are conservative: all bits
+// set = unknown.
 struct TileArgs {
-    const unsigned char* flag_in;
-    const unsigned char* flag_out;
+    const unsigned short* flag_in;
+    const unsigned short* flag_out;
     int* tiles;
     int* ntiles_active;   // this stage's counter (zeroed by the other stage's tiles_kernel)
     int* ntiles_reset;    // the other stage's counter
