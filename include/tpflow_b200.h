@@ -140,6 +140,9 @@ int tp_selftest_minmod(int device, long n, const double* a, const double* b, dou
 /* tiles listed by the last predictor / corrector launch (dry tiles whose stage is a
  * bitwise no-op are skipped) and the number of tiles of the grid */
 int tp_active_tiles(tp_ctx* c, int* pred, int* corr, int* total);
+/* how many tiles of the last corrector list were "safe" (every value their box reads is
+ * +-0 or of magnitude in [2^-200, 2^200): FASTDIV window tests compiled out) */
+int tp_safe_tiles(tp_ctx* c, int* corr);
 /* development probe: per-phase warp cycles of the stage kernels [2][19] (pred, corr;
  * slot 16 counts warps, 17/18 sum warp lifetimes in cycles / ns); all zero unless the library was built with `make timing` */
 int tp_debug_phase_cycles(unsigned long long* out, int reset);

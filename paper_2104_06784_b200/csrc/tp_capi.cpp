@@ -130,10 +130,12 @@ struct tp_ctx {
     bool fastdiv = true;
     int graph_steps = 16;
     bool skip_dry = true;  // list only tiles that are not bitwise no-ops (tiles_kernel)
+    bool geo_safe = false; // every jb (and so every face jbf) in [1, 2^100]: safe tiles allowed
     unsigned short* dFlagA = nullptr;  // per-tile TileFlag bits of A / B (all set = unknown)
     unsigned short* dFlagB = nullptr;
     int* dTiles = nullptr;            // active-tile list of the stage in flight + its count
-    int* dNact = nullptr;             // [4] list counts: predictor, corrector; last-launch stats
+    int* dNact = nullptr;             // [6] list counts pred, corr; last-launch stats pred, corr;
+                                      // safe-tile counts pred, corr
     int last_tiles_stage = 1;         // stage of the last tiles_kernel enqueued (0 pred, 1 corr)
     bool lam_valid = false;
     bool ghosts_in_B = false;
@@ -261,6 +263,7 @@ tpb::TileArgs tile_args(tp_ctx* c, const tpb::StageArgs& a, bool corr) {
     t.ring_ineligible = (c->inflow_active || !a.loop) ? 1 : 0;
     t.south_ineligible = c->g.has_south ? 0 : 1;
     t.north_ineligible = c->g.has_north ? 0 : 1;
+    t.safe_ok = (c->fastdiv && c->geo_safe) ? 1 : 0;
     t.loop = a.loop;
     t.sc = c->dSc;
     return t;
@@ -275,6 +278,7 @@ cudaError_t launch_stage_sel(tp_ctx* c, const tpb::StageArgs& a, bool fastdiv, b
     const int stage = corr ? 1 : 0;
     if (c->last_tiles_stage == stage) {
         cudaError_t e0 = cudaMemsetAsync(t.ntiles_active, 0, sizeof(int), st);
+        if (e0 == cudaSuccess) e0 = cudaMemsetAsync(t.ntiles_active + 4, 0, sizeof(int), st);
         if (e0 != cudaSuccess) return e0;
     }
     c->last_tiles_stage = stage;
@@ -560,8 +564,8 @@ void create_impl(tp_ctx* c, const tp_params* p, const tp_dem* dem, int row0, int
     ck(cudaMalloc(&c->dFlagA, ntiles * sizeof(unsigned short)), "cudaMalloc flags");
     ck(cudaMalloc(&c->dFlagB, ntiles * sizeof(unsigned short)), "cudaMalloc flags");
     ck(cudaMalloc(&c->dTiles, sizeof(int) * ntiles), "cudaMalloc tiles");
-    ck(cudaMalloc(&c->dNact, 4 * sizeof(int)), "cudaMalloc tiles");
-    ck(cudaMemsetAsync(c->dNact, 0, 4 * sizeof(int), c->stream), "memset");
+    ck(cudaMalloc(&c->dNact, 6 * sizeof(int)), "cudaMalloc tiles");
+    ck(cudaMemsetAsync(c->dNact, 0, 6 * sizeof(int), c->stream), "memset");
     invalidate_flags(c, true, true);
     {
         // device geometry layout (tp_types.h GeoField): the 14 reference fields
@@ -588,6 +592,13 @@ void create_impl(tp_ctx* c, const tp_params* p, const tp_dem* dem, int row0, int
                 if (i + 1 < c->nx) dg[tpb::G_RJBFX * n + k] = 1.0 / (0.5 * (jb + gjb[gj * gnx + i + 1]));
                 if (gj + 1 < G.ny) dg[tpb::G_RJBFY * n + k] = 1.0 / (0.5 * (jb + gjb[(gj + 1) * gnx + i]));
             }
+        }
+        // safe tiles (tp_kernels.cu stage_phase1<FD, false>) need every face/cell divisor in
+        // the FASTDIV window: jb in [1, 2^100] makes jb and 0.5*(jb_l + jb_r) qualify
+        c->geo_safe = true;
+        for (size_t k = 0; k < n && c->geo_safe; ++k) {
+            const double jb = dg[tpb::G_JB * n + k];
+            c->geo_safe = jb >= 1.0 && jb <= 0x1p100;
         }
         ck(cudaMemsetAsync(c->rawGeo, 0, sizeof(double) * tpb::G_COUNT * c->fs, c->stream), "memset");
         ck(cudaMemcpy2DAsync(c->dGeo, c->pitch * sizeof(double), dg.data(), c->nx * sizeof(double),
@@ -937,8 +948,10 @@ int tp_steps(tp_ctx* c, double t_next, double t_end, long max_steps, double* t, 
             c->graph1 = capture_steps(c, 1);
             c->graphK_steps = c->graph_steps;
         }
-        if (c->last_tiles_stage == 0)  // the graphs start with a predictor list
+        if (c->last_tiles_stage == 0) {  // the graphs start with a predictor list
             ck(cudaMemsetAsync(c->dNact, 0, sizeof(int), c->stream), "memset");
+            ck(cudaMemsetAsync(c->dNact + 4, 0, sizeof(int), c->stream), "memset");
+        }
         c->last_tiles_stage = 1;
         long long done_steps = 0;
         DevScalars h{};
@@ -1185,6 +1198,13 @@ int tp_selftest_minmod(int device, long n, const double* a, const double* b, dou
     if (n <= 0 || !a || !b || !out) return TP_ERR_INTERNAL;
     if (cudaSetDevice(device) != cudaSuccess) return TP_ERR_CUDA;
     return tpb::selftest_minmod(n, a, b, out) == cudaSuccess ? TP_OK : TP_ERR_CUDA;
+}
+
+int tp_safe_tiles(tp_ctx* c, int* corr) {
+    TP_GUARD(c, {
+        ck(cudaMemcpyAsync(corr, c->dNact + 5, sizeof(int), cudaMemcpyDeviceToHost, c->stream), "tiles D2H");
+        ck(cudaStreamSynchronize(c->stream), "sync");
+    })
 }
 
 int tp_active_tiles(tp_ctx* c, int* pred, int* corr, int* total) {

@@ -13,7 +13,8 @@ namespace tpb {
 // XI = true for a xi face (normal X: a_nn = a11, a_nt = a12), false for eta
 // (normal Y: a_nn = a22, a_nt = a21).  out[6] in field order.
 // rjbf = RN(1/jbf) precomputed on the host (geometry field G_RJBFX/G_RJBFY).
-template <bool FD, bool XI>
+// CHK = false: the "safe tile" form without the FASTDIV window tests.
+template <bool FD, bool XI, bool CHK = true>
 __device__ __forceinline__ void face_flux(const double (&L)[6], const double (&R)[6], double jb_l,
                                           double jb_r, double nZ_l, double nZ_r, double ann_l,
                                           double ann_r, double ant_l, double ant_r, double rjbf,
@@ -23,12 +24,12 @@ __device__ __forceinline__ void face_flux(const double (&L)[6], const double (&R
     const double cf = 0.5 * (nZ_l + nZ_r);
     const double ann = 0.5 * (ann_l + ann_r);
     const double ant = 0.5 * (ant_l + ant_r);
-    const Rcp rj = mkrcp_const<FD>(jbf, rjbf);
+    const Rcp rj = mkrcp_const<FD, CHK>(jbf, rjbf);
 
     // solver.cpp:265-275
     bool ok = rj.ok;
-    double hL0 = dq<FD>(L[0], rj, ok), hL1 = dq<FD>(L[1], rj, ok);
-    double hR0 = dq<FD>(R[0], rj, ok), hR1 = dq<FD>(R[1], rj, ok);
+    double hL0 = dq<FD, CHK>(L[0], rj, ok), hL1 = dq<FD, CHK>(L[1], rj, ok);
+    double hR0 = dq<FD, CHK>(R[0], rj, ok), hR1 = dq<FD, CHK>(R[1], rj, ok);
     if (!ok) {
         dfix<FD>(hL0, L[0], rj);
         dfix<FD>(hL1, L[1], rj);
@@ -53,8 +54,8 @@ __device__ __forceinline__ void face_flux(const double (&L)[6], const double (&R
     const double qnR1 = XI ? R[4] : R[5], qtR1 = XI ? R[5] : R[4];
 
     ok = rj.ok;
-    double jL0 = dq<FD>(qnL0, rj, ok), jR0 = dq<FD>(qnR0, rj, ok);
-    double jL1 = dq<FD>(qnL1, rj, ok), jR1 = dq<FD>(qnR1, rj, ok);
+    double jL0 = dq<FD, CHK>(qnL0, rj, ok), jR0 = dq<FD, CHK>(qnR0, rj, ok);
+    double jL1 = dq<FD, CHK>(qnL1, rj, ok), jR1 = dq<FD, CHK>(qnR1, rj, ok);
     if (!ok) {
         dfix<FD>(jL0, qnL0, rj);
         dfix<FD>(jR0, qnR0, rj);
@@ -66,10 +67,10 @@ __device__ __forceinline__ void face_flux(const double (&L)[6], const double (&R
     double fL0, fR0, fL1, fR1;
     if (FD) {  // four desingularisation divisions, one shared slow-path branch
         bool okf = true;
-        fL0 = desing_factor_g(dL0, P.eps_h, okf);
-        fR0 = desing_factor_g(dR0, P.eps_h, okf);
-        fL1 = desing_factor_g(dL1, P.eps_h, okf);
-        fR1 = desing_factor_g(dR1, P.eps_h, okf);
+        fL0 = desing_factor_g<CHK>(dL0, P.eps_h, okf);
+        fR0 = desing_factor_g<CHK>(dR0, P.eps_h, okf);
+        fL1 = desing_factor_g<CHK>(dL1, P.eps_h, okf);
+        fR1 = desing_factor_g<CHK>(dR1, P.eps_h, okf);
         if (!okf) {
             fL0 = desing_factor<FD>(dL0, P.eps_h);
             fR0 = desing_factor<FD>(dR0, P.eps_h);

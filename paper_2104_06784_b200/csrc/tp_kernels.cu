@@ -62,12 +62,19 @@ __device__ __forceinline__ unsigned cell_flag_bits(int cx, int cy) {
            ((e && n) ? TF_NE : 0u);
 }
 
+// +-0, or magnitude in [2^-200, 2^200): the safe-tile window (TF_UNSAFE)
+__device__ __forceinline__ bool in_safe_window(double x) {
+    const unsigned hi2 = static_cast<unsigned>(__double2hiint(x)) << 1;
+    const unsigned lo = static_cast<unsigned>(__double2loint(x));
+    return ((hi2 - ((1023u - 200u) << 21)) < (400u << 21)) | ((hi2 | lo) == 0u);
+}
+
 // regularize + [check_finite + lambda] + store of one updated cell: the tail of
 // advance_step's stages (solver.cpp:139-166, :482-494, :556-573).
 template <bool FD, bool CORR>
 __device__ __forceinline__ unsigned long long cell_epilogue(double (&un)[6], const Rcp& rj, double nZ, int X, int Y,
                                               const Phys& P, DevScalars* sc, double& lam_local,
-                                              double* out, long long fs, long long o3) {
+                                              double* out, long long fs, long long o3, bool& safe_out) {
     // regularize (solver.cpp:139-166), solid then fluid
     double hpv[2];
     {
@@ -141,14 +148,94 @@ __device__ __forceinline__ unsigned long long cell_epilogue(double (&un)[6], con
     }
 
     unsigned long long bits = 0ull;
+    bool inwin = true;
 #pragma unroll
     for (int f = 0; f < 6; ++f) {
         out[f * fs + o3] = un[f];
         bits |= static_cast<unsigned long long>(__double_as_longlong(un[f]));
+        inwin = inwin && in_safe_window(un[f]);
     }
-    return bits;  // feeds the tile's output flag
+    safe_out = inwin;
+    return bits;  // feeds the tile's output flags
 }
 
+
+// Phase 1 of the stage kernel on the staged boxes: xi faces, eta faces and the cell
+// fields of the whole box (see stage_kernel).  CHK = false is the safe-tile form
+// (DESIGN.md §3): every numerator is +-0 or in the FASTDIV window by construction, so
+// the window tests and their fix-up branches are compiled out.
+template <bool FD, bool CHK>
+__device__ __forceinline__ void stage_phase1(const double* __restrict__ S, const double* __restrict__ G,
+                                             double* FX, double* FY, double* V, double* PJ, const Phys& P) {
+    // faces: thread t owns xi face t and eta face t, written as one straight-line
+    // block so the two independent dependency chains interleave (ILP)
+    {
+        const int it = threadIdx.x;
+        const bool hx = it < NFX, hy = it < NFY;
+        const int fx = it % (TX + 1), tyx = it / (TX + 1);
+        const int kx = hx ? (tyx + 2) * W2 + fx + 1 : 2 * W2 + 2;  // xi face between kx and kx+1
+        const int txy = it % TX, fy = it / TX;
+        const int ky = hy ? (fy + 1) * W2 + txy + 2 : 2 * W2 + 2;  // eta face between ky and ky+W2
+        double Lx[6], Rx[6], Ly[6], Ry[6];
+#pragma unroll
+        for (int f = 0; f < 6; ++f) {
+            const double* row = S + f * BOX + kx - 1;
+            const double c0 = row[0], c1 = row[1], c2 = row[2], c3 = row[3];
+            Lx[f] = edge_plus(c0, c1, c2);
+            Rx[f] = edge_minus(c1, c2, c3);
+            const double* col = S + f * BOX + ky - W2;
+            const double d0 = col[0], d1 = col[W2], d2 = col[2 * W2], d3 = col[3 * W2];
+            Ly[f] = edge_plus(d0, d1, d2);
+            Ry[f] = edge_minus(d1, d2, d3);
+        }
+        double ox[6], oy[6];
+        face_flux<FD, true, CHK>(Lx, Rx, G[G_JB * BOX + kx], G[G_JB * BOX + kx + 1], G[G_NZ * BOX + kx],
+                            G[G_NZ * BOX + kx + 1], G[G_A11 * BOX + kx], G[G_A11 * BOX + kx + 1],
+                            G[G_A12 * BOX + kx], G[G_A12 * BOX + kx + 1], G[G_RJBFX * BOX + kx], P, ox);
+        face_flux<FD, false, CHK>(Ly, Ry, G[G_JB * BOX + ky], G[G_JB * BOX + ky + W2], G[G_NZ * BOX + ky],
+                             G[G_NZ * BOX + ky + W2], G[G_A22 * BOX + ky], G[G_A22 * BOX + ky + W2],
+                             G[G_A21 * BOX + ky], G[G_A21 * BOX + ky + W2], G[G_RJBFY * BOX + ky], P, oy);
+        if (hx) {
+#pragma unroll
+            for (int f = 0; f < 6; ++f) FX[f * NFX + it] = ox[f];
+        }
+        if (hy) {
+#pragma unroll
+            for (int f = 0; f < 6; ++f) FY[f * NFY + it] = oy[f];
+        }
+    }
+    for (int k = threadIdx.x; k < BOX; k += NT) {
+        {
+            // cell fields (solver.cpp:172-184) on box cell k
+            if (P.adv_only) continue;  // velocities/pjb feed sources and brackets only
+            const double jb = G[G_JB * BOX + k];
+            const Rcp rj = mkrcp_const<FD, CHK>(jb, G[G_RJB * BOX + k]);
+            const double ws = S[0 * BOX + k], wf = S[1 * BOX + k];
+            const double qsx = S[2 * BOX + k], qsy = S[3 * BOX + k];
+            const double qfx = S[4 * BOX + k], qfy = S[5 * BOX + k];
+            bool ok = rj.ok;
+            double hs = dq<FD, CHK>(ws, rj, ok), hf = dq<FD, CHK>(wf, rj, ok);
+            double jsx = dq<FD, CHK>(qsx, rj, ok), jsy = dq<FD, CHK>(qsy, rj, ok);
+            double jfx = dq<FD, CHK>(qfx, rj, ok), jfy = dq<FD, CHK>(qfy, rj, ok);
+            if (!ok) {
+                dfix<FD>(hs, ws, rj);
+                dfix<FD>(hf, wf, rj);
+                dfix<FD>(jsx, qsx, rj);
+                dfix<FD>(jsy, qsy, rj);
+                dfix<FD>(jfx, qfx, rj);
+                dfix<FD>(jfy, qfy, rj);
+            }
+            const double h = hs + hf;
+            double fsld, fflu;
+            desing_pair<FD, CHK>(hs, hf, P.eps_h, fsld, fflu);
+            V[0 * BOX + k] = jsx * fsld;
+            V[1 * BOX + k] = jsy * fsld;
+            V[2 * BOX + k] = jfx * fflu;
+            V[3 * BOX + k] = jfy * fflu;
+            PJ[k] = jb * h * (G[G_NZ * BOX + k] * h * 0.5);  // solver.cpp:182
+        }
+    }
+}
 
 // ---------------------------------------------------------------------------
 // The fused stage kernel.
@@ -191,7 +278,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
         if (li < nact) {
             const int e = A.tiles[li];
             mbar_expect_tx(&barc, kTmaCellBytes);
-            tma_load_3d(sm + SM_C, &A.tm_c, 3 + (e & 0xffff) * TX + 1, 3 + (e >> 16) * TY, G_NX, &barc);
+            tma_load_3d(sm + SM_C, &A.tm_c, 3 + (e & 0xffff) * TX + 1, 3 + ((e >> 16) & 0x3fff) * TY, G_NX, &barc);
         }
     };
     (void)ntiles;
@@ -201,7 +288,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
         if (static_cast<int>(blockIdx.x) < nact) {
             const int e = A.tiles[blockIdx.x];
             s_tile = e;
-            const int bx0 = 1 + (e & 0xffff) * TX, by0 = 1 + (e >> 16) * TY;
+            const int bx0 = 1 + (e & 0xffff) * TX, by0 = 1 + ((e >> 16) & 0x3fff) * TY;
             mbar_expect_tx(&bar, kTmaBytes);
             // x coordinate + 1: the leading pad column of the device layout (tp_capi.cpp)
             tma_load_3d(S, &A.tm_s, bx0 + 1, by0, 0, &bar);
@@ -216,7 +303,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
     TPROBE_DECL
     for (int li = blockIdx.x; li < nact; li += gridDim.x, ++iter) {
     const int entry = s_tile;  // written by thread 0 before the previous end-of-tile barrier
-    const int tix = entry & 0xffff, tiy = entry >> 16;
+    const int tix = entry & 0xffff, tiy = (entry >> 16) & 0x3fff;
     const int tile = tiy * A.ntx + tix;
     const int X0 = 3 + tix * TX;
     const int Y0 = 3 + tiy * TY;
@@ -237,7 +324,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
         if (threadIdx.x == 0 && nli < nact) {
             const int e = next_entry;
             s_tile = e;
-            const int bx0n = 1 + (e & 0xffff) * TX, by0n = 1 + (e >> 16) * TY;
+            const int bx0n = 1 + (e & 0xffff) * TX, by0n = 1 + ((e >> 16) & 0x3fff) * TY;
             mbar_expect_tx(&bar, kTmaBytes);
             tma_load_3d(S, &A.tm_s, bx0n + 1, by0n, 0, &bar);
             tma_load_3d(sm + SM_G, &A.tm_g, bx0n + 1, by0n, 0, &bar);
@@ -252,74 +339,8 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
     // left off the list by tiles_kernel, and a listed dry tile computes the same +0.0)
 
     // ---- Phase 1: xi faces, eta faces, cell fields -----------------------------
-    // faces: thread t owns xi face t and eta face t, written as one straight-line
-    // block so the two independent dependency chains interleave (ILP)
-    {
-        const int it = threadIdx.x;
-        const bool hx = it < NFX, hy = it < NFY;
-        const int fx = it % (TX + 1), tyx = it / (TX + 1);
-        const int kx = hx ? (tyx + 2) * W2 + fx + 1 : 2 * W2 + 2;  // xi face between kx and kx+1
-        const int txy = it % TX, fy = it / TX;
-        const int ky = hy ? (fy + 1) * W2 + txy + 2 : 2 * W2 + 2;  // eta face between ky and ky+W2
-        double Lx[6], Rx[6], Ly[6], Ry[6];
-#pragma unroll
-        for (int f = 0; f < 6; ++f) {
-            const double* row = S + f * BOX + kx - 1;
-            const double c0 = row[0], c1 = row[1], c2 = row[2], c3 = row[3];
-            Lx[f] = edge_plus(c0, c1, c2);
-            Rx[f] = edge_minus(c1, c2, c3);
-            const double* col = S + f * BOX + ky - W2;
-            const double d0 = col[0], d1 = col[W2], d2 = col[2 * W2], d3 = col[3 * W2];
-            Ly[f] = edge_plus(d0, d1, d2);
-            Ry[f] = edge_minus(d1, d2, d3);
-        }
-        double ox[6], oy[6];
-        face_flux<FD, true>(Lx, Rx, G[G_JB * BOX + kx], G[G_JB * BOX + kx + 1], G[G_NZ * BOX + kx],
-                            G[G_NZ * BOX + kx + 1], G[G_A11 * BOX + kx], G[G_A11 * BOX + kx + 1],
-                            G[G_A12 * BOX + kx], G[G_A12 * BOX + kx + 1], G[G_RJBFX * BOX + kx], P, ox);
-        face_flux<FD, false>(Ly, Ry, G[G_JB * BOX + ky], G[G_JB * BOX + ky + W2], G[G_NZ * BOX + ky],
-                             G[G_NZ * BOX + ky + W2], G[G_A22 * BOX + ky], G[G_A22 * BOX + ky + W2],
-                             G[G_A21 * BOX + ky], G[G_A21 * BOX + ky + W2], G[G_RJBFY * BOX + ky], P, oy);
-        if (hx) {
-#pragma unroll
-            for (int f = 0; f < 6; ++f) FX[f * NFX + it] = ox[f];
-        }
-        if (hy) {
-#pragma unroll
-            for (int f = 0; f < 6; ++f) FY[f * NFY + it] = oy[f];
-        }
-    }
-    for (int k = threadIdx.x; k < BOX; k += NT) {
-        {
-            // cell fields (solver.cpp:172-184) on box cell k
-            if (P.adv_only) continue;  // velocities/pjb feed sources and brackets only
-            const double jb = G[G_JB * BOX + k];
-            const Rcp rj = mkrcp_const<FD>(jb, G[G_RJB * BOX + k]);
-            const double ws = S[0 * BOX + k], wf = S[1 * BOX + k];
-            const double qsx = S[2 * BOX + k], qsy = S[3 * BOX + k];
-            const double qfx = S[4 * BOX + k], qfy = S[5 * BOX + k];
-            bool ok = rj.ok;
-            double hs = dq<FD>(ws, rj, ok), hf = dq<FD>(wf, rj, ok);
-            double jsx = dq<FD>(qsx, rj, ok), jsy = dq<FD>(qsy, rj, ok);
-            double jfx = dq<FD>(qfx, rj, ok), jfy = dq<FD>(qfy, rj, ok);
-            if (!ok) {
-                dfix<FD>(hs, ws, rj);
-                dfix<FD>(hf, wf, rj);
-                dfix<FD>(jsx, qsx, rj);
-                dfix<FD>(jsy, qsy, rj);
-                dfix<FD>(jfx, qfx, rj);
-                dfix<FD>(jfy, qfy, rj);
-            }
-            const double h = hs + hf;
-            double fsld, fflu;
-            desing_pair<FD>(hs, hf, P.eps_h, fsld, fflu);
-            V[0 * BOX + k] = jsx * fsld;
-            V[1 * BOX + k] = jsy * fsld;
-            V[2 * BOX + k] = jfx * fflu;
-            V[3 * BOX + k] = jfy * fflu;
-            PJ[k] = jb * h * (G[G_NZ * BOX + k] * h * 0.5);  // solver.cpp:182
-        }
-    }
+    if (FD && (entry & kTileSafe)) stage_phase1<FD, false>(S, G, FX, FY, V, PJ, P);
+    else stage_phase1<FD, true>(S, G, FX, FY, V, PJ, P);
     TPROBE(4);  // Phase 1 work
     __syncthreads();
     TPROBE(5);  // Phase 1 barrier
@@ -481,6 +502,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
     const Rcp rdx = mkrcp_const<FD>(P.dxi, P.r_dxi);
     const Rcp rdy = mkrcp_const<FD>(P.deta, P.r_deta);
     unsigned long long obits = 0ull;
+    bool osafe = true;
     if (p3) {
         const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
         const int X = p3x, Y = p3y;
@@ -598,7 +620,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
         }
 
         TPROBE(13);  // phase 3: Heun average
-        obits = cell_epilogue<FD, CORR>(un, rj, nZ, X, Y, P, sc, lam_local, A.out, fs, o3);
+        obits = cell_epilogue<FD, CORR>(un, rj, nZ, X, Y, P, sc, lam_local, A.out, fs, o3, osafe);
         TPROBE(14);  // phase 3: regularize, finite, lambda, stores
     }
 
@@ -634,7 +656,8 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
     // the tile's output flags: warp OR, one shared atomic per warp; the end-of-tile
     // barrier (FX/FY/V/PJ/BR/cell box are rewritten by the next tile) publishes them
     {
-        const unsigned fb = (p3 && obits != 0ull) ? cell_flag_bits(threadIdx.x % TX, threadIdx.x / TX) : 0u;
+        const unsigned fb = ((p3 && obits != 0ull) ? cell_flag_bits(threadIdx.x % TX, threadIdx.x / TX) : 0u) |
+                            (osafe ? 0u : static_cast<unsigned>(TF_UNSAFE));
         const unsigned wf = __reduce_or_sync(0xffffffffu, fb);
         if ((threadIdx.x & 31) == 0 && wf) atomicOr(&s_flags, wf);
     }
@@ -659,7 +682,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
 __device__ __forceinline__ void tiles_body(const TileArgs& a, int block) {
     const int ntiles = a.ntx * a.nty;
     const int t = block * blockDim.x + threadIdx.x;
-    bool active = false;
+    bool active = false, safe = false;
     if (t < ntiles) {
         const int tx = t % a.ntx, ty = t / a.ntx;
         const bool ring = tx == 0 || tx == a.ntx - 1 || ty == 0 || ty == a.nty - 1;
@@ -684,6 +707,23 @@ __device__ __forceinline__ void tiles_body(const TileArgs& a, int block) {
             skip = need == 0u;
         }
         active = !skip;
+        if (active && a.safe_ok && !(ring && a.ring_ineligible) && !(ty == 0 && a.south_ineligible) &&
+            !(ty == a.nty - 1 && a.north_ineligible)) {
+            // safe: no value the box reads (this tile and the facing parts of its 8
+            // neighbours; ghosts are clamp copies of them) is outside the window
+            const unsigned short* F = a.flag_in;
+            unsigned u = F[t];
+            const bool xl = tx > 0, xr = tx < a.ntx - 1, yl = ty > 0, yr = ty < a.nty - 1;
+            if (xl) u |= F[t - 1];
+            if (xr) u |= F[t + 1];
+            if (yl) u |= F[t - a.ntx];
+            if (yr) u |= F[t + a.ntx];
+            if (xl && yl) u |= F[t - a.ntx - 1];
+            if (xr && yl) u |= F[t - a.ntx + 1];
+            if (xl && yr) u |= F[t + a.ntx - 1];
+            if (xr && yr) u |= F[t + a.ntx + 1];
+            safe = (u & TF_UNSAFE) == 0u;
+        }
         if (skip && ring) {
 #pragma unroll
             for (int q = 0; q < 4; ++q) a.tally[4ll * t + q] = 0.0;
@@ -691,13 +731,19 @@ __device__ __forceinline__ void tiles_body(const TileArgs& a, int block) {
     }
     // the other stage's counter was consumed by the stage before this one and is
     // appended to only after this stage: reset it here (saves a memset node)
-    if (t == 0) *a.ntiles_reset = 0;
+    if (t == 0) {
+        *a.ntiles_reset = 0;
+        a.ntiles_reset[4] = 0;  // the other stage's safe-tile count (diagnostics)
+    }
     const unsigned m = __ballot_sync(0xffffffffu, active);
+    const unsigned ms = __ballot_sync(0xffffffffu, active && safe);
     const int lane = threadIdx.x & 31;
     int base = 0;
     if (lane == 0 && m) base = atomicAdd(a.ntiles_active, __popc(m));
+    if (lane == 0 && ms) atomicAdd(a.ntiles_active + 4, __popc(ms));
     base = __shfl_sync(0xffffffffu, base, 0);
-    if (active) a.tiles[base + __popc(m & ((1u << lane) - 1u))] = ((t / a.ntx) << 16) | (t % a.ntx);
+    if (active)
+        a.tiles[base + __popc(m & ((1u << lane) - 1u))] = ((t / a.ntx) << 16) | (t % a.ntx) | (safe ? kTileSafe : 0);
 }
 
 __global__ void __launch_bounds__(NT) tiles_kernel(TileArgs a) {

@@ -120,10 +120,14 @@ struct StageArgs {
 
 // Per-tile output flags: which regions of the tile's interior hold a value with a nonzero
 // bit (the 2-cell bands and 2x2 corners are what a neighbour's radius-2 box reads).
+// TF_UNSAFE: some output value is neither +-0 nor of magnitude in [2^-200, 2^200)
+// (the "safe tile" window).
 enum TileFlag : unsigned {
     TF_ANY = 1u, TF_W = 2u, TF_E = 4u, TF_S = 8u, TF_N = 16u,
-    TF_SW = 32u, TF_SE = 64u, TF_NW = 128u, TF_NE = 256u, TF_ALL = 0xffffu
+    TF_SW = 32u, TF_SE = 64u, TF_NW = 128u, TF_NE = 256u, TF_UNSAFE = 512u, TF_ALL = 0xffffu
 };
+// list-entry bit: every state value the tile's box reads is +-0 or in the safe window
+constexpr int kTileSafe = 1 << 30;
 
 // Dry-tile classification before a stage.  flag_in: per-tile flags of the stage's input
 // buffer (the radius-2 box reads interior cells of the tile and the facing bands/corners
@@ -135,13 +139,15 @@ struct TileArgs {
     const unsigned short* flag_in;
     const unsigned short* flag_out;
     int* tiles;
-    int* ntiles_active;   // this stage's counter (zeroed by the other stage's tiles_kernel)
+    int* ntiles_active;   // this stage's counter (zeroed by the other stage's tiles_kernel);
+                          // [4] past it: this stage's safe-tile count
     int* ntiles_reset;    // the other stage's counter
     double* tally;
     int ntx, nty;
     int skip;             // 0 = list every tile
     int ring_ineligible;  // 1 = ring tiles read non-copy ghosts (Mode-II inflow): never skip them
     int south_ineligible, north_ineligible;  // slab edges next to halo rows: never skip
+    int safe_ok;          // FASTDIV on and the context's geometry divisors in the window
     int loop;
     DevScalars* sc;
 };

@@ -197,6 +197,12 @@ class Simulator:
         self._check(self.L.tp_active_tiles(self.h, C.byref(p), C.byref(c), C.byref(t)))
         return p.value, c.value, t.value
 
+    def safe_tiles(self) -> int:
+        """Tiles of the last corrector list that ran the safe (window-test-free) path."""
+        n = C.c_int()
+        self._check(self.L.tp_safe_tiles(self.h, C.byref(n)))
+        return n.value
+
     def synchronize(self) -> None:
         self._check(self.L.tp_synchronize(self.h))
 

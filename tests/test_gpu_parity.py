@@ -191,6 +191,33 @@ def test_signed_zero_state(gpu, oracle_kind):
     assert_bitwise(sim.state(), ref.state(), "state with signed zeros")
 
 
+def test_safe_window_edges(gpu, oracle_kind):
+    """Values outside the safe-tile window (nonzero magnitudes below 2^-200 or
+    at/above 2^200, subnormals) mark their tile and its neighbours unsafe, which then take
+    the checked FASTDIV path; the rest of the grid keeps the safe path.  Both must match."""
+    sc = scenarios.wet_valley(96, 80)
+    ref, sim = _pair(sc, oracle_kind)
+    ref.steps(0.0, 1.0e9, 5, t_end=1.0e9)  # a developed state with nonzero momenta
+    s = ref.state()
+    s[0, 10, 10] = 2.0 ** -201          # just below the window (thickness)
+    s[3, 30, 40] = 5e-310               # subnormal momentum
+    s[4, 50, 20] = -(2.0 ** -200)       # the window's lower edge: still safe
+    s[2, 60, 70] = 2.0 ** -180          # tiny but inside
+    s[5, 70, 90] = 2.0 ** 200           # the window's upper edge: unsafe
+    ref.set_state(s)
+    sim.set_state(s)
+    # two stages warm the flags (set_state marks every tile unknown), then steps run
+    # with a mix of safe and unsafe tiles
+    tr, dts_r, _ = ref.steps(0.0, 1.0e9, 30, t_end=1.0e9)
+    t1, dts_1, _ = sim.steps(0.0, 1.0e9, 2, t_end=1.0e9, record_dts=True)
+    act_p, act_c, ntiles = sim.active_tiles()
+    safe = sim.safe_tiles()
+    assert 0 < safe < act_c, (safe, act_c)  # both paths ran in the last corrector
+    tg, dts_g, _ = sim.steps(t1, 1.0e9, 28, t_end=1.0e9, record_dts=True)
+    assert_bitwise(np.concatenate([dts_1, dts_g]), dts_r, "dt sequence")
+    assert_bitwise(sim.state(), ref.state(), "state around out-of-window values")
+
+
 @pytest.mark.parametrize("make", [lambda: scenarios.c1_hill(96), lambda: scenarios.wet_valley(96, 80),
                                   lambda: scenarios.c3_channel(96, 48, t_end=30.0, dt_out=0.5)])
 def test_full_tile_list_bitwise(gpu, oracle_kind, make):
