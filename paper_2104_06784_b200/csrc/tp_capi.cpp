@@ -131,6 +131,7 @@ struct tp_ctx {
     int graph_steps = 16;
     bool skip_dry = true;  // list only tiles that are not bitwise no-ops (tiles_kernel)
     bool geo_safe = false; // every jb (and so every face jbf) in [1, 2^100]: safe tiles allowed
+    bool geo_safe2 = false; // geometry and constants inside the window-B bounds
     unsigned short* dFlagA = nullptr;  // per-tile TileFlag bits of A / B (all set = unknown)
     unsigned short* dFlagB = nullptr;
     int* dTiles = nullptr;            // active-tile list of the stage in flight + its count
@@ -264,6 +265,7 @@ tpb::TileArgs tile_args(tp_ctx* c, const tpb::StageArgs& a, bool corr) {
     t.south_ineligible = c->g.has_south ? 0 : 1;
     t.north_ineligible = c->g.has_north ? 0 : 1;
     t.safe_ok = (c->fastdiv && c->geo_safe) ? 1 : 0;
+    t.safe2_ok = (t.safe_ok && c->geo_safe2) ? 1 : 0;
     t.loop = a.loop;
     t.sc = c->dSc;
     return t;
@@ -599,6 +601,26 @@ void create_impl(tp_ctx* c, const tp_params* p, const tp_dem* dem, int row0, int
         for (size_t k = 0; k < n && c->geo_safe; ++k) {
             const double jb = dg[tpb::G_JB * n + k];
             c->geo_safe = jb >= 1.0 && jb <= 0x1p100;
+        }
+        // window B (Phase 2 + Phase-3 divergence without window tests) assumes every
+        // geometry value is 0 or of magnitude in [2^-50, 2^50], jb <= 2^50, and the
+        // constants that enter numerators within 2^+-20 (eps_h within [2^-60, 2^20]);
+        // the bound chain is in DESIGN.md §3
+        auto mag_ok = [](double v, double lo, double hi) {
+            const double a = std::fabs(v);
+            return a == 0.0 || (a >= lo && a <= hi);
+        };
+        c->geo_safe2 = c->geo_safe;
+        for (size_t k = 0; k < 14 * n && c->geo_safe2; ++k)
+            c->geo_safe2 = std::isfinite(c->geo_h[k]) && mag_ok(c->geo_h[k], 0x1p-50, 0x1p50);
+        for (size_t k = 0; k < n && c->geo_safe2; ++k) c->geo_safe2 = dg[tpb::G_JB * n + k] <= 0x1p50;
+        {
+            const tpb::Phys& P = c->ph;
+            const double w20 = 0x1p20, n20 = 0x1p-20;
+            c->geo_safe2 = c->geo_safe2 && P.eps_h >= 0x1p-60 && P.eps_h <= w20 && P.eps >= n20 &&
+                           P.eps <= w20 && mag_ok(P.oma, n20, 1.0) && mag_ok(P.theta_b, n20, w20) &&
+                           P.N_R >= n20 && P.N_R <= w20 && P.dxi >= n20 && P.dxi <= w20 &&
+                           P.deta >= n20 && P.deta <= w20;
         }
         ck(cudaMemsetAsync(c->rawGeo, 0, sizeof(double) * tpb::G_COUNT * c->fs, c->stream), "memset");
         ck(cudaMemcpy2DAsync(c->dGeo, c->pitch * sizeof(double), dg.data(), c->nx * sizeof(double),

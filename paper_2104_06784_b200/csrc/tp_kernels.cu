@@ -21,6 +21,8 @@
 //   check_finite: (2 << 62) | (field << 56) | (j << 28) | i
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include "tp_face.cuh"
 #include "tp_stage_common.cuh"
 #include "tp_types.h"
@@ -69,12 +71,20 @@ __device__ __forceinline__ bool in_safe_window(double x) {
     return ((hi2 - ((1023u - 200u) << 21)) < (400u << 21)) | ((hi2 | lo) == 0u);
 }
 
+// window B of the safe-tile form of Phase 2 and the Phase-3 divergence (TF_UNSAFE2)
+__device__ __forceinline__ bool in_safe_window2(double x) {
+    const unsigned hi2 = static_cast<unsigned>(__double2hiint(x)) << 1;
+    const unsigned lo = static_cast<unsigned>(__double2loint(x));
+    return ((hi2 - ((1023u - 100u) << 21)) < (200u << 21)) | ((hi2 | lo) == 0u);
+}
+
 // regularize + [check_finite + lambda] + store of one updated cell: the tail of
 // advance_step's stages (solver.cpp:139-166, :482-494, :556-573).
 template <bool FD, bool CORR>
 __device__ __forceinline__ unsigned long long cell_epilogue(double (&un)[6], const Rcp& rj, double nZ, int X, int Y,
                                               const Phys& P, DevScalars* sc, double& lam_local,
-                                              double* out, long long fs, long long o3, bool& safe_out) {
+                                              double* out, long long fs, long long o3, bool& safe_out,
+                                              bool& safe2_out) {
     // regularize (solver.cpp:139-166), solid then fluid
     double hpv[2];
     {
@@ -148,14 +158,18 @@ __device__ __forceinline__ unsigned long long cell_epilogue(double (&un)[6], con
     }
 
     unsigned long long bits = 0ull;
-    bool inwin = true;
+    bool inwin = true, inwin2 = true;
 #pragma unroll
     for (int f = 0; f < 6; ++f) {
         out[f * fs + o3] = un[f];
         bits |= static_cast<unsigned long long>(__double_as_longlong(un[f]));
         inwin = inwin && in_safe_window(un[f]);
+        inwin2 = inwin2 && in_safe_window2(un[f]);
     }
+    // window B also needs non-negative thicknesses (no cancellation in hs + hf)
+    inwin2 = inwin2 && (__double2hiint(un[0]) >= 0 || un[0] == 0.0) && (__double2hiint(un[1]) >= 0 || un[1] == 0.0);
     safe_out = inwin;
+    safe2_out = inwin2;
     return bits;  // feeds the tile's output flags
 }
 
@@ -278,7 +292,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
         if (li < nact) {
             const int e = A.tiles[li];
             mbar_expect_tx(&barc, kTmaCellBytes);
-            tma_load_3d(sm + SM_C, &A.tm_c, 3 + (e & 0xffff) * TX + 1, 3 + ((e >> 16) & 0x3fff) * TY, G_NX, &barc);
+            tma_load_3d(sm + SM_C, &A.tm_c, 3 + (e & 0xffff) * TX + 1, 3 + ((e >> 16) & 0x1fff) * TY, G_NX, &barc);
         }
     };
     (void)ntiles;
@@ -288,7 +302,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
         if (static_cast<int>(blockIdx.x) < nact) {
             const int e = A.tiles[blockIdx.x];
             s_tile = e;
-            const int bx0 = 1 + (e & 0xffff) * TX, by0 = 1 + ((e >> 16) & 0x3fff) * TY;
+            const int bx0 = 1 + (e & 0xffff) * TX, by0 = 1 + ((e >> 16) & 0x1fff) * TY;
             mbar_expect_tx(&bar, kTmaBytes);
             // x coordinate + 1: the leading pad column of the device layout (tp_capi.cpp)
             tma_load_3d(S, &A.tm_s, bx0 + 1, by0, 0, &bar);
@@ -303,7 +317,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
     TPROBE_DECL
     for (int li = blockIdx.x; li < nact; li += gridDim.x, ++iter) {
     const int entry = s_tile;  // written by thread 0 before the previous end-of-tile barrier
-    const int tix = entry & 0xffff, tiy = (entry >> 16) & 0x3fff;
+    const int tix = entry & 0xffff, tiy = (entry >> 16) & 0x1fff;
     const int tile = tiy * A.ntx + tix;
     const int X0 = 3 + tix * TX;
     const int Y0 = 3 + tiy * TY;
@@ -324,7 +338,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
         if (threadIdx.x == 0 && nli < nact) {
             const int e = next_entry;
             s_tile = e;
-            const int bx0n = 1 + (e & 0xffff) * TX, by0n = 1 + ((e >> 16) & 0x3fff) * TY;
+            const int bx0n = 1 + (e & 0xffff) * TX, by0n = 1 + ((e >> 16) & 0x1fff) * TY;
             mbar_expect_tx(&bar, kTmaBytes);
             tma_load_3d(S, &A.tm_s, bx0n + 1, by0n, 0, &bar);
             tma_load_3d(sm + SM_G, &A.tm_g, bx0n + 1, by0n, 0, &bar);
@@ -351,135 +365,144 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
     // so that the 16 threads without a cell take the 62 extra brackets.
     const Rcp r2x = mkrcp_const<FD>(P.two_dxi, P.r_two_dxi);
     const Rcp r2y = mkrcp_const<FD>(P.two_deta, P.r_two_deta);
-    const Rcp rNR = mkrcp_const<FD>(P.N_R, P.r_NR);
     // partial rhs sums in the reference's order: rhs[2] = div + ((sn + sf) + sv),
     // rhs[4] = div + ((((sn + sd) + sf) + sv) + svis)  (solver.cpp:442-445)
     double Ps2 = 0.0, Ps3 = 0.0, Pf4 = 0.0, Pf5 = 0.0, visc = 0.0;
     mbar_wait(&barc, iter & 1u);
     TPROBE(6);  // cell-geometry box wait
-    const int cidx = threadIdx.x;  // (ty*TX + tx) of this thread's Phase-3 cell
-    if (p3 && !P.adv_only) {
-        const int bk = (threadIdx.x / TX + 2) * W2 + (threadIdx.x % TX + 2);
-        const double nX = Cg[0 * TX * TY + cidx], nY = Cg[1 * TX * TY + cidx];
-        const double dXx = Cg[2 * TX * TY + cidx], dYx = Cg[3 * TX * TY + cidx];
-        const double dZx = Cg[4 * TX * TY + cidx], dXy = Cg[5 * TX * TY + cidx];
-        const double dYy = Cg[6 * TX * TY + cidx], dZy = Cg[7 * TX * TY + cidx];
-        const double nZ = G[G_NZ * BOX + bk];
-        const Rcp rnz = mkrcp_const<FD>(nZ, Cg[8 * TX * TY + cidx]);
-        const double jb = G[G_JB * BOX + bk];
-        const Rcp rj = mkrcp_const<FD>(jb, G[G_RJB * BOX + bk]);
-        const double a11 = G[G_A11 * BOX + bk], a12 = G[G_A12 * BOX + bk];
-        const double a21 = G[G_A21 * BOX + bk], a22 = G[G_A22 * BOX + bk];
-        const double ws = S[0 * BOX + bk], wf = S[1 * BOX + bk];
-        const double gpx = PJ[bk + 1] - PJ[bk - 1], gpy = PJ[bk + W2] - PJ[bk - W2];
-        const double vsx = V[0 * BOX + bk], vsy = V[1 * BOX + bk];
-        const double vfx = V[2 * BOX + bk], vfy = V[3 * BOX + bk];
-        const double nzs = -(nX * vsx + nY * vsy), nzf = -(nX * vfx + nY * vfy);
-        const Rcp reNR = mkrcp_const<FD>(P.eps_NR, P.r_eps_NR);
-        bool ok2 = rj.ok && rnz.ok && r2x.ok && r2y.ok;
-        double hs = dq<FD>(ws, rj, ok2), hf = dq<FD>(wf, rj, ok2);
-        double vzs = dq<FD>(nzs, rnz, ok2), vzf = dq<FD>(nzf, rnz, ok2);
-        double gPx = dq<FD>(gpx, r2x, ok2), gPy = dq<FD>(gpy, r2y, ok2);
-        if (!ok2) {
-            dfix<FD>(hs, ws, rj);
-            dfix<FD>(hf, wf, rj);
-            dfix<FD>(vzs, nzs, rnz);
-            dfix<FD>(vzf, nzf, rnz);
-            dfix<FD>(gPx, gpx, r2x);
-            dfix<FD>(gPy, gpy, r2y);
-        }
-        const double h = hs + hf;
-        double phi_s = 0.0, phi_f = 0.0, hsf_h = 0.0;
-        if (!(h <= 0.0)) {
-            const Rcp rh = mkrcp<FD>(h);
-            const double hsf = hs * hf;
-            bool okh = rh.ok;
-            double q1 = dq<FD>(hs, rh, okh), q2 = dq<FD>(hf, rh, okh), q3 = dq<FD>(hsf, rh, okh);
-            if (!okh) {
-                dfix<FD>(q1, hs, rh);
-                dfix<FD>(q2, hf, rh);
-                dfix<FD>(q3, hsf, rh);
+    // (a) + (b) as a generic lambda: CHK = false is the safe-tile form (DESIGN.md §3,
+    // window B: every box value +-0 or of magnitude in [2^-100, 2^100), geometry and
+    // constants checked at setup) with the FASTDIV window tests compiled out
+    const bool safe2 = FD && (entry & kTileSafe2);
+    auto phase2 = [&](auto chk_tag) {
+        constexpr bool CHK = decltype(chk_tag)::value;
+        const Rcp rNRc = mkrcp_const<FD, CHK>(P.N_R, P.r_NR);
+        const int cidx = threadIdx.x;  // (ty*TX + tx) of this thread's Phase-3 cell
+        if (p3 && !P.adv_only) {
+            const int bk = (threadIdx.x / TX + 2) * W2 + (threadIdx.x % TX + 2);
+            const double nX = Cg[0 * TX * TY + cidx], nY = Cg[1 * TX * TY + cidx];
+            const double dXx = Cg[2 * TX * TY + cidx], dYx = Cg[3 * TX * TY + cidx];
+            const double dZx = Cg[4 * TX * TY + cidx], dXy = Cg[5 * TX * TY + cidx];
+            const double dYy = Cg[6 * TX * TY + cidx], dZy = Cg[7 * TX * TY + cidx];
+            const double nZ = G[G_NZ * BOX + bk];
+            const Rcp rnz = mkrcp_const<FD, CHK>(nZ, Cg[8 * TX * TY + cidx]);
+            const double jb = G[G_JB * BOX + bk];
+            const Rcp rj = mkrcp_const<FD, CHK>(jb, G[G_RJB * BOX + bk]);
+            const double a11 = G[G_A11 * BOX + bk], a12 = G[G_A12 * BOX + bk];
+            const double a21 = G[G_A21 * BOX + bk], a22 = G[G_A22 * BOX + bk];
+            const double ws = S[0 * BOX + bk], wf = S[1 * BOX + bk];
+            const double gpx = PJ[bk + 1] - PJ[bk - 1], gpy = PJ[bk + W2] - PJ[bk - W2];
+            const double vsx = V[0 * BOX + bk], vsy = V[1 * BOX + bk];
+            const double vfx = V[2 * BOX + bk], vfy = V[3 * BOX + bk];
+            const double nzs = -(nX * vsx + nY * vsy), nzf = -(nX * vfx + nY * vfy);
+            const Rcp reNR = mkrcp_const<FD, CHK>(P.eps_NR, P.r_eps_NR);
+            bool ok2 = rj.ok && rnz.ok && (!CHK || (r2x.ok && r2y.ok));
+            double hs = dq<FD, CHK>(ws, rj, ok2), hf = dq<FD, CHK>(wf, rj, ok2);
+            double vzs = dq<FD, CHK>(nzs, rnz, ok2), vzf = dq<FD, CHK>(nzf, rnz, ok2);
+            double gPx = dq<FD, CHK>(gpx, r2x, ok2), gPy = dq<FD, CHK>(gpy, r2y, ok2);
+            if (!ok2) {
+                dfix<FD>(hs, ws, rj);
+                dfix<FD>(hf, wf, rj);
+                dfix<FD>(vzs, nzs, rnz);
+                dfix<FD>(vzf, nzf, rnz);
+                dfix<FD>(gPx, gpx, r2x);
+                dfix<FD>(gPy, gpy, r2y);
             }
-            if (!(h < P.h_dry)) {  // phi = h < h_dry ? 0 : hs / h  (solver.cpp:410-411)
-                phi_s = q1;
-                phi_f = q2;
+            const double h = hs + hf;
+            double phi_s = 0.0, phi_f = 0.0, hsf_h = 0.0;
+            if (!(h <= 0.0)) {
+                const Rcp rh = mkrcp<FD, CHK>(h);
+                const double hsf = hs * hf;
+                bool okh = rh.ok;
+                double q1 = dq<FD, CHK>(hs, rh, okh), q2 = dq<FD, CHK>(hf, rh, okh), q3 = dq<FD, CHK>(hsf, rh, okh);
+                if (!okh) {
+                    dfix<FD>(q1, hs, rh);
+                    dfix<FD>(q2, hf, rh);
+                    dfix<FD>(q3, hsf, rh);
+                }
+                if (!(h < P.h_dry)) {  // phi = h < h_dry ? 0 : hs / h  (solver.cpp:410-411)
+                    phi_s = q1;
+                    phi_f = q2;
+                }
+                hsf_h = q3;
             }
-            hsf_h = q3;
-        }
-        // physics::curvature_accel (physics.hpp:47-52) with vz from tangency
-        const double kap_s = ((vsx * dXx + vsy * dYx) + vzs * dZx) * vsx + ((vsx * dXy + vsy * dYy) + vzs * dZy) * vsy;
-        const double kap_f = ((vfx * dXx + vfy * dYx) + vzf * dZx) * vfx + ((vfx * dXy + vfy * dYy) + vzf * dZy) * vfy;
-        // physics::hydrostatic_terms (physics.hpp:56-69)
-        const double p_b_s = smax(0.0, hs * (nZ * P.oma - P.eps_chi * kap_s));
-        const double p_b_f = smax(0.0, hf * (nZ - P.eps_chi * kap_f));
-        // solid: gravity + pressure gradient + drag (physics.hpp:98-155)
-        const double sn_sx = jb * p_b_s * nX, sn_sy = jb * p_b_s * nY;
-        const double Avx = a11 * gPx + a21 * gPy;
-        const double Avy = a12 * gPx + a22 * gPy;
-        const double fsp = P.neg_eps_alpha * phi_s;
-        double sv_sx = 0.0, sv_sy = 0.0, sv_fx = 0.0, sv_fy = 0.0;
-        if (!(h <= 0.0)) {
-            const double common = jb * P.C_d * hsf_h;
-            const double cx = common * (vfx - vsx);
-            const double cy = common * (vfy - vsy);
-            sv_sx = P.alpha * cx;
-            sv_sy = P.alpha * cy;
-            sv_fx = -cx;
-            sv_fy = -cy;
-        }
-        // fluid: gravity + friction + pressure gradient + drag (+ viscous in Phase 3)
-        const double sn_fx = jb * p_b_f * nX, sn_fy = jb * p_b_f * nY;
-        const double coeff = dv<FD>(jb * hf * P.theta_b, reNR);
-        const double ephf = P.eps * phi_f;
-        visc = dv<FD>(ephf, rNR);
-        Ps2 = sn_sx + fsp * Avx + sv_sx;
-        Ps3 = sn_sy + fsp * Avy + sv_sy;
-        Pf4 = sn_fx + -coeff * vfx + ephf * Avx + sv_fx;
-        Pf5 = sn_fy + -coeff * vfy + ephf * Avy + sv_fy;
-    }
-    if (!P.adv_only) {
-        constexpr int NB1 = (TX + 2) * TY;  // rows 2..TY+1, cols 1..TX+2
-        constexpr int NB = NB1 + 2 * TX;    // + rows 1 and TY+2, cols 2..TX+1
-        // threads with a Phase-3 cell: one bracket each; the rest stride over the remainder
-        const int stride = threadIdx.x < TX * TY ? NB : NT - TX * TY;
-        for (int it = threadIdx.x; it < NB; it += stride) {
-            int bx, by;
-            if (it < NB1) {
-                bx = 1 + it % (TX + 2);
-                by = 2 + it / (TX + 2);
-            } else {
-                const int r = it - NB1;
-                bx = 2 + r % TX;
-                by = (r < TX) ? 1 : TY + 2;
+            // physics::curvature_accel (physics.hpp:47-52) with vz from tangency
+            const double kap_s = ((vsx * dXx + vsy * dYx) + vzs * dZx) * vsx + ((vsx * dXy + vsy * dYy) + vzs * dZy) * vsy;
+            const double kap_f = ((vfx * dXx + vfy * dYx) + vzf * dZx) * vfx + ((vfx * dXy + vfy * dYy) + vzf * dZy) * vfy;
+            // physics::hydrostatic_terms (physics.hpp:56-69)
+            const double p_b_s = smax(0.0, hs * (nZ * P.oma - P.eps_chi * kap_s));
+            const double p_b_f = smax(0.0, hf * (nZ - P.eps_chi * kap_f));
+            // solid: gravity + pressure gradient + drag (physics.hpp:98-155)
+            const double sn_sx = jb * p_b_s * nX, sn_sy = jb * p_b_s * nY;
+            const double Avx = a11 * gPx + a21 * gPy;
+            const double Avy = a12 * gPx + a22 * gPy;
+            const double fsp = P.neg_eps_alpha * phi_s;
+            double sv_sx = 0.0, sv_sy = 0.0, sv_fx = 0.0, sv_fy = 0.0;
+            if (!(h <= 0.0)) {
+                const double common = jb * P.C_d * hsf_h;
+                const double cx = common * (vfx - vsx);
+                const double cy = common * (vfy - vsy);
+                sv_sx = P.alpha * cx;
+                sv_sy = P.alpha * cy;
+                sv_fx = -cx;
+                sv_fy = -cy;
             }
-            const int k = by * W2 + bx;
-            const double jb = G[G_JB * BOX + k];
-            const double a11 = G[G_A11 * BOX + k], a12 = G[G_A12 * BOX + k];
-            const double a21 = G[G_A21 * BOX + k], a22 = G[G_A22 * BOX + k];
-            const Rcp rj = mkrcp_const<FD>(jb, G[G_RJB * BOX + k]);
-            // solver.cpp:197-205 + physics::viscous_brackets (physics.hpp:166-174)
-            const double* vxf = V + 2 * BOX;
-            const double* vyf = V + 3 * BOX;
-            const double n0 = S[0 * BOX + k] + S[1 * BOX + k];
-            const double n1 = vxf[k + 1] - vxf[k - 1], n2 = vxf[k + W2] - vxf[k - W2];
-            const double n3 = vyf[k + 1] - vyf[k - 1], n4 = vyf[k + W2] - vyf[k - W2];
-            bool ok = rj.ok && r2x.ok && r2y.ok;
-            double h = dq<FD>(n0, rj, ok);
-            double gux = dq<FD>(n1, r2x, ok), guy = dq<FD>(n2, r2y, ok);
-            double gwx = dq<FD>(n3, r2x, ok), gwy = dq<FD>(n4, r2y, ok);
-            if (!ok) {
-                dfix<FD>(h, n0, rj);
-                dfix<FD>(gux, n1, r2x);
-                dfix<FD>(guy, n2, r2y);
-                dfix<FD>(gwx, n3, r2x);
-                dfix<FD>(gwy, n4, r2y);
-            }
-            const double jh = jb * h;
-            BR[0 * BOX + k] = jh * (a11 * gux + a21 * guy);
-            BR[1 * BOX + k] = jh * (a12 * gwx + a22 * gwy);
-            BR[2 * BOX + k] = jh * ((a12 * gux + a22 * guy) + (a11 * gwx + a21 * gwy));
+            // fluid: gravity + friction + pressure gradient + drag (+ viscous in Phase 3)
+            const double sn_fx = jb * p_b_f * nX, sn_fy = jb * p_b_f * nY;
+            const double coeff = dv<FD, CHK>(jb * hf * P.theta_b, reNR);
+            const double ephf = P.eps * phi_f;
+            visc = dv<FD, CHK>(ephf, rNRc);
+            Ps2 = sn_sx + fsp * Avx + sv_sx;
+            Ps3 = sn_sy + fsp * Avy + sv_sy;
+            Pf4 = sn_fx + -coeff * vfx + ephf * Avx + sv_fx;
+            Pf5 = sn_fy + -coeff * vfy + ephf * Avy + sv_fy;
         }
-    }
+        if (!P.adv_only) {
+            constexpr int NB1 = (TX + 2) * TY;  // rows 2..TY+1, cols 1..TX+2
+            constexpr int NB = NB1 + 2 * TX;    // + rows 1 and TY+2, cols 2..TX+1
+            // threads with a Phase-3 cell: one bracket each; the rest stride over the remainder
+            const int stride = threadIdx.x < TX * TY ? NB : NT - TX * TY;
+            for (int it = threadIdx.x; it < NB; it += stride) {
+                int bx, by;
+                if (it < NB1) {
+                    bx = 1 + it % (TX + 2);
+                    by = 2 + it / (TX + 2);
+                } else {
+                    const int r = it - NB1;
+                    bx = 2 + r % TX;
+                    by = (r < TX) ? 1 : TY + 2;
+                }
+                const int k = by * W2 + bx;
+                const double jb = G[G_JB * BOX + k];
+                const double a11 = G[G_A11 * BOX + k], a12 = G[G_A12 * BOX + k];
+                const double a21 = G[G_A21 * BOX + k], a22 = G[G_A22 * BOX + k];
+                const Rcp rj = mkrcp_const<FD, CHK>(jb, G[G_RJB * BOX + k]);
+                // solver.cpp:197-205 + physics::viscous_brackets (physics.hpp:166-174)
+                const double* vxf = V + 2 * BOX;
+                const double* vyf = V + 3 * BOX;
+                const double n0 = S[0 * BOX + k] + S[1 * BOX + k];
+                const double n1 = vxf[k + 1] - vxf[k - 1], n2 = vxf[k + W2] - vxf[k - W2];
+                const double n3 = vyf[k + 1] - vyf[k - 1], n4 = vyf[k + W2] - vyf[k - W2];
+                bool ok = rj.ok && (!CHK || (r2x.ok && r2y.ok));
+                double h = dq<FD, CHK>(n0, rj, ok);
+                double gux = dq<FD, CHK>(n1, r2x, ok), guy = dq<FD, CHK>(n2, r2y, ok);
+                double gwx = dq<FD, CHK>(n3, r2x, ok), gwy = dq<FD, CHK>(n4, r2y, ok);
+                if (!ok) {
+                    dfix<FD>(h, n0, rj);
+                    dfix<FD>(gux, n1, r2x);
+                    dfix<FD>(guy, n2, r2y);
+                    dfix<FD>(gwx, n3, r2x);
+                    dfix<FD>(gwy, n4, r2y);
+                }
+                const double jh = jb * h;
+                BR[0 * BOX + k] = jh * (a11 * gux + a21 * guy);
+                BR[1 * BOX + k] = jh * (a12 * gwx + a22 * gwy);
+                BR[2 * BOX + k] = jh * ((a12 * gux + a22 * guy) + (a11 * gwx + a21 * gwy));
+            }
+        }
+    };
+    if (safe2) phase2(std::false_type{});
+    else phase2(std::true_type{});
     // this thread's Phase-3 cell out of the staged boxes (they are recycled below)
     double sc6[6], gjb = 1.0, grjb = 1.0, gnz = 1.0;
     {
@@ -502,7 +525,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
     const Rcp rdx = mkrcp_const<FD>(P.dxi, P.r_dxi);
     const Rcp rdy = mkrcp_const<FD>(P.deta, P.r_deta);
     unsigned long long obits = 0ull;
-    bool osafe = true;
+    bool osafe = true, osafe2 = true;
     if (p3) {
         const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
         const int X = p3x, Y = p3y;
@@ -511,51 +534,57 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
         const double jb = gjb;
         const Rcp rj = mkrcp_const<FD>(jb, grjb);
 
-        // flux divergence (solver.cpp:396-399)
-        double dx[6], dy[6], nx_[6], ny_[6];
-        bool ok = rdx.ok && rdy.ok;
-#pragma unroll
-        for (int f = 0; f < 6; ++f) {
-            const double* fx = FX + f * NFX + ty * (TX + 1) + tx;
-            const double* fy = FY + f * NFY + ty * TX + tx;
-            nx_[f] = -(fx[1] - fx[0]);
-            ny_[f] = -(fy[TX] - fy[0]);
-            dx[f] = dq<FD>(nx_[f], rdx, ok);
-            dy[f] = dq<FD>(ny_[f], rdy, ok);
-        }
-        if (!ok) {
+        // divergence + viscous source as a generic lambda (CHK = false: safe tile, window B)
+        double rhs[6];
+        auto div_visc = [&](auto chk_tag) {
+            constexpr bool CHK = decltype(chk_tag)::value;
+            // flux divergence (solver.cpp:396-399)
+            double dx[6], dy[6], nx_[6], ny_[6];
+            bool ok = !CHK || (rdx.ok && rdy.ok);
 #pragma unroll
             for (int f = 0; f < 6; ++f) {
-                dfix<FD>(dx[f], nx_[f], rdx);
-                dfix<FD>(dy[f], ny_[f], rdy);
+                const double* fx = FX + f * NFX + ty * (TX + 1) + tx;
+                const double* fy = FY + f * NFY + ty * TX + tx;
+                nx_[f] = -(fx[1] - fx[0]);
+                ny_[f] = -(fy[TX] - fy[0]);
+                dx[f] = dq<FD, CHK>(nx_[f], rdx, ok);
+                dy[f] = dq<FD, CHK>(ny_[f], rdy, ok);
             }
-        }
-        double rhs[6];
+            if (!ok) {
 #pragma unroll
-        for (int f = 0; f < 6; ++f) rhs[f] = dx[f] + dy[f];
-
-        if (!P.adv_only) {
-            const double* bvx = BR;
-            const double* bvy = BR + BOX;
-            const double* bxy = BR + 2 * BOX;
-            const double s1 = 2.0 * (bvx[bk + 1] - bvx[bk - 1]), s2 = bxy[bk + W2] - bxy[bk - W2];
-            const double s3 = 2.0 * (bvy[bk + W2] - bvy[bk - W2]), s4 = bxy[bk + 1] - bxy[bk - 1];
-            bool ok3 = r2x.ok && r2y.ok;
-            double v1 = dq<FD>(s1, r2x, ok3), v2 = dq<FD>(s2, r2y, ok3);
-            double v3 = dq<FD>(s3, r2y, ok3), v4 = dq<FD>(s4, r2x, ok3);
-            if (!ok3) {
-                dfix<FD>(v1, s1, r2x);
-                dfix<FD>(v2, s2, r2y);
-                dfix<FD>(v3, s3, r2y);
-                dfix<FD>(v4, s4, r2x);
+                for (int f = 0; f < 6; ++f) {
+                    dfix<FD>(dx[f], nx_[f], rdx);
+                    dfix<FD>(dy[f], ny_[f], rdy);
+                }
             }
-            const double svis_x = visc * (v1 + v2);
-            const double svis_y = visc * (v3 + v4);
-            rhs[2] = rhs[2] + Ps2;
-            rhs[3] = rhs[3] + Ps3;
-            rhs[4] = rhs[4] + (Pf4 + svis_x);
-            rhs[5] = rhs[5] + (Pf5 + svis_y);
-        }
+#pragma unroll
+            for (int f = 0; f < 6; ++f) rhs[f] = dx[f] + dy[f];
+
+            if (!P.adv_only) {
+                const double* bvx = BR;
+                const double* bvy = BR + BOX;
+                const double* bxy = BR + 2 * BOX;
+                const double s1 = 2.0 * (bvx[bk + 1] - bvx[bk - 1]), s2 = bxy[bk + W2] - bxy[bk - W2];
+                const double s3 = 2.0 * (bvy[bk + W2] - bvy[bk - W2]), s4 = bxy[bk + 1] - bxy[bk - 1];
+                bool ok3 = !CHK || (r2x.ok && r2y.ok);
+                double v1 = dq<FD, CHK>(s1, r2x, ok3), v2 = dq<FD, CHK>(s2, r2y, ok3);
+                double v3 = dq<FD, CHK>(s3, r2y, ok3), v4 = dq<FD, CHK>(s4, r2x, ok3);
+                if (!ok3) {
+                    dfix<FD>(v1, s1, r2x);
+                    dfix<FD>(v2, s2, r2y);
+                    dfix<FD>(v3, s3, r2y);
+                    dfix<FD>(v4, s4, r2x);
+                }
+                const double svis_x = visc * (v1 + v2);
+                const double svis_y = visc * (v3 + v4);
+                rhs[2] = rhs[2] + Ps2;
+                rhs[3] = rhs[3] + Ps3;
+                rhs[4] = rhs[4] + (Pf4 + svis_x);
+                rhs[5] = rhs[5] + (Pf5 + svis_y);
+            }
+        };
+        if (safe2) div_visc(std::false_type{});
+        else div_visc(std::true_type{});
 
         // stage update: predictor u = u0 + dt*R (:518), corrector u += dt*R (:531)
         double un[6];
@@ -620,7 +649,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
         }
 
         TPROBE(13);  // phase 3: Heun average
-        obits = cell_epilogue<FD, CORR>(un, rj, nZ, X, Y, P, sc, lam_local, A.out, fs, o3, osafe);
+        obits = cell_epilogue<FD, CORR>(un, rj, nZ, X, Y, P, sc, lam_local, A.out, fs, o3, osafe, osafe2);
         TPROBE(14);  // phase 3: regularize, finite, lambda, stores
     }
 
@@ -657,7 +686,8 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
     // barrier (FX/FY/V/PJ/BR/cell box are rewritten by the next tile) publishes them
     {
         const unsigned fb = ((p3 && obits != 0ull) ? cell_flag_bits(threadIdx.x % TX, threadIdx.x / TX) : 0u) |
-                            (osafe ? 0u : static_cast<unsigned>(TF_UNSAFE));
+                            (osafe ? 0u : static_cast<unsigned>(TF_UNSAFE)) |
+                            (osafe2 ? 0u : static_cast<unsigned>(TF_UNSAFE2));
         const unsigned wf = __reduce_or_sync(0xffffffffu, fb);
         if ((threadIdx.x & 31) == 0 && wf) atomicOr(&s_flags, wf);
     }
@@ -682,7 +712,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
 __device__ __forceinline__ void tiles_body(const TileArgs& a, int block) {
     const int ntiles = a.ntx * a.nty;
     const int t = block * blockDim.x + threadIdx.x;
-    bool active = false, safe = false;
+    bool active = false, safe = false, safe2 = false;
     if (t < ntiles) {
         const int tx = t % a.ntx, ty = t / a.ntx;
         const bool ring = tx == 0 || tx == a.ntx - 1 || ty == 0 || ty == a.nty - 1;
@@ -723,6 +753,7 @@ __device__ __forceinline__ void tiles_body(const TileArgs& a, int block) {
             if (xl && yr) u |= F[t + a.ntx - 1];
             if (xr && yr) u |= F[t + a.ntx + 1];
             safe = (u & TF_UNSAFE) == 0u;
+            safe2 = a.safe2_ok && (u & TF_UNSAFE2) == 0u;
         }
         if (skip && ring) {
 #pragma unroll
@@ -743,7 +774,8 @@ __device__ __forceinline__ void tiles_body(const TileArgs& a, int block) {
     if (lane == 0 && ms) atomicAdd(a.ntiles_active + 4, __popc(ms));
     base = __shfl_sync(0xffffffffu, base, 0);
     if (active)
-        a.tiles[base + __popc(m & ((1u << lane) - 1u))] = ((t / a.ntx) << 16) | (t % a.ntx) | (safe ? kTileSafe : 0);
+        a.tiles[base + __popc(m & ((1u << lane) - 1u))] = ((t / a.ntx) << 16) | (t % a.ntx) | (safe ? kTileSafe : 0) |
+                                                          (safe2 ? kTileSafe2 : 0);
 }
 
 __global__ void __launch_bounds__(NT) tiles_kernel(TileArgs a) {

@@ -202,7 +202,9 @@ def test_safe_window_edges(gpu, oracle_kind):
     s[0, 10, 10] = 2.0 ** -201          # just below the window (thickness)
     s[3, 30, 40] = 5e-310               # subnormal momentum
     s[4, 50, 20] = -(2.0 ** -200)       # the window's lower edge: still safe
-    s[2, 60, 70] = 2.0 ** -180          # tiny but inside
+    s[2, 60, 70] = 2.0 ** -180          # inside window A, outside window B
+    s[1, 40, 60] = 2.0 ** -101          # just outside window B
+    s[3, 20, 80] = -(2.0 ** 99)         # inside window B
     s[5, 70, 90] = 2.0 ** 200           # the window's upper edge: unsafe
     ref.set_state(s)
     sim.set_state(s)
