@@ -36,6 +36,7 @@ cudaError_t launch_regularize(const GridDesc& g, const Phys& P, double* s, const
                               DevScalars* sc, bool fastdiv, cudaStream_t st);
 cudaError_t init_kernels();
 cudaError_t launch_tiles(const TileArgs& a, cudaStream_t st);
+cudaError_t launch_pack_state(const GridDesc& g, const double* src, double* dst, bool unpack, cudaStream_t st);
 cudaError_t launch_pre(const PreArgs& a, cudaStream_t st);
 int bc_blocks(const GridDesc& g);
 cudaError_t selftest_division(long long n, unsigned long long seed, unsigned long long* mismatches);
@@ -135,6 +136,7 @@ struct tp_ctx {
     unsigned short* dFlagA = nullptr;  // per-tile TileFlag bits of A / B (all set = unknown)
     unsigned short* dFlagB = nullptr;
     int* dTiles = nullptr;            // active-tile list of the stage in flight + its count
+    double* dDense = nullptr;         // dense [6][ny][nx] staging for host transfers (lazy)
     int* dNact = nullptr;             // [6] list counts pred, corr; last-launch stats pred, corr;
                                       // safe-tile counts pred, corr
     int last_tiles_stage = 1;         // stage of the last tiles_kernel enqueued (0 pred, 1 corr)
@@ -442,15 +444,23 @@ void check_error(tp_ctx* c, const double* pred_buf) {
     if (key != tpb::kNoError) raise_error_key(c, key, pred_buf);
 }
 
-// host dense (nx*ny per field) <-> device pitched
+// host dense (nx*ny per field) <-> device pitched: one contiguous DMA copy through a
+// dense device staging buffer, re-pitched by a kernel (a 2-D copy with 6*ny short rows
+// runs at a fraction of the link bandwidth)
+double* dense_staging(tp_ctx* c) {
+    if (!c->dDense) ck(cudaMalloc(&c->dDense, sizeof(double) * 6ull * c->ny * c->nx), "cudaMalloc staging");
+    return c->dDense;
+}
 void upload_state(tp_ctx* c, double* dst, const double* src) {
-    ck(cudaMemcpy2DAsync(dst, c->pitch * sizeof(double), src, c->nx * sizeof(double),
-                         c->nx * sizeof(double), 6ull * c->ny, cudaMemcpyHostToDevice, c->stream),
+    double* d = dense_staging(c);
+    ck(cudaMemcpyAsync(d, src, sizeof(double) * 6ull * c->ny * c->nx, cudaMemcpyHostToDevice, c->stream),
        "state H2D");
+    ck(tpb::launch_pack_state(c->g, d, dst, true, c->stream), "unpack state");
 }
 void download_state(tp_ctx* c, double* dst, const double* src) {
-    ck(cudaMemcpy2DAsync(dst, c->nx * sizeof(double), src, c->pitch * sizeof(double),
-                         c->nx * sizeof(double), 6ull * c->ny, cudaMemcpyDeviceToHost, c->stream),
+    double* d = dense_staging(c);
+    ck(tpb::launch_pack_state(c->g, src, d, false, c->stream), "pack state");
+    ck(cudaMemcpyAsync(dst, d, sizeof(double) * 6ull * c->ny * c->nx, cudaMemcpyDeviceToHost, c->stream),
        "state D2H");
     ck(cudaStreamSynchronize(c->stream), "sync");
 }
@@ -687,6 +697,7 @@ void tp_destroy(tp_ctx* c) {
     cudaFree(c->dDts);
     cudaFree(c->dFlagA);
     cudaFree(c->dFlagB);
+    cudaFree(c->dDense);
     cudaFree(c->dTiles);
     cudaFree(c->dNact);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
