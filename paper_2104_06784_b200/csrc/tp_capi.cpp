@@ -37,6 +37,8 @@ cudaError_t launch_regularize(const GridDesc& g, const Phys& P, double* s, const
 cudaError_t init_kernels();
 cudaError_t launch_tiles(const TileArgs& a, cudaStream_t st);
 cudaError_t launch_pack_state(const GridDesc& g, const double* src, double* dst, bool unpack, cudaStream_t st);
+cudaError_t launch_snapshot(const GridDesc& g, const double* s, const double* geo, double* out, int ncols,
+                            int nrows, double H, double h_dry, double eps_h, double vu, cudaStream_t st);
 cudaError_t launch_pre(const PreArgs& a, cudaStream_t st);
 int bc_blocks(const GridDesc& g);
 cudaError_t selftest_division(long long n, unsigned long long seed, unsigned long long* mismatches);
@@ -1051,36 +1053,15 @@ int tp_interior_mass(tp_ctx* c, double* ms, double* mf) {
 
 int tp_snapshot(tp_ctx* c, double* out) {
     TP_GUARD(c, {
-        // Simulator::snapshot (solver.cpp:590-617)
-        std::vector<double> s = host_state(c);
-        const size_t n = static_cast<size_t>(c->nx) * c->ny;
+        // Simulator::snapshot (solver.cpp:590-617) on the device (snapshot_kernel), then one
+        // contiguous copy of the 6 interior fields
+        double* d = dense_staging(c);  // 6*ny*nx >= 6*nrows*ncols
         const size_t m = static_cast<size_t>(c->ncols) * c->nrows;
-        const double* jbf = c->geo_h.data() + 3 * n;
-        const double vu = std::sqrt(c->p.g * c->p.L);
-        const double eps_h = c->p.eps_h;
-        std::fill(out, out + 6 * m, 0.0);
-        auto desing = [&](double q, double jb, double hp) {
-            double hm = std::max(hp, eps_h);
-            double denom = hp * hp + hm * hm;
-            return (q / jb) * (2.0 * hp / denom);
-        };
-        for (int j = 0; j < c->nrows; ++j) {
-            for (int i = 0; i < c->ncols; ++i) {
-                const size_t k = static_cast<size_t>(j + kGhost) * c->nx + (i + kGhost);
-                const size_t o = static_cast<size_t>(j) * c->ncols + i;
-                double jb = jbf[k];
-                double hs = s[0 * n + k] / jb;
-                double hf = s[1 * n + k] / jb;
-                double h = hs + hf;
-                out[0 * m + o] = h * c->p.H;
-                if (h < c->p.h_dry) continue;
-                out[1 * m + o] = hs / h;
-                out[2 * m + o] = desing(s[2 * n + k], jb, hs) * vu;
-                out[3 * m + o] = desing(s[3 * n + k], jb, hs) * vu;
-                out[4 * m + o] = desing(s[4 * n + k], jb, hf) * vu;
-                out[5 * m + o] = desing(s[5 * n + k], jb, hf) * vu;
-            }
-        }
+        ck(tpb::launch_snapshot(c->g, c->dA, c->dGeo, d, c->ncols, c->nrows, c->p.H, c->p.h_dry, c->p.eps_h,
+                                std::sqrt(c->p.g * c->p.L), c->stream),
+           "snapshot_kernel");
+        ck(cudaMemcpyAsync(out, d, sizeof(double) * 6 * m, cudaMemcpyDeviceToHost, c->stream), "snapshot D2H");
+        ck(cudaStreamSynchronize(c->stream), "sync");
     })
 }
 

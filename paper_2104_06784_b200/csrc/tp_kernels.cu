@@ -1151,6 +1151,44 @@ __global__ void unpack_state_kernel(GridDesc g, const double* __restrict__ src, 
         dst[f * g.fs + j * g.pitch + i] = src[k];
     }
 }
+// Simulator::snapshot (solver.cpp:590-617): h_total, phi_s and the four desingularised
+// velocities of the interior cells in physical units, +0.0 on dry cells, IEEE division and
+// the reference's expression trees (physics.hpp:33-37).  out: dense [6][nrows][ncols].
+__global__ void snapshot_kernel(GridDesc g, const double* __restrict__ s, const double* __restrict__ geo,
+                                double* __restrict__ out, int ncols, int nrows, double H, double h_dry,
+                                double eps_h, double vu) {
+    const long long m = static_cast<long long>(ncols) * nrows;
+    for (long long o = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; o < m;
+         o += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const int j = static_cast<int>(o / ncols), i = static_cast<int>(o - static_cast<long long>(j) * ncols);
+        const long long k = static_cast<long long>(j + 3) * g.pitch + (i + 3);
+        const double jb = geo[G_JB * g.fs + k];
+        const double hs = s[0 * g.fs + k] / jb;
+        const double hf = s[1 * g.fs + k] / jb;
+        const double h = hs + hf;
+        double v[6] = {h * H, 0.0, 0.0, 0.0, 0.0, 0.0};
+        if (!(h < h_dry)) {
+            auto desing = [&](double q, double hp) {
+                const double hm = smax(hp, eps_h);
+                const double denom = hp * hp + hm * hm;
+                return (q / jb) * (2.0 * hp / denom);
+            };
+            v[1] = hs / h;
+            v[2] = desing(s[2 * g.fs + k], hs) * vu;
+            v[3] = desing(s[3 * g.fs + k], hs) * vu;
+            v[4] = desing(s[4 * g.fs + k], hf) * vu;
+            v[5] = desing(s[5 * g.fs + k], hf) * vu;
+        }
+#pragma unroll
+        for (int f = 0; f < 6; ++f) out[f * m + o] = v[f];
+    }
+}
+cudaError_t launch_snapshot(const GridDesc& g, const double* s, const double* geo, double* out, int ncols,
+                            int nrows, double H, double h_dry, double eps_h, double vu, cudaStream_t st) {
+    snapshot_kernel<<<4 * g_num_sms, 256, 0, st>>>(g, s, geo, out, ncols, nrows, H, h_dry, eps_h, vu);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_pack_state(const GridDesc& g, const double* src, double* dst, bool unpack, cudaStream_t st) {
     if (unpack) unpack_state_kernel<<<4 * g_num_sms, 256, 0, st>>>(g, src, dst);
     else pack_state_kernel<<<4 * g_num_sms, 256, 0, st>>>(g, src, dst);
@@ -1178,7 +1216,8 @@ cudaError_t init_kernels() {
         reinterpret_cast<const void*>(&tiles_kernel), reinterpret_cast<const void*>(&pre_kernel),
         reinterpret_cast<const void*>(&regularize_kernel<true>),
         reinterpret_cast<const void*>(&regularize_kernel<false>),
-        reinterpret_cast<const void*>(&pack_state_kernel), reinterpret_cast<const void*>(&unpack_state_kernel)};
+        reinterpret_cast<const void*>(&pack_state_kernel), reinterpret_cast<const void*>(&unpack_state_kernel),
+        reinterpret_cast<const void*>(&snapshot_kernel)};
     for (const void* f : fns)
         if ((e = cudaFuncGetAttributes(&fa, f)) != cudaSuccess) return e;
     return cudaSuccess;

@@ -146,6 +146,20 @@ def test_run_report_matches(gpu, oracle_kind):
     assert_bitwise(sim.state(), ref.state(), "state after run")
 
 
+@pytest.mark.parametrize("make", [lambda: scenarios.c1_hill(64), lambda: scenarios.wet_valley(80, 72)])
+def test_snapshot_bitwise(gpu, oracle_kind, make):
+    """Simulator::snapshot (solver.cpp:590-617) computed on the device, field by field."""
+    sc = make()
+    ref, sim = _pair(sc, oracle_kind)
+    tr, _, _ = ref.steps(0.0, 1.0e9, 25, t_end=1.0e9)
+    tg, _, _ = sim.steps(0.0, 1.0e9, 25, t_end=1.0e9)
+    assert tr == tg
+    snap_r = ref.snapshot(tr)
+    snap_g = sim.snapshot(tg)
+    got = np.stack([snap_g.h_total, snap_g.phi_s, snap_g.vX_s, snap_g.vY_s, snap_g.vX_f, snap_g.vY_f])
+    assert_bitwise(got, snap_r.reshape(got.shape), "snapshot fields")
+
+
 def test_negative_thickness_error_matches(gpu, oracle_kind):
     """regularize's NumericsError text (solver.cpp:147-152)."""
     sc = scenarios.c1_hill(32)
