@@ -136,38 +136,21 @@ def cpu_reference(config, ncols, nrows, steps, lanes, timeout=600):
     raise RuntimeError("CPU reference failed: " + err)
 
 
-def time_stages(sim, n=4):
-    """Per-stage kernel time: CUDA events recorded on the launching stream right around
-    each stage kernel (tp_stage_timed), median over n device-loop-equivalent steps."""
+def time_stages(sim, n=20):
+    """Per-stage kernel time in the production context: n steps of the device loop replayed
+    from a one-step CUDA graph with events recorded on the launching stream right around
+    the predictor and corrector kernels (tp_steps_timed).  Returns mean ms per launch and
+    the tiles the last step processed."""
     import ctypes as C
-    L = sim.L
-    h = sim.h
-    lam = C.c_double(0.0)
-    tp, tc, ap, ac = [], [], [], []
-    t = C.c_double(0.0)
-    hit = C.c_int()
-    dtv = C.c_double()
-    ms = C.c_float()
-    tcur = sim._bench_t
-    import torch
-    lam_dev = torch.zeros(1, dtype=torch.float64, device="cuda")
-    for _ in range(n):
-        sim._check(L.tp_step_begin(h, tcur, 1e9, 1e9))
-        sim._check(L.tp_bc(h, 0))
-        sim._check(L.tp_lambda_local(h, C.c_void_p(lam_dev.data_ptr())))
-        sim._check(L.tp_dt_from(h, C.c_void_p(lam_dev.data_ptr())))
-        sim._check(L.tp_stage_timed(h, 0, C.byref(ms)))
-        tp.append(ms.value)
-        sim._check(L.tp_bc(h, 1))
-        sim._check(L.tp_stage_timed(h, 1, C.byref(ms)))
-        tc.append(ms.value)
-        p_, c_, _ = sim.active_tiles()
-        ap.append(p_)
-        ac.append(c_)
-        sim._check(L.tp_step_end(h, C.byref(t), C.byref(hit), C.byref(dtv)))
-        tcur = t.value
-    sim._bench_t = tcur
-    return statistics.median(tp), statistics.median(tc), statistics.median(ap), statistics.median(ac)
+    t = C.c_double(sim._bench_t)
+    steps, hit = C.c_long(), C.c_int()
+    pm, cm = C.c_float(), C.c_float()
+    sim._check(sim.L.tp_steps_timed(sim.h, 1e9, 1e9, n, C.byref(t), C.byref(steps), C.byref(hit),
+                                    C.byref(pm), C.byref(cm)))
+    sim._bench_t = t.value
+    k = max(steps.value, 1)
+    p_, c_, _ = sim.active_tiles()
+    return pm.value / k, cm.value / k, p_, c_
 
 
 def ncu_traffic():
@@ -334,7 +317,7 @@ def main():
     ap.add_argument("--ncols", type=int, default=2048)
     ap.add_argument("--nrows", type=int, default=2048)
     ap.add_argument("--graph-steps", type=int, default=16)
-    ap.add_argument("--roofline-reps", type=int, default=5)
+    ap.add_argument("--roofline-reps", type=int, default=20)
     ap.add_argument("--cpu-steps", type=int, default=6)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()

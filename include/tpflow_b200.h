@@ -96,6 +96,11 @@ int tp_set_advection_only(tp_ctx* c, int on);
  * receives every accepted dt.  The host synchronises once per CUDA graph. */
 int tp_steps(tp_ctx* c, double t_next, double t_end, long max_steps, double* t, long* steps,
              int* hit, double* dts);
+/* tp_steps replaying a one-step graph that records CUDA events (external event nodes on the
+ * context stream) right around the predictor and corrector kernels; *pred_ms / *corr_ms =
+ * the summed device time of those kernels over the steps taken (measurement hook) */
+int tp_steps_timed(tp_ctx* c, double t_next, double t_end, long max_steps, double* t, long* steps, int* hit,
+                   float* pred_ms, float* corr_ms);
 
 /* audit[0..4] = solid {initial, final, injected, outflow, clipped}, [5..9] fluid
  * (MassAudit, config.hpp:60-75); initial/final are host-owned (see tp_set_audit). */

@@ -66,6 +66,8 @@ SIGNATURES = {
     "tp_dt_from": (C.c_int, [_vp, _vp]),
     "tp_stage": (C.c_int, [_vp, C.c_int]),
     "tp_stage_timed": (C.c_int, [_vp, C.c_int, C.POINTER(C.c_float)]),
+    "tp_steps_timed": (C.c_int, [_vp, C.c_double, C.c_double, C.c_long, _dp, _lp, _ip, C.POINTER(C.c_float),
+                                 C.POINTER(C.c_float)]),
     "tp_step_end": (C.c_int, [_vp, _dp, _ip, _dp]),
     "tp_set_stream": (C.c_int, [_vp, _vp]),
     "tp_synchronize": (C.c_int, [_vp]),

@@ -149,6 +149,8 @@ struct tp_ctx {
     bool hydro_set = false;
     int adv_only = 0;
     cudaGraphExec_t graphK = nullptr, graph1 = nullptr;
+    cudaGraphExec_t graphT = nullptr;   // one step with timing events around the stage kernels
+    cudaEvent_t evT[4] = {nullptr, nullptr, nullptr, nullptr};
     int graphK_steps = 0;
     long launches = 0;
     double t_next_last = 0.0;
@@ -225,7 +227,8 @@ void build_phys(tp_ctx* c) {
 void drop_graphs(tp_ctx* c) {
     if (c->graphK) cudaGraphExecDestroy(c->graphK);
     if (c->graph1) cudaGraphExecDestroy(c->graph1);
-    c->graphK = c->graph1 = nullptr;
+    if (c->graphT) cudaGraphExecDestroy(c->graphT);
+    c->graphK = c->graph1 = c->graphT = nullptr;
 }
 
 tpb::StageArgs stage_args(tp_ctx* c, bool corr, int loop) {
@@ -331,7 +334,7 @@ void launch_post(tp_ctx* c, int loop) {
 // one whole step of the device loop: 5 kernels
 //   pre(bc(u,t) + predictor list + compute_dt) -> predictor -> pre(bc(u*,t+dt) + corrector list)
 //   -> corrector -> post(t += dt, audit, stop flag)
-void enqueue_loop_step(tp_ctx* c) {
+void enqueue_loop_step(tp_ctx* c, cudaEvent_t* ev = nullptr) {
     for (int corr = 0; corr < 2; ++corr) {
         const tpb::StageArgs sa = stage_args(c, corr != 0, 1);
         tpb::PreArgs p{};
@@ -349,18 +352,20 @@ void enqueue_loop_step(tp_ctx* c) {
         p.with_dt = corr ? 0 : 1;
         ck(tpb::launch_pre(p, c->stream), corr ? "pre (corrector)" : "pre (predictor)");
         c->last_tiles_stage = corr;
+        if (ev) ck(cudaEventRecordWithFlags(ev[2 * corr], c->stream, cudaEventRecordExternal), "event");
         ck(tpb::launch_stage(sa, c->fastdiv, corr != 0, c->stream), corr ? "corrector" : "predictor");
+        if (ev) ck(cudaEventRecordWithFlags(ev[2 * corr + 1], c->stream, cudaEventRecordExternal), "event");
     }
     launch_post(c, 1);
 }
 
-cudaGraphExec_t capture_steps(tp_ctx* c, int k) {
+cudaGraphExec_t capture_steps(tp_ctx* c, int k, cudaEvent_t* ev = nullptr) {
     cudaGraph_t graph = nullptr;
     const int saved_stage = c->last_tiles_stage;
     c->last_tiles_stage = 1;  // a replay always follows a corrector (tp_steps resets otherwise)
     ck(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal), "begin capture");
     try {
-        for (int s = 0; s < k; ++s) enqueue_loop_step(c);
+        for (int s = 0; s < k; ++s) enqueue_loop_step(c, ev);
     } catch (...) {
         cudaStreamEndCapture(c->stream, &graph);
         if (graph) cudaGraphDestroy(graph);
@@ -700,6 +705,8 @@ void tp_destroy(tp_ctx* c) {
     cudaFree(c->dFlagA);
     cudaFree(c->dFlagB);
     cudaFree(c->dDense);
+    for (auto& e : c->evT)
+        if (e) cudaEventDestroy(e);
     cudaFree(c->dTiles);
     cudaFree(c->dNact);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
@@ -1005,6 +1012,54 @@ int tp_steps(tp_ctx* c, double t_next, double t_end, long max_steps, double* t, 
         c->ghosts_in_B = c->ghosts_in_B || h.steps > 0;
         if (dts && h.steps > 0)
             ck(cudaMemcpy(dts, c->dDts, sizeof(double) * h.steps, cudaMemcpyDeviceToHost), "dts D2H");
+        if (h.err_key != tpb::kNoError) {
+            c->lam_valid = false;
+            raise_error_key(c, h.err_key, c->dB);
+        }
+    })
+}
+
+int tp_steps_timed(tp_ctx* c, double t_next, double t_end, long max_steps, double* t, long* steps, int* hit,
+                   float* pred_ms, float* corr_ms) {
+    TP_GUARD(c, {
+        // tp_steps one step per graph replay, with CUDA events recorded (as external event
+        // nodes of the graph, on the launching stream) right around the two stage kernels:
+        // the kernels' device time in their production context
+        *steps = 0;
+        *hit = 0;
+        *pred_ms = *corr_ms = 0.0f;
+        c->launches = 0;
+        if (max_steps <= 0 || !(*t < t_end)) return TP_OK;
+        ck(cudaMemsetAsync(&c->dSc->dts, 0, sizeof(double*), c->stream), "dts null");
+        write_ctrl(c, *t, t_next, t_end, 0.0, max_steps);
+        if (!c->lam_valid) fresh_lambda(c);
+        if (!c->evT[0])
+            for (auto& e : c->evT) ck(cudaEventCreate(&e), "event");
+        if (!c->graphT) c->graphT = capture_steps(c, 1, c->evT);
+        if (c->last_tiles_stage == 0) {
+            ck(cudaMemsetAsync(c->dNact, 0, sizeof(int), c->stream), "memset");
+            ck(cudaMemsetAsync(c->dNact + 4, 0, sizeof(int), c->stream), "memset");
+        }
+        c->last_tiles_stage = 1;
+        DevScalars h{};
+        for (;;) {
+            ck(cudaGraphLaunch(c->graphT, c->stream), "graph launch");
+            c->launches += 5;
+            h = read_scalars(c);
+            if (h.steps > *steps) {
+                float a = 0.0f, b = 0.0f;
+                ck(cudaEventElapsedTime(&a, c->evT[0], c->evT[1]), "elapsed");
+                ck(cudaEventElapsedTime(&b, c->evT[2], c->evT[3]), "elapsed");
+                *pred_ms += a;
+                *corr_ms += b;
+                *steps = static_cast<long>(h.steps);
+            }
+            if (h.done) break;
+        }
+        *t = h.t;
+        *hit = h.steps > 0 ? h.hit : 0;
+        c->lam_valid = h.steps > 0 || c->lam_valid;
+        c->ghosts_in_B = c->ghosts_in_B || h.steps > 0;
         if (h.err_key != tpb::kNoError) {
             c->lam_valid = false;
             raise_error_key(c, h.err_key, c->dB);
