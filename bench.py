@@ -136,6 +136,28 @@ def cpu_reference(config, ncols, nrows, steps, lanes, timeout=600):
     raise RuntimeError("CPU reference failed: " + err)
 
 
+class RunClock:
+    """The run loop's output schedule (solver.cpp:627-649): steps are taken toward
+    t_next = min(next_out, t_end) and stop on exact output hits, as Simulator::run does."""
+
+    def __init__(self, sim):
+        tu = sim.cfg.scaling.t_unit()
+        self.sim, self.t = sim, 0.0
+        self.t_end = sim.cfg.t_end / tu
+        self.dt_out = sim.cfg.dt_out / tu
+        self.next_out = self.dt_out
+
+    def advance(self, k):
+        done = 0
+        while done < k and self.t < self.t_end:
+            t_next = min(self.next_out, self.t_end)
+            self.t, n, hit = self.sim.steps(self.t, t_next, k - done, t_end=self.t_end)
+            done += n
+            if hit and t_next == self.next_out:
+                self.next_out += self.dt_out
+        return done
+
+
 def time_stages(sim, n=20):
     """Per-stage kernel time in the production context: n steps of the device loop replayed
     from a one-step CUDA graph with events recorded on the launching stream right around
@@ -145,8 +167,9 @@ def time_stages(sim, n=20):
     t = C.c_double(sim._bench_t)
     steps, hit = C.c_long(), C.c_int()
     pm, cm = C.c_float(), C.c_float()
-    sim._check(sim.L.tp_steps_timed(sim.h, 1e9, 1e9, n, C.byref(t), C.byref(steps), C.byref(hit),
-                                    C.byref(pm), C.byref(cm)))
+    tu = sim.cfg.scaling.t_unit()
+    sim._check(sim.L.tp_steps_timed(sim.h, sim._bench_t_next, sim.cfg.t_end / tu, n, C.byref(t), C.byref(steps),
+                                    C.byref(hit), C.byref(pm), C.byref(cm)))
     sim._bench_t = t.value
     k = max(steps.value, 1)
     p_, c_, _ = sim.active_tiles()
@@ -182,14 +205,15 @@ def run_b200(args):
     sim.set_stream(stream.cuda_stream)
     setup_s = time.perf_counter() - t_setup
 
-    t, n, _ = sim.steps(0.0, 1e9, args.warmup, t_end=1e9)
+    clock = RunClock(sim)
+    clock.advance(args.warmup)
     torch.cuda.synchronize()
     clocks = ClockSampler(0)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with clocks:
         torch.cuda.synchronize()
         e0.record(stream)
-        t, n, _ = sim.steps(t, 1e9, args.steps, t_end=1e9)
+        n = clock.advance(args.steps)
         e1.record(stream)
         torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
@@ -199,7 +223,8 @@ def run_b200(args):
     value = cells * args.steps / (ms / 1e3) / 1e9
 
     # roofline leg: the two stage kernels (the dominant kernel of the step)
-    sim._bench_t = t
+    sim._bench_t = clock.t
+    sim._bench_t_next = min(clock.next_out, clock.t_end)
     t_pred, t_corr, tp_p, tp_c = time_stages(sim, n=args.roofline_reps)
     peak, peak_src = load_peaks()
     achieved = ALG_BYTES_PER_CELL_UPDATE * cells / ((t_pred + t_corr) / 1e3) / 1e9
@@ -234,7 +259,10 @@ def run_b200(args):
     torch.cuda.synchronize()
     w0 = time.perf_counter()
     sim._check(sim.L.tp_set_state(sim.h, C.cast(h_in.data_ptr(), C.POINTER(C.c_double))))
-    te, ne, _ = sim.steps(t, 1e9, args.steps, t_end=1e9)
+    clock.t = sim._bench_t
+    while clock.next_out <= clock.t:  # an output hit inside the roofline leg
+        clock.next_out += clock.dt_out
+    ne = clock.advance(args.steps)
     sim._check(sim.L.tp_get_state(sim.h, C.cast(h_out.data_ptr(), C.POINTER(C.c_double))))
     w1 = time.perf_counter()
     e2e = {"value": round(cells * ne / (w1 - w0) / 1e9, 4), "unit": "GCUPS",
@@ -258,9 +286,11 @@ def run_b200(args):
         "metric": METRIC, "value": round(value, 4), "unit": "GCUPS", "n_gpus": 1,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 5),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (deterministic valley DEM + compact paraboloid release, scenarios.py)",
-        "config": {"workload": f"{sc.name} Mode-I release, {sc.ncols}x{sc.nrows} interior cells, "
-                               "cellsize 5 m, Table-1 parameters, CFL 0.1",
+        "data": f"synthetic (deterministic {sc.name} generator in scenarios.py: DEM + "
+                f"{'inflow hydrograph' if sc.config.inflow else 'compact release'}; no network data)",
+        "config": {"workload": f"{sc.name} {'Mode-II inflow' if sc.config.inflow else 'Mode-I release'}, "
+                               f"{sc.ncols}x{sc.nrows} interior cells, cellsize {sc.cellsize:g} m, Table-1 "
+                               f"parameters, CFL {sc.config.cfl:g}, output every {sc.config.dt_out:g} s",
                    "grid": [sc.ncols, sc.nrows], "wet_fraction_t0": round(float((sc.h0 > 0).mean()), 4)
                    if sc.h0 is not None else None,
                    "l2": "inputs larger than L2 (state 2x%.0f MB + geometry %.0f MB > 126 MB)"
