@@ -151,6 +151,20 @@ int tp_safe_tiles(tp_ctx* c, int* corr);
 /* development probe: per-phase warp cycles of the stage kernels [2][19] (pred, corr;
  * slot 16 counts warps, 17/18 sum warp lifetimes in cycles / ns); all zero unless the library was built with `make timing` */
 int tp_debug_phase_cycles(unsigned long long* out, int reset);
+/* ---- device-resident row-slab exchange over peer memory (tp_peer.cu) ----------------
+ * Slabs (tp_create_slab) connected here run tp_steps with the halo rows stored straight
+ * into the neighbours' buffers and the lambda all-reduce done in device memory: no host
+ * round trip per step (replaces the host-driven tp_halo_pack / tp_lambda_local path).
+ * One rank per GPU: every rank calls tp_peer_export, the blobs are all-gathered (any
+ * transport), every rank calls tp_peer_connect with all nranks blobs in rank order, and
+ * every rank then calls tp_steps with identical arguments.  Contexts of one process:
+ * tp_peer_connect_local, then tp_steps_group. */
+#define TP_PEER_BLOB_BYTES 256
+int tp_peer_export(tp_ctx* c, void* blob /* TP_PEER_BLOB_BYTES */);
+int tp_peer_connect(tp_ctx* c, int rank, int nranks, const void* blobs /* nranks * TP_PEER_BLOB_BYTES */);
+int tp_peer_connect_local(tp_ctx* c, int rank, int nranks, tp_ctx* const* all);
+int tp_steps_group(tp_ctx* const* cs, int n, double t_next, double t_end, long max_steps, double* t,
+                   long* steps, int* hit);
 /* number of kernels launched by the last tp_steps call (graph replays included) */
 long tp_kernel_launches(const tp_ctx* c);
 

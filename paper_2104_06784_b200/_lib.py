@@ -76,6 +76,10 @@ SIGNATURES = {
     "tp_selftest_division": (C.c_int, [C.c_int, C.c_long, C.c_ulonglong, C.POINTER(C.c_ulonglong)]),
     "tp_selftest_minmod": (C.c_int, [C.c_int, C.c_long, _dp, _dp, _dp]),
     "tp_active_tiles": (C.c_int, [_vp, _ip, _ip, _ip]),
+    "tp_peer_export": (C.c_int, [_vp, _vp]),
+    "tp_peer_connect": (C.c_int, [_vp, C.c_int, C.c_int, _vp]),
+    "tp_peer_connect_local": (C.c_int, [_vp, C.c_int, C.c_int, C.POINTER(_vp)]),
+    "tp_steps_group": (C.c_int, [C.POINTER(_vp), C.c_int, C.c_double, C.c_double, C.c_long, _dp, _lp, _ip]),
     "tp_safe_tiles": (C.c_int, [_vp, _ip]),
     "tp_debug_phase_cycles": (C.c_int, [C.POINTER(C.c_ulonglong), C.c_int]),
 }

@@ -36,6 +36,9 @@ cudaError_t launch_regularize(const GridDesc& g, const Phys& P, double* s, const
                               DevScalars* sc, bool fastdiv, cudaStream_t st);
 cudaError_t init_kernels();
 cudaError_t launch_tiles(const TileArgs& a, cudaStream_t st);
+cudaError_t launch_peer_lambda(const PeerLink& L, DevScalars* sc, cudaStream_t st);
+cudaError_t launch_peer_halo(const PeerLink& L, const GridDesc& g, const double* s, int buf, DevScalars* sc,
+                             cudaStream_t st);
 cudaError_t launch_pack_state(const GridDesc& g, const double* src, double* dst, bool unpack, cudaStream_t st);
 cudaError_t launch_snapshot(const GridDesc& g, const double* s, const double* geo, double* out, int ncols,
                             int nrows, double H, double h_dry, double eps_h, double vu, cudaStream_t st);
@@ -139,6 +142,12 @@ struct tp_ctx {
     unsigned short* dFlagB = nullptr;
     int* dTiles = nullptr;            // active-tile list of the stage in flight + its count
     double* dDense = nullptr;         // dense [6][ny][nx] staging for host transfers (lazy)
+    // device-resident slab exchange (tp_peer.cu)
+    tpb::PeerBox* dBox = nullptr;     // this slab's mailbox (exported to the other ranks)
+    tpb::PeerLink link{};
+    bool peered = false;
+    unsigned long long peer_base = 0; // host copy of DevScalars::peer_base
+    std::vector<void*> ipc_opened;    // CUDA-IPC mappings to close at destroy
     int* dNact = nullptr;             // [6] list counts pred, corr; last-launch stats pred, corr;
                                       // safe-tile counts pred, corr
     int last_tiles_stage = 1;         // stage of the last tiles_kernel enqueued (0 pred, 1 corr)
@@ -335,6 +344,8 @@ void launch_post(tp_ctx* c, int loop) {
 //   pre(bc(u,t) + predictor list + compute_dt) -> predictor -> pre(bc(u*,t+dt) + corrector list)
 //   -> corrector -> post(t += dt, audit, stop flag)
 void enqueue_loop_step(tp_ctx* c, cudaEvent_t* ev = nullptr) {
+    // slabs connected by tp_peer_connect*: the lambda + stop all-reduce before compute_dt
+    if (c->peered) ck(tpb::launch_peer_lambda(c->link, c->dSc, c->stream), "peer lambda");
     for (int corr = 0; corr < 2; ++corr) {
         const tpb::StageArgs sa = stage_args(c, corr != 0, 1);
         tpb::PreArgs p{};
@@ -352,6 +363,10 @@ void enqueue_loop_step(tp_ctx* c, cudaEvent_t* ev = nullptr) {
         p.with_dt = corr ? 0 : 1;
         ck(tpb::launch_pre(p, c->stream), corr ? "pre (corrector)" : "pre (predictor)");
         c->last_tiles_stage = corr;
+        // halo rows after apply_boundaries (solver.cpp:639, :523), straight into the
+        // neighbours' buffers, then wait for theirs
+        if (c->peered)
+            ck(tpb::launch_peer_halo(c->link, c->g, corr ? c->dB : c->dA, corr, c->dSc, c->stream), "peer halo");
         if (ev) ck(cudaEventRecordWithFlags(ev[2 * corr], c->stream, cudaEventRecordExternal), "event");
         ck(tpb::launch_stage(sa, c->fastdiv, corr != 0, c->stream), corr ? "corrector" : "predictor");
         if (ev) ck(cudaEventRecordWithFlags(ev[2 * corr + 1], c->stream, cudaEventRecordExternal), "event");
@@ -435,6 +450,8 @@ void raise_error_key(tp_ctx* c, unsigned long long key, const double* pred_buf) 
                      tpb::host::to_string_f(hp) + " at cell (" + std::to_string(X - kGhost) + ", " +
                      std::to_string(Y - kGhost + c->row0) + ")"};
     }
+    if (cls == 3)
+        throw CudaErr{"slab exchange: a neighbour did not arrive within the timeout (peer exchange, tp_peer.cu)"};
     static const char* names[6] = {"ws", "wf", "qsx", "qsy", "qfx", "qfy"};
     const int f = static_cast<int>((key >> 56) & 0x3full);
     const int Y = static_cast<int>((key >> 28) & 0xfffffffull);
@@ -583,6 +600,8 @@ void create_impl(tp_ctx* c, const tp_params* p, const tp_dem* dem, int row0, int
     ck(cudaMalloc(&c->dFlagA, ntiles * sizeof(unsigned short)), "cudaMalloc flags");
     ck(cudaMalloc(&c->dFlagB, ntiles * sizeof(unsigned short)), "cudaMalloc flags");
     ck(cudaMalloc(&c->dTiles, sizeof(int) * ntiles), "cudaMalloc tiles");
+    ck(cudaMalloc(&c->dBox, sizeof(tpb::PeerBox)), "cudaMalloc mailbox");
+    ck(cudaMemsetAsync(c->dBox, 0, sizeof(tpb::PeerBox), c->stream), "memset");
     ck(cudaMalloc(&c->dNact, 6 * sizeof(int)), "cudaMalloc tiles");
     ck(cudaMemsetAsync(c->dNact, 0, 6 * sizeof(int), c->stream), "memset");
     invalidate_flags(c, true, true);
@@ -709,6 +728,8 @@ void tp_destroy(tp_ctx* c) {
         if (e) cudaEventDestroy(e);
     cudaFree(c->dTiles);
     cudaFree(c->dNact);
+    for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
+    cudaFree(c->dBox);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
     delete c;
 }
@@ -963,6 +984,88 @@ int tp_set_advection_only(tp_ctx* c, int on) {
     })
 }
 
+}  // extern "C"
+
+namespace {
+
+// tp_steps in pieces, so several contexts of one process (slabs connected by
+// tp_peer_connect_local) can advance in lockstep: every member must launch the same
+// graphs, because the graphs exchange with each other.
+struct StepsRun {
+    long long max_steps = 0;
+    long long launched = 0;  // graph steps launched (sequence-number bookkeeping)
+    DevScalars h{};
+    bool finished = false;
+    double* dts = nullptr;
+};
+
+void steps_begin(tp_ctx* c, StepsRun& r, double t, double t_next, double t_end, long max_steps, double* dts) {
+    r.max_steps = max_steps;
+    r.dts = dts;
+    c->launches = 0;
+    if (dts && c->dts_cap < max_steps) {
+        cudaFree(c->dDts);
+        c->dDts = nullptr;
+        ck(cudaMalloc(&c->dDts, sizeof(double) * max_steps), "cudaMalloc dts");
+        c->dts_cap = max_steps;
+    }
+    double* dts_dev = dts ? c->dDts : nullptr;
+    ck(cudaMemcpyAsync(&c->dSc->dts, &dts_dev, sizeof(double*), cudaMemcpyHostToDevice, c->stream), "dts ptr");
+    write_ctrl(c, t, t_next, t_end, 0.0, max_steps);
+    if (c->peered)
+        ck(cudaMemcpyAsync(&c->dSc->peer_base, &c->peer_base, sizeof(c->peer_base), cudaMemcpyHostToDevice,
+                           c->stream),
+           "peer base");
+    if (!c->lam_valid) {
+        fresh_lambda(c);
+        c->launches += 1;
+    }
+    if (!c->graphK || c->graphK_steps != c->graph_steps) {
+        drop_graphs(c);
+        c->graphK = capture_steps(c, c->graph_steps);
+        c->graph1 = capture_steps(c, 1);
+        c->graphK_steps = c->graph_steps;
+    }
+    if (c->last_tiles_stage == 0) {  // the graphs start with a predictor list
+        ck(cudaMemsetAsync(c->dNact, 0, sizeof(int), c->stream), "memset");
+        ck(cudaMemsetAsync(c->dNact + 4, 0, sizeof(int), c->stream), "memset");
+    }
+    c->last_tiles_stage = 1;
+}
+
+void steps_launch(tp_ctx* c, StepsRun& r) {
+    const bool big = (r.max_steps - r.h.steps) >= c->graph_steps;
+    const int k = big ? c->graph_steps : 1;
+    ck(cudaGraphLaunch(big ? c->graphK : c->graph1, c->stream), "graph launch");
+    c->launches += (c->peered ? 10L : 5L) * k;
+    r.launched += k;
+}
+
+void steps_poll(tp_ctx* c, StepsRun& r) {
+    r.h = read_scalars(c);
+    r.finished = r.h.done != 0;
+}
+
+void steps_end(tp_ctx* c, StepsRun& r, double* t, long* steps, int* hit) {
+    const DevScalars& h = r.h;
+    if (c->peered) c->peer_base += 4ull * static_cast<unsigned long long>(r.launched + 1);
+    *steps = static_cast<long>(h.steps);
+    *t = h.t;
+    *hit = h.steps > 0 ? h.hit : 0;
+    c->lam_valid = h.steps > 0 || c->lam_valid;
+    c->ghosts_in_B = c->ghosts_in_B || h.steps > 0;
+    if (r.dts && h.steps > 0)
+        ck(cudaMemcpy(r.dts, c->dDts, sizeof(double) * h.steps, cudaMemcpyDeviceToHost), "dts D2H");
+    if (h.err_key != tpb::kNoError) {
+        c->lam_valid = false;
+        raise_error_key(c, h.err_key, c->dB);
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
 int tp_steps(tp_ctx* c, double t_next, double t_end, long max_steps, double* t, long* steps, int* hit,
              double* dts) {
     TP_GUARD(c, {
@@ -970,52 +1073,173 @@ int tp_steps(tp_ctx* c, double t_next, double t_end, long max_steps, double* t, 
         *hit = 0;
         c->launches = 0;
         if (max_steps <= 0 || !(*t < t_end)) return TP_OK;
-        if (dts && c->dts_cap < max_steps) {
-            cudaFree(c->dDts);
-            c->dDts = nullptr;
-            ck(cudaMalloc(&c->dDts, sizeof(double) * max_steps), "cudaMalloc dts");
-            c->dts_cap = max_steps;
+        StepsRun r;
+        steps_begin(c, r, *t, t_next, t_end, max_steps, dts);
+        while (!r.finished) {
+            steps_launch(c, r);
+            steps_poll(c, r);
         }
-        double* dts_dev = dts ? c->dDts : nullptr;
-        ck(cudaMemcpyAsync(&c->dSc->dts, &dts_dev, sizeof(double*), cudaMemcpyHostToDevice, c->stream),
-           "dts ptr");
-        write_ctrl(c, *t, t_next, t_end, 0.0, max_steps);
-        if (!c->lam_valid) {
-            fresh_lambda(c);
-            c->launches += 1;
+        steps_end(c, r, t, steps, hit);
+    })
+}
+
+int tp_steps_group(tp_ctx* const* cs, int n, double t_next, double t_end, long max_steps, double* t, long* steps,
+                   int* hit) {
+    tp_ctx* c0 = n > 0 ? cs[0] : nullptr;
+    TP_GUARD(c0, {
+        if (n <= 0) throw ConfigErr{"tp_steps_group: no contexts"};
+        *steps = 0;
+        *hit = 0;
+        if (max_steps <= 0 || !(*t < t_end)) return TP_OK;
+        std::vector<StepsRun> runs(static_cast<size_t>(n));
+        for (int k = 0; k < n; ++k) {
+            cudaSetDevice(cs[k]->device);
+            steps_begin(cs[k], runs[k], *t, t_next, t_end, max_steps, nullptr);
         }
-        if (!c->graphK || c->graphK_steps != c->graph_steps) {
-            drop_graphs(c);
-            c->graphK = capture_steps(c, c->graph_steps);
-            c->graph1 = capture_steps(c, 1);
-            c->graphK_steps = c->graph_steps;
-        }
-        if (c->last_tiles_stage == 0) {  // the graphs start with a predictor list
-            ck(cudaMemsetAsync(c->dNact, 0, sizeof(int), c->stream), "memset");
-            ck(cudaMemsetAsync(c->dNact + 4, 0, sizeof(int), c->stream), "memset");
-        }
-        c->last_tiles_stage = 1;
-        long long done_steps = 0;
-        DevScalars h{};
         for (;;) {
-            const bool big = (max_steps - done_steps) >= c->graph_steps;
-            ck(cudaGraphLaunch(big ? c->graphK : c->graph1, c->stream), "graph launch");
-            c->launches += 5L * (big ? c->graph_steps : 1);
-            h = read_scalars(c);
-            done_steps = h.steps;
-            if (h.done) break;
+            for (int k = 0; k < n; ++k) {  // every member launches before anyone waits
+                cudaSetDevice(cs[k]->device);
+                steps_launch(cs[k], runs[k]);
+            }
+            bool any = false, all = true;
+            for (int k = 0; k < n; ++k) {
+                cudaSetDevice(cs[k]->device);
+                steps_poll(cs[k], runs[k]);
+                any = any || runs[k].finished;
+                all = all && runs[k].finished;
+            }
+            if (any) {
+                if (!all) throw CudaErr{"tp_steps_group: members stopped at different steps"};
+                break;
+            }
         }
-        *steps = static_cast<long>(h.steps);
-        *t = h.t;
-        *hit = h.steps > 0 ? h.hit : 0;
-        c->lam_valid = h.steps > 0 || c->lam_valid;
-        c->ghosts_in_B = c->ghosts_in_B || h.steps > 0;
-        if (dts && h.steps > 0)
-            ck(cudaMemcpy(dts, c->dDts, sizeof(double) * h.steps, cudaMemcpyDeviceToHost), "dts D2H");
-        if (h.err_key != tpb::kNoError) {
-            c->lam_valid = false;
-            raise_error_key(c, h.err_key, c->dB);
+        double tk = 0.0;
+        long sk = 0;
+        int hk = 0;
+        std::string err;
+        for (int k = 0; k < n; ++k) {  // finish every member, then report the first error
+            cudaSetDevice(cs[k]->device);
+            try {
+                steps_end(cs[k], runs[k], &tk, &sk, &hk);
+            } catch (const NumErr& e) {
+                if (err.empty()) err = e.msg;
+            }
+            if (k == 0) {
+                *t = tk;
+                *steps = sk;
+                *hit = hk;
+            }
         }
+        cudaSetDevice(c0->device);
+        if (!err.empty()) throw NumErr{err};
+    })
+}
+
+// ---- device-resident slab exchange: connection ------------------------------------
+
+namespace {
+struct PeerBlob {  // what one rank publishes (TP_PEER_BLOB_BYTES, include/tpflow_b200.h)
+    cudaIpcMemHandle_t state[2];
+    cudaIpcMemHandle_t box;
+    long long fs;
+    int ny, row0, row1, nx, pad[2];
+};
+static_assert(sizeof(PeerBlob) <= TP_PEER_BLOB_BYTES, "peer blob too large");
+
+void peer_check_layout(tp_ctx* c, int rank, int nranks) {
+    if (nranks < 1 || nranks > tpb::kMaxRanks) throw ConfigErr{"peer: nranks must be in [1, 16]"};
+    if (rank < 0 || rank >= nranks) throw ConfigErr{"peer: rank out of range"};
+    (void)c;
+}
+
+void peer_finish(tp_ctx* c, int rank, int nranks) {
+    c->link.rank = rank;
+    c->link.nranks = nranks;
+    c->link.my_box = c->dBox;
+    c->peered = nranks > 1;
+    c->peer_base = 0;
+    ck(cudaMemsetAsync(c->dBox, 0, sizeof(tpb::PeerBox), c->stream), "memset");
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    drop_graphs(c);
+}
+}  // namespace
+
+int tp_peer_export(tp_ctx* c, void* blob) {
+    TP_GUARD(c, {
+        PeerBlob b{};
+        ck(cudaIpcGetMemHandle(&b.state[0], c->rawA), "ipc handle");
+        ck(cudaIpcGetMemHandle(&b.state[1], c->rawB), "ipc handle");
+        ck(cudaIpcGetMemHandle(&b.box, c->dBox), "ipc handle");
+        b.fs = c->fs;
+        b.ny = c->ny;
+        b.row0 = c->row0;
+        b.row1 = c->row1;
+        b.nx = c->nx;
+        std::memset(blob, 0, TP_PEER_BLOB_BYTES);
+        std::memcpy(blob, &b, sizeof(b));
+    })
+}
+
+int tp_peer_connect(tp_ctx* c, int rank, int nranks, const void* blobs) {
+    TP_GUARD(c, {
+        peer_check_layout(c, rank, nranks);
+        const auto* B = static_cast<const unsigned char*>(blobs);
+        auto blob = [&](int r) {
+            PeerBlob b;
+            std::memcpy(&b, B + static_cast<size_t>(r) * TP_PEER_BLOB_BYTES, sizeof(b));
+            return b;
+        };
+        auto open = [&](const cudaIpcMemHandle_t& h) {
+            void* p = nullptr;
+            ck(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess), "ipc open");
+            c->ipc_opened.push_back(p);
+            return p;
+        };
+        tpb::PeerLink L{};
+        for (int r = 0; r < nranks; ++r)
+            L.box[r] = r == rank ? c->dBox : static_cast<tpb::PeerBox*>(open(blob(r).box));
+        for (int side = 0; side < 2; ++side) {
+            const int nb = side == 0 ? rank - 1 : rank + 1;
+            if (nb < 0 || nb >= nranks) continue;
+            const PeerBlob b = blob(nb);
+            if (b.nx != c->nx || (side == 0 ? b.row1 != c->row0 : b.row0 != c->row1))
+                throw ConfigErr{"peer: rank " + std::to_string(nb) + " is not the adjacent slab"};
+            for (int buf = 0; buf < 2; ++buf)
+                L.nbr_state[buf][side] = static_cast<double*>(open(b.state[buf])) + 1;  // + pad column
+            L.nbr_fs[side] = b.fs;
+            L.nbr_ny[side] = b.ny;
+            L.nbr_box[side] = L.box[nb];
+        }
+        c->link = L;
+        peer_finish(c, rank, nranks);
+    })
+}
+
+int tp_peer_connect_local(tp_ctx* c, int rank, int nranks, tp_ctx* const* all) {
+    TP_GUARD(c, {
+        peer_check_layout(c, rank, nranks);
+        tpb::PeerLink L{};
+        for (int r = 0; r < nranks; ++r) L.box[r] = all[r]->dBox;
+        for (int side = 0; side < 2; ++side) {
+            const int nb = side == 0 ? rank - 1 : rank + 1;
+            if (nb < 0 || nb >= nranks) continue;
+            const tp_ctx* o = all[nb];
+            if (o->nx != c->nx || (side == 0 ? o->row1 != c->row0 : o->row0 != c->row1))
+                throw ConfigErr{"peer: context " + std::to_string(nb) + " is not the adjacent slab"};
+            if (o->device != c->device) {
+                const cudaError_t e = cudaDeviceEnablePeerAccess(o->device, 0);
+                if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+                    ck(e, "peer access");
+                cudaGetLastError();
+            }
+            L.nbr_state[0][side] = o->dA;
+            L.nbr_state[1][side] = o->dB;
+            L.nbr_fs[side] = o->fs;
+            L.nbr_ny[side] = o->ny;
+            L.nbr_box[side] = o->dBox;
+        }
+        c->link = L;
+        peer_finish(c, rank, nranks);
     })
 }
 

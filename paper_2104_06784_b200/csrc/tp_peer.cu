@@ -1,0 +1,163 @@
+// Device-resident row-slab exchange over peer memory (NVLink / CUDA IPC), SURVEY.md §8(e).
+//
+// One context per slab (one rank per GPU, or several contexts in one process).  Each
+// step of the device loop exchanges, without the host:
+//   * the wave-speed bound: every rank writes its local lambda (the bits of a double
+//     >= 0, so the unsigned maximum is the floating maximum: exact, partition independent)
+//     and its stop flag into every rank's mailbox, then each rank reduces its own mailbox
+//     (peer_lambda_kernel, before compute_dt);
+//   * the halo rows exactly where the reference refills ghosts (solver.cpp:639, :523):
+//     after apply_boundaries each slab stores its 2 edge interior rows of all 6 fields,
+//     at full padded width (W/E ghosts included, which keeps the reference's corner
+//     semantics), straight into the neighbour's halo rows, then releases a sequence number
+//     into the neighbour's mailbox (peer_halo_push_kernel); the neighbour's
+//     peer_wait_kernel acquires it before its stage kernel reads the box.
+// Sequence numbers derive from the step counter, which every rank advances identically
+// (dt is identical), so the graph of a step is the same on every rank.  Stores are
+// made visible with __threadfence_system() + st.release.sys; waits use ld.acquire.sys.
+// A wait that sees no progress for kPeerTimeoutNs sets the context's error key.
+#include <cuda_runtime.h>
+
+#include "tp_types.h"
+
+namespace tpb {
+
+constexpr unsigned long long kPeerTimeoutNs = 20ull * 1000ull * 1000ull * 1000ull;  // 20 s
+constexpr unsigned long long kPeerTimeoutKey = (3ull << 62);  // error class 3: peer timeout
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+// spin until *p >= seq; false on timeout
+__device__ __forceinline__ bool wait_seq(const unsigned long long* p, unsigned long long seq) {
+    if (ld_acquire_sys(p) >= seq) return true;
+    const unsigned long long t0 = gtime();
+    for (;;) {
+        __nanosleep(200);
+        if (ld_acquire_sys(p) >= seq) return true;
+        if (gtime() - t0 > kPeerTimeoutNs) return false;
+    }
+}
+
+// Sequence numbers of one step (steps = DevScalars::steps before the step's post).
+// peer_base is advanced by the host after every tp_steps call by 4 * (graph steps + 1),
+// identically on every rank, so sequence numbers only grow.
+__device__ __forceinline__ unsigned long long seq_of(const DevScalars* sc, int phase) {
+    return sc->peer_base + 4ull * static_cast<unsigned long long>(sc->steps) +
+           static_cast<unsigned long long>(phase) + 1ull;
+}
+
+// lambda + stop all-reduce of one step (one CTA of kMaxRanks threads).  Runs whatever
+// the stop flag says, so every rank executes the same exchanges.
+__global__ void peer_lambda_kernel(PeerLink L, DevScalars* sc) {
+    __shared__ unsigned long long red[2][kMaxRanks];
+    __shared__ int timed_out;
+    const int k = threadIdx.x;
+    const unsigned long long seq = seq_of(sc, 0);
+    if (k == 0) timed_out = 0;
+    __syncthreads();
+    if (k < L.nranks) {
+        PeerBox* b = L.box[k];
+        b->lam_val[L.rank] = sc->lam_cur;
+        b->stop_val[L.rank] = (sc->err_key != kNoError) ? 1ull : 0ull;
+        __threadfence_system();
+        st_release_sys(&b->lam_seq[L.rank], seq);
+    }
+    __syncthreads();
+    unsigned long long lam = 0ull, stop = 0ull;
+    if (k < L.nranks) {
+        if (wait_seq(&L.my_box->lam_seq[k], seq)) {
+            lam = *(volatile unsigned long long*)&L.my_box->lam_val[k];
+            stop = *(volatile unsigned long long*)&L.my_box->stop_val[k];
+        } else {
+            atomicExch(&timed_out, 1);
+        }
+    }
+    red[0][k] = lam;
+    red[1][k] = stop;
+    __syncthreads();
+    if (k == 0) {
+        unsigned long long m = 0ull, st = 0ull;
+        for (int r = 0; r < L.nranks; ++r) {
+            m = red[0][r] > m ? red[0][r] : m;
+            st |= red[1][r];
+        }
+        sc->lam_cur = m;
+        if (st) sc->done = 1;
+        if (timed_out) {
+            atomicMin(&sc->err_key, kPeerTimeoutKey);
+            sc->done = 1;
+        }
+    }
+}
+
+// Store this slab's 2 edge interior rows of buffer `buf` into each neighbour's halo rows,
+// then release the sequence number into the neighbour's mailbox (last CTA per side).
+//   to the south neighbour (rank-1): my rows 3,4   -> its rows ny-3, ny-2
+//   to the north neighbour (rank+1): my rows ny-5, ny-4 -> its rows 1, 2
+__global__ void peer_halo_push_kernel(PeerLink L, GridDesc g, const double* __restrict__ s, int buf,
+                                      DevScalars* sc) {
+    if (*(volatile int*)&sc->done) return;  // consistent on every rank (see peer_lambda_kernel)
+    const int side = blockIdx.y;
+    double* dst = L.nbr_state[buf][side];
+    if (!dst) return;
+    const long long n = 2ll * 6 * g.nx;  // 2 rows x 6 fields x padded width
+    const int src_row = side == 0 ? 3 : g.ny - 5;
+    const int dst_row = side == 0 ? L.nbr_ny[0] - 3 : 1;
+    const long long dfs = L.nbr_fs[side];
+    for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < n;
+         e += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const int i = static_cast<int>(e % g.nx);
+        const long long r = e / g.nx;      // f * 2 + row
+        const int f = static_cast<int>(r >> 1), dr = static_cast<int>(r & 1);
+        dst[f * dfs + static_cast<long long>(dst_row + dr) * g.pitch + i] =
+            s[f * g.fs + static_cast<long long>(src_row + dr) * g.pitch + i];
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned int* cnt = &L.my_box->push_done[buf][side];
+        if (atomicAdd(cnt, 1u) == gridDim.x - 1) {  // the last CTA of this side
+            *cnt = 0u;
+            __threadfence_system();
+            // the neighbour files data from its north (side 1) when we are its south
+            st_release_sys(&L.nbr_box[side]->halo_seq[buf][side == 0 ? 1 : 0], seq_of(sc, 1 + buf));
+        }
+    }
+}
+
+// Wait for the halo rows of buffer `buf` from both neighbours.
+__global__ void peer_wait_kernel(PeerLink L, DevScalars* sc, int buf) {
+    if (*(volatile int*)&sc->done) return;
+    const int side = threadIdx.x;
+    if (side > 1 || !L.nbr_state[buf][side]) return;
+    if (!wait_seq(&L.my_box->halo_seq[buf][side], seq_of(sc, 1 + buf))) {
+        atomicMin(&sc->err_key, kPeerTimeoutKey);
+        sc->done = 1;
+    }
+}
+
+cudaError_t launch_peer_lambda(const PeerLink& L, DevScalars* sc, cudaStream_t st) {
+    peer_lambda_kernel<<<1, kMaxRanks, 0, st>>>(L, sc);
+    return cudaGetLastError();
+}
+cudaError_t launch_peer_halo(const PeerLink& L, const GridDesc& g, const double* s, int buf, DevScalars* sc,
+                             cudaStream_t st) {
+    peer_halo_push_kernel<<<dim3(16, 2), 256, 0, st>>>(L, g, s, buf, sc);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    peer_wait_kernel<<<1, 32, 0, st>>>(L, sc, buf);
+    return cudaGetLastError();
+}
+
+}  // namespace tpb

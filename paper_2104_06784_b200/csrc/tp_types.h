@@ -68,6 +68,7 @@ struct DevScalars {
     unsigned long long err_key;   // earliest error (see error keys in tp_kernels.cu)
     double audit[10];             // solid {initial, final, injected, outflow, clipped}, fluid {...}
     double* dts;                  // optional per-step dt record (device)
+    unsigned long long peer_base; // sequence base of the slab exchange (tp_peer.cu)
 };
 
 struct GridDesc {
@@ -183,6 +184,30 @@ struct PostArgs {
     const double* tally_corr;
     int ntx, nty;
     int loop;
+};
+
+// ---- device-resident row-slab exchange (tp_peer.cu) ----------------------------
+constexpr int kMaxRanks = 16;
+// Per-context mailbox in device memory (exported by CUDA IPC across processes): the
+// neighbours write halo-arrival sequence numbers, every rank writes its lambda slot.
+struct PeerBox {
+    unsigned long long halo_seq[2][2];          // [buf A/B][side 0 = from south, 1 = from north]
+    unsigned long long lam_seq[kMaxRanks];      // [rank] sequence of lam_val/stop_val
+    unsigned long long lam_val[kMaxRanks];      // bits of the rank's local lambda (>= 0)
+    unsigned long long stop_val[kMaxRanks];     // 1 if the rank stopped (error)
+    unsigned int push_done[2][2];               // local: CTAs finished pushing [buf][side]
+    unsigned int pad[4];
+};
+// Where this slab's neighbours live (pointers valid in this process: own allocations,
+// allocations of contexts in this process, or CUDA-IPC mappings of other processes').
+struct PeerLink {
+    double* nbr_state[2][2];     // [buf A/B][side 0 = rank-1 (south), 1 = rank+1 (north)]; null = none
+    long long nbr_fs[2];
+    int nbr_ny[2];
+    PeerBox* nbr_box[2];
+    PeerBox* box[kMaxRanks];     // every rank's mailbox (lambda all-reduce)
+    PeerBox* my_box;
+    int rank, nranks;
 };
 
 }  // namespace tpb

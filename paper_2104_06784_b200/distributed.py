@@ -226,6 +226,53 @@ class SlabRunner:
             np.sum([s.audit() for s in self.slabs], axis=0)
 
 
+class PeerGroup:
+    """Slabs of one process joined by the device-resident exchange (tp_peer_connect_local):
+    halo rows are stored straight into the neighbour's buffers and lambda is reduced in
+    device memory inside the step graphs (tp_peer.cu), no host round trip per step.
+    Every slab needs its own CUDA stream (a slab's waits must not block its neighbour)."""
+
+    def __init__(self, slabs):
+        self.slabs = list(slabs)
+        n = len(self.slabs)
+        streams = {id(s.stream) for s in self.slabs}
+        if len(streams) != n:
+            raise ValueError("PeerGroup: every slab needs its own stream")
+        self.L = self.slabs[0].L
+        self._hs = (C.c_void_p * n)(*[s.h.value for s in self.slabs])
+        for r, s in enumerate(self.slabs):
+            s.sim._check(self.L.tp_peer_connect_local(s.h, r, n, self._hs))
+
+    def steps(self, t: float, t_next: float, max_steps: int, t_end: Optional[float] = None):
+        tt, n, hit = C.c_double(t), C.c_long(), C.c_int()
+        te = t_next if t_end is None else t_end
+        self.slabs[0].sim._check(self.L.tp_steps_group(self._hs, len(self.slabs), t_next, te, int(max_steps),
+                                                       C.byref(tt), C.byref(n), C.byref(hit)))
+        return tt.value, n.value, bool(hit.value)
+
+    def audit(self) -> np.ndarray:
+        return np.sum([s.audit() for s in self.slabs], axis=0)
+
+
+def peer_connect_ranks(slab: "CudaSlab", group=None) -> None:
+    """One slab per process: all-gather the CUDA-IPC blobs (include/tpflow_b200.h
+    TP_PEER_BLOB_BYTES) over torch.distributed and connect; afterwards every rank calls
+    slab.sim.steps(...) with identical arguments."""
+    import torch
+    import torch.distributed as dist
+    nb = 256
+    blob = (C.c_ubyte * nb)()
+    slab.sim._check(slab.L.tp_peer_export(slab.h, blob))
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    dev = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
+    mine = torch.tensor(list(bytes(blob)), dtype=torch.uint8, device=dev)
+    allb = [torch.empty(nb, dtype=torch.uint8, device=dev) for _ in range(world)]
+    dist.all_gather(allb, mine, group=group)
+    flat = bytes(torch.cat(allb).cpu().tolist())
+    buf = (C.c_ubyte * len(flat)).from_buffer_copy(flat)
+    slab.sim._check(slab.L.tp_peer_connect(slab.h, rank, world, buf))
+
+
 def assemble(states: Sequence[np.ndarray]) -> np.ndarray:
     """Interior rows of per-slab padded states -> the interior of the whole grid."""
     return np.concatenate([s[:, 3:-3, 3:-3] for s in states], axis=1)

@@ -5,7 +5,7 @@ import numpy as np
 import pytest
 
 from paper_2104_06784_b200 import scenarios
-from paper_2104_06784_b200.distributed import CudaSlab, LocalComm, SlabRunner, assemble, decompose
+from paper_2104_06784_b200.distributed import CudaSlab, LocalComm, PeerGroup, SlabRunner, assemble, decompose
 from tests.util import assert_bitwise
 
 pytestmark = pytest.mark.gpu
@@ -31,3 +31,78 @@ def test_cuda_slabs_equal_single_device(gpu, oracle_kind, make, parts):
     assert t2 == t1
     assert_bitwise(assemble([s.state() for s in slabs]), ref.state()[:, 3:-3, 3:-3], "interior")
     np.testing.assert_allclose(run.audit(), ref.audit(), rtol=1e-12, atol=1e-300)
+
+
+@pytest.mark.parametrize("parts", [2, 3])
+@pytest.mark.parametrize("make", [lambda: scenarios.c1_hill(64),
+                                  lambda: scenarios.c3_channel(80, 48, t_end=30.0, dt_out=0.5),
+                                  lambda: scenarios.wet_valley(96, 70)])
+def test_peer_slabs_equal_single_device(gpu, oracle_kind, make, parts):
+    """Device-resident exchange (tp_peer.cu): halo rows stored into the neighbours'
+    buffers and lambda reduced in device memory inside the step graphs."""
+    import torch
+    from oracle.oracle import OracleSim
+    sc = make()
+    steps = 40
+    t_next = 0.5 / sc.config.scaling.t_unit() if sc.config.inflow else 1e9
+    ref = OracleSim(sc, oracle_kind)
+    t1, d1, _ = ref.steps(0.0, t_next, steps, t_end=1e9)
+    slabs = [CudaSlab(sc, r, stream=torch.cuda.Stream()) for r in decompose(sc.nrows, parts)]
+    group = PeerGroup(slabs)
+    t2, n2, _ = group.steps(0.0, t_next, steps, t_end=1e9)
+    assert n2 == len(d1)
+    assert t2 == t1
+    assert_bitwise(assemble([s.state() for s in slabs]), ref.state()[:, 3:-3, 3:-3], "interior")
+    np.testing.assert_allclose(group.audit(), ref.audit(), rtol=1e-12, atol=1e-300)
+    # a second call continues the same sequence numbering
+    t3, n3, _ = group.steps(t2, t_next, 7, t_end=1e9)
+    t4, d4, _ = ref.steps(t1, t_next, 7, t_end=1e9)
+    assert n3 == len(d4) and t3 == t4
+    assert_bitwise(assemble([s.state() for s in slabs]), ref.state()[:, 3:-3, 3:-3], "interior after 2nd call")
+
+
+def _peer_rank_main(rank, world, port, make_name, steps, outdir):
+    """One rank of the two-process test (both on cuda:0; CUDA IPC within one device)."""
+    import os
+    import torch
+    import torch.distributed as dist
+    from paper_2104_06784_b200.distributed import CudaSlab, decompose, peer_connect_ranks
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    sc = _MAKERS[make_name]()
+    slab = CudaSlab(sc, decompose(sc.nrows, world)[rank], stream=torch.cuda.Stream())
+    peer_connect_ranks(slab)
+    t_next = 0.5 / sc.config.scaling.t_unit() if sc.config.inflow else 1e9
+    t, n, hit = slab.sim.steps(0.0, t_next, steps, t_end=1e9)
+    np.save(os.path.join(outdir, f"state{rank}.npy"), slab.state())
+    np.save(os.path.join(outdir, f"meta{rank}.npy"), np.array([t, n]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+_MAKERS = {"c1": lambda: scenarios.c1_hill(64), "wet": lambda: scenarios.wet_valley(96, 70)}
+
+
+@pytest.mark.parametrize("make_name", ["c1", "wet"])
+def test_peer_two_processes_ipc(gpu, oracle_kind, make_name, tmp_path):
+    """Two processes (one rank each, as under torchrun) connected by CUDA IPC: the halo
+    stores and the lambda reduction cross process boundaries in device memory."""
+    import socket
+    import torch.multiprocessing as mp
+    from oracle.oracle import OracleSim
+    steps = 25
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    mp.start_processes(_peer_rank_main, args=(2, port, make_name, steps, str(tmp_path)), nprocs=2,
+                       start_method="spawn")
+    sc = _MAKERS[make_name]()
+    ref = OracleSim(sc, oracle_kind)
+    t_next = 0.5 / sc.config.scaling.t_unit() if sc.config.inflow else 1e9
+    t1, d1, _ = ref.steps(0.0, t_next, steps, t_end=1e9)
+    states = [np.load(tmp_path / f"state{r}.npy") for r in range(2)]
+    metas = [np.load(tmp_path / f"meta{r}.npy") for r in range(2)]
+    for m in metas:
+        assert m[0] == t1 and int(m[1]) == len(d1)
+    assert_bitwise(assemble(states), ref.state()[:, 3:-3, 3:-3], "interior (2 processes)")
