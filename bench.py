@@ -193,7 +193,7 @@ def run_b200(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if world > 1 or args.gpus > 1:
         from paper_2104_06784_b200 import distributed
-        return distributed.bench_main(args, METRIC)
+        return distributed.bench_main(args, METRIC, clock_sampler=ClockSampler)
 
     torch.cuda.set_device(0)
     sc = scenario_for(args.config, args.ncols, args.nrows)

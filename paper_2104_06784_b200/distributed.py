@@ -279,11 +279,14 @@ def assemble(states: Sequence[np.ndarray]) -> np.ndarray:
 
 
 # ---------------------------------------------------------------------------
-# bench.py --gpus N (torchrun): weak scaling, one 2048-row slab per rank
+# bench.py --gpus N (torchrun): weak scaling, one slab per rank, device-resident exchange
 # ---------------------------------------------------------------------------
-def bench_main(args, metric: str) -> None:
+def bench_main(args, metric: str, clock_sampler=None) -> None:
+    """Each rank owns a [rows_per x ncols] slab of one (ncols x rows_per*N) grid of the
+    chosen scenario; slabs are joined by the device-resident exchange (tp_peer.cu over
+    CUDA IPC / NVLink).  Timed: K steps of the device loop on every rank, CUDA events on
+    the launching stream, max over ranks."""
     import json
-    import time
     import torch
     import torch.distributed as dist
     from . import scenarios
@@ -291,39 +294,86 @@ def bench_main(args, metric: str) -> None:
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
+    ndev = torch.cuda.device_count()
+    dev = local % ndev  # one GPU per rank; fewer GPUs than ranks only for functional runs
+    torch.cuda.set_device(dev)
     if not dist.is_initialized():
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        dist.init_process_group("nccl" if ndev >= world else "gloo",
+                                **({"device_id": torch.device(f"cuda:{dev}")} if ndev >= world else {}))
     rows_per = args.nrows
     sc = scenarios.SCENARIOS[args.config](args.ncols, rows_per * world) if args.config != "c1" \
         else scenarios.c1_hill(args.ncols)
     rows = decompose(sc.nrows, world)[rank]
     stream = torch.cuda.Stream()
-    slab = CudaSlab(sc, rows, device=local, stream=stream)
-    runner = SlabRunner([slab], TorchComm())
-    with torch.cuda.stream(stream):
-        t, _, _ = runner.steps(0.0, 1e9, args.warmup, t_end=1e9)
-        torch.cuda.synchronize()
-        dist.barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        t, dts, _ = runner.steps(t, 1e9, args.steps, t_end=1e9)
-        e1.record(stream)
-        torch.cuda.synchronize()
-    ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=f"cuda:{local}")
-    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    ms = float(ms.item())
+    slab = CudaSlab(sc, rows, device=dev, stream=stream)
+    peer_connect_ranks(slab)
+    sim = slab.sim
+    sim.set_option("graph_steps", args.graph_steps)
+    tu = sc.config.scaling.t_unit()
+    t_end = sc.config.t_end / tu
+    t_next = min(sc.config.dt_out / tu, t_end)
+
+    t, n0, _ = sim.steps(0.0, t_next, args.warmup, t_end=t_end)
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks = clock_sampler(dev) if clock_sampler else None
+    if clocks:
+        clocks.__enter__()
+    torch.cuda.synchronize()
+    e0.record(stream)
+    t, n, _ = sim.steps(t, t_next, args.steps, t_end=t_end)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if clocks:
+        clocks.__exit__(None, None, None)
+    launches = sim.kernel_launches()
+    act_p, act_c, ntiles = sim.active_tiles()
+    ms_t = torch.tensor([e0.elapsed_time(e1), float(n)], dtype=torch.float64)
+    if dist.get_backend() == "nccl":
+        ms_t = ms_t.cuda()
+    dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms, nmax = float(ms_t[0]), int(ms_t[1])
+    assert n == args.steps == nmax, (n, args.steps, nmax)
     cells = sc.ncols * sc.nrows
     value = cells * args.steps / (ms / 1e3) / 1e9
+
+    # e2e: the same steps through the C ABI with this rank's state from / to pinned host memory
+    nbytes = 6 * sim.ny * sim.nx * 8
+    h_in = torch.empty(6 * sim.ny * sim.nx, dtype=torch.float64, pin_memory=True)
+    h_out = torch.empty_like(h_in)
+    dp = C.POINTER(C.c_double)
+    sim._check(sim.L.tp_get_state(sim.h, C.cast(h_in.data_ptr(), dp)))
+    sim._check(sim.L.tp_get_state(sim.h, C.cast(h_out.data_ptr(), dp)))
+    dist.barrier()
+    import time
+    w0 = time.perf_counter()
+    sim._check(sim.L.tp_set_state(sim.h, C.cast(h_in.data_ptr(), dp)))
+    t2, ne, _ = sim.steps(t, t_next, args.steps, t_end=t_end)
+    sim._check(sim.L.tp_get_state(sim.h, C.cast(h_out.data_ptr(), dp)))
+    w = torch.tensor([time.perf_counter() - w0], dtype=torch.float64)
+    if dist.get_backend() == "nccl":
+        w = w.cuda()
+    dist.all_reduce(w, op=dist.ReduceOp.MAX)
+    e2e_v = cells * ne / float(w[0]) / 1e9
     if rank == 0:
         out = {"metric": metric, "value": round(value, 4), "unit": "GCUPS", "n_gpus": world,
                "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 5),
                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-               "data": "synthetic (scenarios.py)",
-               "config": {"workload": f"{sc.name} {sc.ncols}x{sc.nrows} (weak: {rows_per} rows per GPU), "
-                                      "row-block slabs, NCCL halo exchange + lambda all-reduce",
+               "data": f"synthetic (deterministic {sc.name} generator in scenarios.py; no network data)",
+               "config": {"workload": f"{sc.name} {sc.ncols}x{sc.nrows} (weak: {rows_per} rows x {args.ncols} "
+                                      f"per GPU), row-block slabs joined by the device-resident exchange "
+                                      f"(halo rows stored into the neighbour's buffers over peer memory, "
+                                      f"lambda all-reduce in device memory; tp_peer.cu)",
                           "grid": [sc.ncols, sc.nrows], "parallelism": f"slab{world}",
-                          "l2": "inputs larger than L2"},
-               "gpu_launches": None}
+                          "gpus_visible": ndev,
+                          "l2": ("per-rank inputs larger than L2" if 18 * sim.ny * sim.nx * 8 > 126e6 else
+                                 "per-rank inputs fit in L2 (functional size)"),
+                          "active_tiles_last_step_rank0": [act_p, act_c, ntiles]},
+               "e2e": {"value": round(e2e_v, 4), "unit": "GCUPS", "h2d_bytes_per_step": nbytes // max(ne, 1),
+                       "d2h_bytes_per_step": nbytes // max(ne, 1),
+                       "mode": f"per rank: tp_set_state(pinned host) + tp_steps({ne}) + tp_get_state, max over ranks"},
+               "clocks": clocks.summary() if clocks else None,
+               "gpu_launches": launches}
         print(json.dumps(out))
     dist.barrier()
