@@ -148,8 +148,8 @@ struct tp_ctx {
     bool peered = false;
     unsigned long long peer_base = 0; // host copy of DevScalars::peer_base
     std::vector<void*> ipc_opened;    // CUDA-IPC mappings to close at destroy
-    int* dNact = nullptr;             // [6] list counts pred, corr; last-launch stats pred, corr;
-                                      // safe-tile counts pred, corr
+    int* dNact = nullptr;             // [8] list counts pred, corr; last-launch stats pred, corr;
+                                      // safe-tile counts pred, corr; tile-scheduler counters
     int last_tiles_stage = 1;         // stage of the last tiles_kernel enqueued (0 pred, 1 corr)
     bool lam_valid = false;
     bool ghosts_in_B = false;
@@ -261,6 +261,7 @@ tpb::StageArgs stage_args(tp_ctx* c, bool corr, int loop) {
     a.ntiles_active = c->dNact + (corr ? 1 : 0);
     a.flag_out = corr ? c->dFlagA : c->dFlagB;
     a.nact_stat = c->dNact + 2;
+    a.work = c->dNact + 6 + (corr ? 1 : 0);
     return a;
 }
 
@@ -271,6 +272,7 @@ tpb::TileArgs tile_args(tp_ctx* c, const tpb::StageArgs& a, bool corr) {
     t.tiles = c->dTiles;
     t.ntiles_active = c->dNact + (corr ? 1 : 0);
     t.ntiles_reset = c->dNact + (corr ? 0 : 1);
+    t.work = c->dNact + 6 + (corr ? 1 : 0);
     t.tally = a.tally;
     t.ntx = c->ntx;
     t.nty = c->nty;
@@ -602,8 +604,8 @@ void create_impl(tp_ctx* c, const tp_params* p, const tp_dem* dem, int row0, int
     ck(cudaMalloc(&c->dTiles, sizeof(int) * ntiles), "cudaMalloc tiles");
     ck(cudaMalloc(&c->dBox, sizeof(tpb::PeerBox)), "cudaMalloc mailbox");
     ck(cudaMemsetAsync(c->dBox, 0, sizeof(tpb::PeerBox), c->stream), "memset");
-    ck(cudaMalloc(&c->dNact, 6 * sizeof(int)), "cudaMalloc tiles");
-    ck(cudaMemsetAsync(c->dNact, 0, 6 * sizeof(int), c->stream), "memset");
+    ck(cudaMalloc(&c->dNact, 8 * sizeof(int)), "cudaMalloc tiles");
+    ck(cudaMemsetAsync(c->dNact, 0, 8 * sizeof(int), c->stream), "memset");
     invalidate_flags(c, true, true);
     {
         // device geometry layout (tp_types.h GeoField): the 14 reference fields

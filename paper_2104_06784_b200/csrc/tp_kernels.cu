@@ -261,6 +261,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
     __shared__ unsigned long long barc;  // per-cell geometry box
     __shared__ int s_tile;               // list entry of the next tile (read by thread 0 at issue time)
     __shared__ unsigned s_flags;         // output-flag bits of the tile in flight
+    __shared__ int s_nli[2];             // next list index, by iteration parity
     const double* Cg = sm + SM_C;        // [NGCELL][TY][TX]: nX, nY, dnX/dxi, dnY/dxi, dnZ/dxi, dnX/deta, dnY/deta, dnZ/deta, RN(1/nZ)
     double* S = sm + SM_S;
     const double* G = sm + SM_G;
@@ -288,9 +289,8 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
     // next tile's TMA is issued as soon as the current tile's staged boxes are
     // dead (after Phase 2), so it lands while Phase 3 computes.
     // list entries are packed (tile row << 16) | tile column (tiles_kernel)
-    auto issue_cell = [&](int li) {  // per-cell geometry of list entry li (thread 0)
+    auto issue_cell = [&](int li, int e) {  // per-cell geometry of list entry li = e (thread 0)
         if (li < nact) {
-            const int e = A.tiles[li];
             mbar_expect_tx(&barc, kTmaCellBytes);
             tma_load_3d(sm + SM_C, &A.tm_c, 3 + (e & 0xffff) * TX + 1, 3 + ((e >> 16) & 0x1fff) * TY, G_NX, &barc);
         }
@@ -307,7 +307,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
             // x coordinate + 1: the leading pad column of the device layout (tp_capi.cpp)
             tma_load_3d(S, &A.tm_s, bx0 + 1, by0, 0, &bar);
             tma_load_3d(sm + SM_G, &A.tm_g, bx0 + 1, by0, 0, &bar);
-            issue_cell(blockIdx.x);
+            issue_cell(blockIdx.x, e);
         }
     }
     if (threadIdx.x == 0) s_flags = 0u;
@@ -315,7 +315,10 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
     double lam_local = 0.0;
     unsigned iter = 0;
     TPROBE_DECL
-    for (int li = blockIdx.x; li < nact; li += gridDim.x, ++iter) {
+    // Dynamic tile scheduler: every CTA starts on list entry blockIdx.x, then claims the
+    // next entry with one atomic per tile (claimed a tile ahead, so the TMA prefetch still
+    // has a target) - CTAs that drew cheap, partially dry tiles take more of them.
+    for (int li = blockIdx.x; li < nact; ++iter) {
     const int entry = s_tile;  // written by thread 0 before the previous end-of-tile barrier
     const int tix = entry & 0xffff, tiy = (entry >> 16) & 0x1fff;
     const int tile = tiy * A.ntx + tix;
@@ -330,9 +333,13 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
 #pragma unroll
         for (int f = 0; f < 6; ++f) prefetch_l2(A.u0 + f * fs + o3);
     }
-    // thread 0 fetches the next list entry now; it is consumed at issue time
-    const int nli = li + gridDim.x;
-    const int next_entry = (threadIdx.x == 0 && nli < nact) ? A.tiles[nli] : 0;
+    // thread 0 claims the next list entry now; it is consumed at issue time
+    int nli = nact, next_entry = 0;
+    if (threadIdx.x == 0) {
+        nli = static_cast<int>(gridDim.x) + atomicAdd(A.work, 1);
+        if (nli < nact) next_entry = A.tiles[nli];
+        s_nli[iter & 1u] = nli;
+    }
     // next tile's boxes into S/G (call only once they are dead)
     auto issue_next = [&]() {
         if (threadIdx.x == 0 && nli < nact) {
@@ -697,8 +704,9 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
     if (threadIdx.x == 0) {
         A.flag_out[tile] = static_cast<unsigned short>(s_flags);
         s_flags = 0u;  // next write after at least one more barrier
-        issue_cell(li + gridDim.x);
+        issue_cell(nli, next_entry);
     }
+    li = s_nli[iter & 1u];  // written before Phase 1, published by the barriers since
     }  // tile loop
     TPROBE_FLUSH(CORR ? 1 : 0)
 
@@ -765,6 +773,7 @@ __device__ __forceinline__ void tiles_body(const TileArgs& a, int block) {
     if (t == 0) {
         *a.ntiles_reset = 0;
         a.ntiles_reset[4] = 0;  // the other stage's safe-tile count (diagnostics)
+        *a.work = 0;            // this stage's dynamic tile scheduler (its previous launch is done)
     }
     const unsigned m = __ballot_sync(0xffffffffu, active);
     const unsigned ms = __ballot_sync(0xffffffffu, active && safe);

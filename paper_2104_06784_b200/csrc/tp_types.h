@@ -117,6 +117,7 @@ struct StageArgs {
     const int* ntiles_active;
     unsigned short* flag_out;        // per-tile TileFlag bits of `out` (nonzero bits per region)
     int* nact_stat;                  // [2] list length of the last predictor / corrector launch
+    int* work;                       // dynamic tile scheduler counter of this stage (zeroed by tiles_kernel)
 };
 
 // Per-tile output flags: which regions of the tile's interior hold a value with a nonzero
@@ -147,6 +148,7 @@ struct TileArgs {
     int* ntiles_active;   // this stage's counter (zeroed by the other stage's tiles_kernel);
                           // [4] past it: this stage's safe-tile count
     int* ntiles_reset;    // the other stage's counter
+    int* work;            // this stage's dynamic tile scheduler counter (zeroed here)
     double* tally;
     int ntx, nty;
     int skip;             // 0 = list every tile
