@@ -15,6 +15,7 @@
 #include <climits>
 #include <cmath>
 #include <cstddef>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -36,6 +37,8 @@ cudaError_t launch_regularize(const GridDesc& g, const Phys& P, double* s, const
                               DevScalars* sc, bool fastdiv, cudaStream_t st);
 cudaError_t init_kernels();
 cudaError_t launch_tiles(const TileArgs& a, cudaStream_t st);
+cudaError_t build_geometry_device(const double* dem_h, int ncols, int nrows, double L, double cellsize, int row0,
+                                  int ny, const GridDesc& g, double* geo, cudaStream_t st);
 cudaError_t launch_peer_lambda(const PeerLink& L, DevScalars* sc, cudaStream_t st);
 cudaError_t launch_peer_halo(const PeerLink& L, const GridDesc& g, const double* s, int buf, DevScalars* sc,
                              cudaStream_t st);
@@ -138,6 +141,7 @@ struct tp_ctx {
     bool skip_dry = true;  // list only tiles that are not bitwise no-ops (tiles_kernel)
     bool geo_safe = false; // every jb (and so every face jbf) in [1, 2^100]: safe tiles allowed
     bool geo_safe2 = false; // geometry and constants inside the window-B bounds
+    bool host_geometry = false;  // TPFLOW_HOST_GEOMETRY=1: host restatement instead of tp_geometry.cu
     unsigned short* dFlagA = nullptr;  // per-tile TileFlag bits of A / B (all set = unknown)
     unsigned short* dFlagB = nullptr;
     int* dTiles = nullptr;            // active-tile list of the stage in flight + its count
@@ -533,6 +537,25 @@ int fail(tp_ctx* c, int code, const std::string& msg) {
         return fail(c, TP_ERR_INTERNAL, e.what());                \
     }
 
+// Window B of the safe-tile form (DESIGN.md §3 item 6): every geometry value 0 or of
+// magnitude in [2^-50, 2^50], jb <= 2^50, and the constants entering numerators within
+// 2^+-20 (eps_h within [2^-60, 2^20]).  n = padded cells of this context.
+void geo_window_b(tp_ctx* c, size_t n) {
+    auto mag_ok = [](double v, double lo, double hi) {
+        const double a = std::fabs(v);
+        return a == 0.0 || (a >= lo && a <= hi);
+    };
+    c->geo_safe2 = c->geo_safe;
+    for (size_t k = 0; k < 14 * n && c->geo_safe2; ++k)
+        c->geo_safe2 = std::isfinite(c->geo_h[k]) && mag_ok(c->geo_h[k], 0x1p-50, 0x1p50);
+    for (size_t k = 0; k < n && c->geo_safe2; ++k) c->geo_safe2 = c->geo_h[3 * n + k] <= 0x1p50;
+    const tpb::Phys& P = c->ph;
+    const double w20 = 0x1p20, n20 = 0x1p-20;
+    c->geo_safe2 = c->geo_safe2 && P.eps_h >= 0x1p-60 && P.eps_h <= w20 && P.eps >= n20 && P.eps <= w20 &&
+                   mag_ok(P.oma, n20, 1.0) && mag_ok(P.theta_b, n20, w20) && P.N_R >= n20 && P.N_R <= w20 &&
+                   P.dxi >= n20 && P.dxi <= w20 && P.deta >= n20 && P.deta <= w20;
+}
+
 void create_impl(tp_ctx* c, const tp_params* p, const tp_dem* dem, int row0, int row1) {
     validate_params(p);
     if (!dem || dem->ncols < 2 || dem->nrows < 2)
@@ -556,17 +579,30 @@ void create_impl(tp_ctx* c, const tp_params* p, const tp_dem* dem, int row0, int
     c->dem.cellsize = dem->cellsize;
     c->dem.z.assign(dem->z, dem->z + static_cast<size_t>(dem->ncols) * dem->nrows);
 
-    // Simulator ctor: geometry of the whole extended DEM (solver.cpp:16), then our rows
-    tpb::host::Geometry G = tpb::host::compute_geometry(tpb::host::extend_grid(c->dem, kGhost), p->L);
-    c->nx = G.nx;
+    // Simulator ctor: geometry of the whole extended DEM (solver.cpp:16), then our rows.
+    // Built on the device (tp_geometry.cu) unless TPFLOW_HOST_GEOMETRY=1 selects the host
+    // restatement (tp_geometry.cpp); both are bit-identical to terrain.cpp.
+    const char* hg = std::getenv("TPFLOW_HOST_GEOMETRY");
+    c->host_geometry = hg && hg[0] == '1';
+    tpb::host::Geometry G;
+    if (c->host_geometry) {
+        G = tpb::host::compute_geometry(tpb::host::extend_grid(c->dem, kGhost), p->L);
+        c->nx = G.nx;
+        c->dxi = G.dxi;
+        c->deta = G.deta;
+    } else {
+        c->nx = dem->ncols + 2 * kGhost;
+        c->dxi = dem->cellsize / p->L;  // terrain.cpp:162-163
+        c->deta = dem->cellsize / p->L;
+    }
     c->ny = c->nrows + 2 * kGhost;
-    c->dxi = G.dxi;
-    c->deta = G.deta;
-    c->geo_h.resize(14ull * c->nx * c->ny);
-    for (int k = 0; k < 14; ++k)
-        std::memcpy(c->geo_h.data() + static_cast<size_t>(k) * c->nx * c->ny,
-                    G.field(k) + static_cast<size_t>(row0) * G.nx,
-                    sizeof(double) * static_cast<size_t>(c->nx) * c->ny);
+    if (c->host_geometry) {
+        c->geo_h.resize(14ull * c->nx * c->ny);
+        for (int k = 0; k < 14; ++k)
+            std::memcpy(c->geo_h.data() + static_cast<size_t>(k) * c->nx * c->ny,
+                        G.field(k) + static_cast<size_t>(row0) * G.nx,
+                        sizeof(double) * static_cast<size_t>(c->nx) * c->ny);
+    }
 
     c->pitch = (c->nx + 1 + 7) & ~7;
     c->fs = static_cast<long long>(c->pitch) * c->ny;
@@ -607,65 +643,75 @@ void create_impl(tp_ctx* c, const tp_params* p, const tp_dem* dem, int row0, int
     ck(cudaMalloc(&c->dNact, 8 * sizeof(int)), "cudaMalloc tiles");
     ck(cudaMemsetAsync(c->dNact, 0, 8 * sizeof(int), c->stream), "memset");
     invalidate_flags(c, true, true);
-    {
-        // device geometry layout (tp_types.h GeoField): the 14 reference fields
-        // regrouped + RN(1/jb), RN(1/nZ) and the face RN(1/jbf) of the whole grid
-        const size_t n = static_cast<size_t>(c->nx) * c->ny;
-        const size_t gnx = static_cast<size_t>(G.nx);
-        std::vector<double> dg(static_cast<size_t>(tpb::G_COUNT) * n, 0.0);
-        auto src = [&](int rf) { return c->geo_h.data() + static_cast<size_t>(rf) * n; };
-        const int map[][2] = {{tpb::G_JB, tpb::R_JB},   {tpb::G_NZ, tpb::R_NZ},   {tpb::G_A11, tpb::R_A11},
-                              {tpb::G_A12, tpb::R_A12}, {tpb::G_A21, tpb::R_A21}, {tpb::G_A22, tpb::R_A22},
-                              {tpb::G_NX, tpb::R_NX},   {tpb::G_NY, tpb::R_NY},
-                              {tpb::G_DNX_DXI, tpb::R_DNX_DXI},   {tpb::G_DNY_DXI, tpb::R_DNY_DXI},
-                              {tpb::G_DNZ_DXI, tpb::R_DNZ_DXI},   {tpb::G_DNX_DETA, tpb::R_DNX_DETA},
-                              {tpb::G_DNY_DETA, tpb::R_DNY_DETA}, {tpb::G_DNZ_DETA, tpb::R_DNZ_DETA}};
-        for (const auto& m : map) std::memcpy(dg.data() + m[0] * n, src(m[1]), sizeof(double) * n);
-        const double* gjb = G.field(tpb::R_JB);  // global rows: the face average may reach row1+3
-        for (int j = 0; j < c->ny; ++j) {
-            const int gj = j + row0;
-            for (int i = 0; i < c->nx; ++i) {
-                const size_t k = static_cast<size_t>(j) * c->nx + i;
-                const double jb = gjb[gj * gnx + i];
-                dg[tpb::G_RJB * n + k] = 1.0 / jb;
-                dg[tpb::G_RNZ * n + k] = 1.0 / src(tpb::R_NZ)[k];
-                if (i + 1 < c->nx) dg[tpb::G_RJBFX * n + k] = 1.0 / (0.5 * (jb + gjb[gj * gnx + i + 1]));
-                if (gj + 1 < G.ny) dg[tpb::G_RJBFY * n + k] = 1.0 / (0.5 * (jb + gjb[(gj + 1) * gnx + i]));
+    if (c->host_geometry) {
+            // device geometry layout (tp_types.h GeoField): the 14 reference fields
+            // regrouped + RN(1/jb), RN(1/nZ) and the face RN(1/jbf) of the whole grid
+            const size_t n = static_cast<size_t>(c->nx) * c->ny;
+            const size_t gnx = static_cast<size_t>(G.nx);
+            std::vector<double> dg(static_cast<size_t>(tpb::G_COUNT) * n, 0.0);
+            auto src = [&](int rf) { return c->geo_h.data() + static_cast<size_t>(rf) * n; };
+            const int map[][2] = {{tpb::G_JB, tpb::R_JB},   {tpb::G_NZ, tpb::R_NZ},   {tpb::G_A11, tpb::R_A11},
+                                  {tpb::G_A12, tpb::R_A12}, {tpb::G_A21, tpb::R_A21}, {tpb::G_A22, tpb::R_A22},
+                                  {tpb::G_NX, tpb::R_NX},   {tpb::G_NY, tpb::R_NY},
+                                  {tpb::G_DNX_DXI, tpb::R_DNX_DXI},   {tpb::G_DNY_DXI, tpb::R_DNY_DXI},
+                                  {tpb::G_DNZ_DXI, tpb::R_DNZ_DXI},   {tpb::G_DNX_DETA, tpb::R_DNX_DETA},
+                                  {tpb::G_DNY_DETA, tpb::R_DNY_DETA}, {tpb::G_DNZ_DETA, tpb::R_DNZ_DETA}};
+            for (const auto& m : map) std::memcpy(dg.data() + m[0] * n, src(m[1]), sizeof(double) * n);
+            const double* gjb = G.field(tpb::R_JB);  // global rows: the face average may reach row1+3
+            for (int j = 0; j < c->ny; ++j) {
+                const int gj = j + row0;
+                for (int i = 0; i < c->nx; ++i) {
+                    const size_t k = static_cast<size_t>(j) * c->nx + i;
+                    const double jb = gjb[gj * gnx + i];
+                    dg[tpb::G_RJB * n + k] = 1.0 / jb;
+                    dg[tpb::G_RNZ * n + k] = 1.0 / src(tpb::R_NZ)[k];
+                    if (i + 1 < c->nx) dg[tpb::G_RJBFX * n + k] = 1.0 / (0.5 * (jb + gjb[gj * gnx + i + 1]));
+                    if (gj + 1 < G.ny) dg[tpb::G_RJBFY * n + k] = 1.0 / (0.5 * (jb + gjb[(gj + 1) * gnx + i]));
+                }
             }
-        }
-        // safe tiles (tp_kernels.cu stage_phase1<FD, false>) need every face/cell divisor in
-        // the FASTDIV window: jb in [1, 2^100] makes jb and 0.5*(jb_l + jb_r) qualify
+            // safe tiles (tp_kernels.cu stage_phase1<FD, false>) need every face/cell divisor in
+            // the FASTDIV window: jb in [1, 2^100] makes jb and 0.5*(jb_l + jb_r) qualify
+            c->geo_safe = true;
+            for (size_t k = 0; k < n && c->geo_safe; ++k) {
+                const double jb = dg[tpb::G_JB * n + k];
+                c->geo_safe = jb >= 1.0 && jb <= 0x1p100;
+            }
+            // window B (Phase 2 + Phase-3 divergence without window tests) assumes every
+            // geometry value is 0 or of magnitude in [2^-50, 2^50], jb <= 2^50, and the
+            // constants that enter numerators within 2^+-20 (eps_h within [2^-60, 2^20]);
+            // the bound chain is in DESIGN.md §3
+            geo_window_b(c, n);
+            ck(cudaMemsetAsync(c->rawGeo, 0, sizeof(double) * tpb::G_COUNT * c->fs, c->stream), "memset");
+            ck(cudaMemcpy2DAsync(c->dGeo, c->pitch * sizeof(double), dg.data(), c->nx * sizeof(double),
+                                 c->nx * sizeof(double), static_cast<size_t>(tpb::G_COUNT) * c->ny,
+                                 cudaMemcpyHostToDevice, c->stream),
+               "geometry H2D");
+            ck(cudaStreamSynchronize(c->stream), "sync");
+    } else {
+        ck(cudaMemsetAsync(c->rawGeo, 0, sizeof(double) * tpb::G_COUNT * c->fs, c->stream), "memset");
+        ck(tpb::build_geometry_device(dem->z, dem->ncols, dem->nrows, p->L, dem->cellsize, row0, c->ny, c->g,
+                                      c->dGeo, c->stream),
+           "device geometry");
+        // host copy of the 14 reference fields (terrain.hpp:59-63 order) for the host-side
+        // initial conditions, error texts and tp_get_geometry
+        const size_t n = static_cast<size_t>(c->nx) * c->ny;
+        c->geo_h.resize(14 * n);
+        const int map[14] = {tpb::G_NX, tpb::G_NY, tpb::G_NZ, tpb::G_JB, tpb::G_A11, tpb::G_A12, tpb::G_A21,
+                             tpb::G_A22, tpb::G_DNX_DXI, tpb::G_DNY_DXI, tpb::G_DNZ_DXI, tpb::G_DNX_DETA,
+                             tpb::G_DNY_DETA, tpb::G_DNZ_DETA};
+        for (int k = 0; k < 14; ++k)
+            ck(cudaMemcpy2DAsync(c->geo_h.data() + k * n, c->nx * sizeof(double), c->dGeo + map[k] * c->fs,
+                                 c->pitch * sizeof(double), c->nx * sizeof(double), c->ny, cudaMemcpyDeviceToHost,
+                                 c->stream),
+               "geometry D2H");
+        ck(cudaStreamSynchronize(c->stream), "sync");
         c->geo_safe = true;
+        c->geo_safe2 = true;
         for (size_t k = 0; k < n && c->geo_safe; ++k) {
-            const double jb = dg[tpb::G_JB * n + k];
+            const double jb = c->geo_h[3 * n + k];
             c->geo_safe = jb >= 1.0 && jb <= 0x1p100;
         }
-        // window B (Phase 2 + Phase-3 divergence without window tests) assumes every
-        // geometry value is 0 or of magnitude in [2^-50, 2^50], jb <= 2^50, and the
-        // constants that enter numerators within 2^+-20 (eps_h within [2^-60, 2^20]);
-        // the bound chain is in DESIGN.md §3
-        auto mag_ok = [](double v, double lo, double hi) {
-            const double a = std::fabs(v);
-            return a == 0.0 || (a >= lo && a <= hi);
-        };
-        c->geo_safe2 = c->geo_safe;
-        for (size_t k = 0; k < 14 * n && c->geo_safe2; ++k)
-            c->geo_safe2 = std::isfinite(c->geo_h[k]) && mag_ok(c->geo_h[k], 0x1p-50, 0x1p50);
-        for (size_t k = 0; k < n && c->geo_safe2; ++k) c->geo_safe2 = dg[tpb::G_JB * n + k] <= 0x1p50;
-        {
-            const tpb::Phys& P = c->ph;
-            const double w20 = 0x1p20, n20 = 0x1p-20;
-            c->geo_safe2 = c->geo_safe2 && P.eps_h >= 0x1p-60 && P.eps_h <= w20 && P.eps >= n20 &&
-                           P.eps <= w20 && mag_ok(P.oma, n20, 1.0) && mag_ok(P.theta_b, n20, w20) &&
-                           P.N_R >= n20 && P.N_R <= w20 && P.dxi >= n20 && P.dxi <= w20 &&
-                           P.deta >= n20 && P.deta <= w20;
-        }
-        ck(cudaMemsetAsync(c->rawGeo, 0, sizeof(double) * tpb::G_COUNT * c->fs, c->stream), "memset");
-        ck(cudaMemcpy2DAsync(c->dGeo, c->pitch * sizeof(double), dg.data(), c->nx * sizeof(double),
-                             c->nx * sizeof(double), static_cast<size_t>(tpb::G_COUNT) * c->ny,
-                             cudaMemcpyHostToDevice, c->stream),
-           "geometry H2D");
-        ck(cudaStreamSynchronize(c->stream), "sync");
+        geo_window_b(c, n);
     }
     // the maps cover the pad column too (x coordinate = logical column + 1)
     c->tmA = make_box_map(c->rawA, c->nx + 1, c->ny, c->pitch, c->fs, 6);

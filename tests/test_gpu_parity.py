@@ -146,6 +146,22 @@ def test_run_report_matches(gpu, oracle_kind):
     assert_bitwise(sim.state(), ref.state(), "state after run")
 
 
+@pytest.mark.parametrize("make", [lambda: scenarios.c1_hill(64), lambda: scenarios.c4_terrain(120, 90),
+                                  lambda: scenarios.c3_channel(96, 48)])
+def test_device_geometry_bitwise(gpu, oracle_kind, make):
+    """Geometry built on the device (tp_geometry.cu) vs the reference's compute_geometry on
+    the extended DEM (terrain.cpp:113-215), all 14 fields, whole grid and a middle slab."""
+    from paper_2104_06784_b200.simulator import Simulator
+    from oracle.oracle import OracleSim
+    sc = make()
+    ref = OracleSim(sc, oracle_kind).geometry()
+    sim = Simulator.from_scenario(sc, init=False)
+    assert_bitwise(sim.geometry(), ref, "device geometry")
+    r0, r1 = sc.nrows // 3, 2 * sc.nrows // 3
+    slab = Simulator.from_scenario(sc, rows=(r0, r1), init=False)
+    assert_bitwise(slab.geometry(), ref[:, r0:r1 + 6, :], "device geometry of a slab")
+
+
 @pytest.mark.parametrize("make", [lambda: scenarios.c1_hill(64), lambda: scenarios.wet_valley(80, 72)])
 def test_snapshot_bitwise(gpu, oracle_kind, make):
     """Simulator::snapshot (solver.cpp:590-617) computed on the device, field by field."""
