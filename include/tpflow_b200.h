@@ -110,6 +110,10 @@ int tp_set_audit(tp_ctx* c, const double* audit10);
 int tp_interior_mass(tp_ctx* c, double* mass_solid, double* mass_fluid);
 /* Simulator::snapshot (solver.cpp:590-617): h, phi_s, vXs, vYs, vXf, vYf on the
  * interior (6 * ncols * nrows_local), physical units */
+/* interior masses reduced on the device (deterministic, compensated; within ~1 ulp of the
+ * exact sum, not bit-identical to the reference's serial KahanSum, which tp_interior_mass
+ * keeps): the fast conservation check for large grids */
+int tp_interior_mass_device(tp_ctx* c, double* ms, double* mf);
 int tp_snapshot(tp_ctx* c, double* out6);
 
 /* ---- multi-GPU slab plumbing (row-block decomposition) ---------

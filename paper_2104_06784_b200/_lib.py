@@ -57,6 +57,7 @@ SIGNATURES = {
     "tp_set_audit": (C.c_int, [_vp, _dp]),
     "tp_interior_mass": (C.c_int, [_vp, _dp, _dp]),
     "tp_snapshot": (C.c_int, [_vp, _dp]),
+    "tp_interior_mass_device": (C.c_int, [_vp, _dp, _dp]),
     "tp_halo_bytes": (C.c_long, [_vp]),
     "tp_halo_pack": (C.c_int, [_vp, C.c_int, C.c_int, _vp]),
     "tp_halo_unpack": (C.c_int, [_vp, C.c_int, C.c_int, _vp]),

@@ -43,6 +43,7 @@ cudaError_t launch_peer_lambda(const PeerLink& L, DevScalars* sc, cudaStream_t s
 cudaError_t launch_peer_halo(const PeerLink& L, const GridDesc& g, const double* s, int buf, DevScalars* sc,
                              cudaStream_t st);
 cudaError_t launch_pack_state(const GridDesc& g, const double* src, double* dst, bool unpack, cudaStream_t st);
+cudaError_t launch_mass(const GridDesc& g, const double* s, double* part, int blocks, cudaStream_t st);
 cudaError_t launch_snapshot(const GridDesc& g, const double* s, const double* geo, double* out, int ncols,
                             int nrows, double H, double h_dry, double eps_h, double vu, cudaStream_t st);
 cudaError_t launch_pre(const PreArgs& a, cudaStream_t st);
@@ -1374,6 +1375,27 @@ int tp_interior_mass(tp_ctx* c, double* ms, double* mf) {
                     sum = t;
                 }
             (p == 0 ? *ms : *mf) = sum * c->dxi * c->deta;
+        }
+    })
+}
+
+int tp_interior_mass_device(tp_ctx* c, double* ms, double* mf) {
+    TP_GUARD(c, {
+        const int blocks = 296;
+        double* d = dense_staging(c);  // >= 4 * blocks doubles
+        ck(tpb::launch_mass(c->g, c->dA, d, blocks, c->stream), "mass_kernel");
+        std::vector<double> part(4ull * blocks);
+        ck(cudaMemcpyAsync(part.data(), d, sizeof(double) * part.size(), cudaMemcpyDeviceToHost, c->stream),
+           "mass D2H");
+        ck(cudaStreamSynchronize(c->stream), "sync");
+        for (int p = 0; p < 2; ++p) {
+            double a = 0.0, e = 0.0;
+            for (int b = 0; b < blocks; ++b) {  // block order, compensated
+                const double x = part[(2 * b + p) * 2], y = a + x, bb = y - a;
+                e += (a - (y - bb)) + (x - bb) + part[(2 * b + p) * 2 + 1];
+                a = y;
+            }
+            (p == 0 ? *ms : *mf) = (a + e) * c->dxi * c->deta;
         }
     })
 }

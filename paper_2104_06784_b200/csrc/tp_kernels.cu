@@ -1198,6 +1198,56 @@ cudaError_t launch_snapshot(const GridDesc& g, const double* s, const double* ge
     return cudaGetLastError();
 }
 
+// Interior mass of ws and wf on the device: each block reduces
+// a fixed set of rows with compensated (TwoSum) accumulation in a fixed order and writes
+// its (sum, error) pair per phase; the host folds the block partials in block order
+// (tp_interior_mass_device).  Deterministic; within ~1 ulp of the exact sum, where the
+// reference's serial KahanSum (field.hpp:46-59, solver.cpp:582-588, kept bit-exact by
+// tp_interior_mass) is within ~2 ulp.
+__device__ __forceinline__ void two_sum(double a, double b, double& s, double& e) {
+    s = a + b;
+    const double bb = s - a;
+    e = (a - (s - bb)) + (b - bb);
+}
+__global__ void __launch_bounds__(256) mass_kernel(GridDesc g, const double* __restrict__ s, double* __restrict__ part) {
+    const int rows = g.ny - 6, cols = g.nx - 6;
+    __shared__ double red[4][256];
+    double acc[2] = {0.0, 0.0}, err[2] = {0.0, 0.0};
+    for (int r = blockIdx.x; r < rows; r += gridDim.x) {
+        const long long o = static_cast<long long>(r + 3) * g.pitch + 3;
+        for (int i = threadIdx.x; i < cols; i += blockDim.x) {
+#pragma unroll
+            for (int p = 0; p < 2; ++p) {
+                double t, e;
+                two_sum(acc[p], s[p * g.fs + o + i], t, e);
+                acc[p] = t;
+                err[p] += e;
+            }
+        }
+    }
+    red[0][threadIdx.x] = acc[0];
+    red[1][threadIdx.x] = err[0];
+    red[2][threadIdx.x] = acc[1];
+    red[3][threadIdx.x] = err[1];
+    __syncthreads();
+    if (threadIdx.x < 2) {  // fixed-order fold of the block's threads
+        const int p = threadIdx.x;
+        double a = 0.0, e = 0.0;
+        for (int k = 0; k < 256; ++k) {
+            double t, ee;
+            two_sum(a, red[2 * p][k], t, ee);
+            a = t;
+            e += ee + red[2 * p + 1][k];
+        }
+        part[(2 * blockIdx.x + p) * 2 + 0] = a;
+        part[(2 * blockIdx.x + p) * 2 + 1] = e;
+    }
+}
+cudaError_t launch_mass(const GridDesc& g, const double* s, double* part, int blocks, cudaStream_t st) {
+    mass_kernel<<<blocks, 256, 0, st>>>(g, s, part);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_pack_state(const GridDesc& g, const double* src, double* dst, bool unpack, cudaStream_t st) {
     if (unpack) unpack_state_kernel<<<4 * g_num_sms, 256, 0, st>>>(g, src, dst);
     else pack_state_kernel<<<4 * g_num_sms, 256, 0, st>>>(g, src, dst);
@@ -1226,7 +1276,7 @@ cudaError_t init_kernels() {
         reinterpret_cast<const void*>(&regularize_kernel<true>),
         reinterpret_cast<const void*>(&regularize_kernel<false>),
         reinterpret_cast<const void*>(&pack_state_kernel), reinterpret_cast<const void*>(&unpack_state_kernel),
-        reinterpret_cast<const void*>(&snapshot_kernel)};
+        reinterpret_cast<const void*>(&snapshot_kernel), reinterpret_cast<const void*>(&mass_kernel)};
     for (const void* f : fns)
         if ((e = cudaFuncGetAttributes(&fa, f)) != cudaSuccess) return e;
     return cudaSuccess;

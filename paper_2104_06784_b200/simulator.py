@@ -233,6 +233,12 @@ class Simulator:
         self._check(self.L.tp_interior_mass(self.h, C.byref(ms), C.byref(mf)))
         return ms.value, mf.value
 
+    def interior_mass_device(self):
+        """(solid, fluid) interior masses reduced on the device (within ~1 ulp of exact)."""
+        ms, mf = C.c_double(), C.c_double()
+        self._check(self.L.tp_interior_mass_device(self.h, C.byref(ms), C.byref(mf)))
+        return ms.value, mf.value
+
     def interior_mass_solid(self) -> float:
         return self.interior_mass()[0]
 

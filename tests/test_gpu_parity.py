@@ -162,6 +162,19 @@ def test_device_geometry_bitwise(gpu, oracle_kind, make):
     assert_bitwise(slab.geometry(), ref[:, r0:r1 + 6, :], "device geometry of a slab")
 
 
+def test_device_mass(gpu, oracle_kind):
+    """Device interior-mass reduction vs the reference's serial KahanSum (solver.cpp:582-588)."""
+    sc = scenarios.wet_valley(200, 170)
+    ref, sim = _pair(sc, oracle_kind)
+    ref.steps(0.0, 1.0e9, 10, t_end=1.0e9)
+    sim.steps(0.0, 1.0e9, 10, t_end=1.0e9)
+    ms_r, mf_r = ref.interior_mass()
+    ms_h, mf_h = sim.interior_mass()
+    ms_d, mf_d = sim.interior_mass_device()
+    assert (ms_h, mf_h) == (ms_r, mf_r)  # host path: the reference's Kahan bit for bit
+    assert abs(ms_d - ms_r) <= 4e-16 * abs(ms_r) and abs(mf_d - mf_r) <= 4e-16 * abs(mf_r)
+
+
 @pytest.mark.parametrize("make", [lambda: scenarios.c1_hill(64), lambda: scenarios.wet_valley(80, 72)])
 def test_snapshot_bitwise(gpu, oracle_kind, make):
     """Simulator::snapshot (solver.cpp:590-617) computed on the device, field by field."""
