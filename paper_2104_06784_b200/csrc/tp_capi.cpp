@@ -287,8 +287,7 @@ tpb::TileArgs tile_args(tp_ctx* c, const tpb::StageArgs& a, bool corr) {
     t.ring_ineligible = (c->inflow_active || !a.loop) ? 1 : 0;
     t.south_ineligible = c->g.has_south ? 0 : 1;
     t.north_ineligible = c->g.has_north ? 0 : 1;
-    t.safe_ok = (c->fastdiv && c->geo_safe) ? 1 : 0;
-    t.safe2_ok = (t.safe_ok && c->geo_safe2) ? 1 : 0;
+    t.safe_ok = (c->fastdiv && c->geo_safe && c->geo_safe2) ? 1 : 0;
     t.loop = a.loop;
     t.sc = c->dSc;
     return t;

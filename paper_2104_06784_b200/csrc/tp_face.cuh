@@ -45,8 +45,15 @@ __device__ __forceinline__ void face_flux(const double (&L)[6], const double (&R
     }
 
     // solver.cpp:277-285
-    const double celL = sqrt(P.eps * cf * smax(htL, 0.0));
-    const double celR = sqrt(P.eps * cf * smax(htR, 0.0));
+    double celL, celR;
+    if (CHK) {
+        celL = sqrt(P.eps * cf * smax(htL, 0.0));
+        celR = sqrt(P.eps * cf * smax(htR, 0.0));
+    } else {  // safe tile: the argument is +-0 or >= 2^-274, so the branch-free sequence is IEEE sqrt
+        bool oks = true;
+        celL = dsqrt_fast(P.eps * cf * smax(htL, 0.0), oks);
+        celR = dsqrt_fast(P.eps * cf * smax(htR, 0.0), oks);
+    }
     // normal / transverse momenta (solver.cpp:259-262)
     const double qnL0 = XI ? L[2] : L[3], qtL0 = XI ? L[3] : L[2];
     const double qnR0 = XI ? R[2] : R[3], qtR0 = XI ? R[3] : R[2];

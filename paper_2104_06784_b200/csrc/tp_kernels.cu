@@ -64,14 +64,7 @@ __device__ __forceinline__ unsigned cell_flag_bits(int cx, int cy) {
            ((e && n) ? TF_NE : 0u);
 }
 
-// +-0, or magnitude in [2^-200, 2^200): the safe-tile window (TF_UNSAFE)
-__device__ __forceinline__ bool in_safe_window(double x) {
-    const unsigned hi2 = static_cast<unsigned>(__double2hiint(x)) << 1;
-    const unsigned lo = static_cast<unsigned>(__double2loint(x));
-    return ((hi2 - ((1023u - 200u) << 21)) < (400u << 21)) | ((hi2 | lo) == 0u);
-}
-
-// window B of the safe-tile form of Phase 2 and the Phase-3 divergence (TF_UNSAFE2)
+// the safe-tile window (TF_UNSAFE2, DESIGN.md §3 item 6): +-0 or magnitude in [2^-100, 2^100)
 __device__ __forceinline__ bool in_safe_window2(double x) {
     const unsigned hi2 = static_cast<unsigned>(__double2hiint(x)) << 1;
     const unsigned lo = static_cast<unsigned>(__double2loint(x));
@@ -83,8 +76,7 @@ __device__ __forceinline__ bool in_safe_window2(double x) {
 template <bool FD, bool CORR>
 __device__ __forceinline__ unsigned long long cell_epilogue(double (&un)[6], const Rcp& rj, double nZ, int X, int Y,
                                               const Phys& P, DevScalars* sc, double& lam_local,
-                                              double* out, long long fs, long long o3, bool& safe_out,
-                                              bool& safe2_out) {
+                                              double* out, long long fs, long long o3, bool& safe2_out) {
     // regularize (solver.cpp:139-166), solid then fluid
     double hpv[2];
     {
@@ -158,17 +150,15 @@ __device__ __forceinline__ unsigned long long cell_epilogue(double (&un)[6], con
     }
 
     unsigned long long bits = 0ull;
-    bool inwin = true, inwin2 = true;
+    bool inwin2 = true;
 #pragma unroll
     for (int f = 0; f < 6; ++f) {
         out[f * fs + o3] = un[f];
         bits |= static_cast<unsigned long long>(__double_as_longlong(un[f]));
-        inwin = inwin && in_safe_window(un[f]);
         inwin2 = inwin2 && in_safe_window2(un[f]);
     }
     // window B also needs non-negative thicknesses (no cancellation in hs + hf)
     inwin2 = inwin2 && (__double2hiint(un[0]) >= 0 || un[0] == 0.0) && (__double2hiint(un[1]) >= 0 || un[1] == 0.0);
-    safe_out = inwin;
     safe2_out = inwin2;
     return bits;  // feeds the tile's output flags
 }
@@ -360,7 +350,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
     // left off the list by tiles_kernel, and a listed dry tile computes the same +0.0)
 
     // ---- Phase 1: xi faces, eta faces, cell fields -----------------------------
-    if (FD && (entry & kTileSafe)) stage_phase1<FD, false>(S, G, FX, FY, V, PJ, P);
+    if (FD && (entry & kTileSafe)) stage_phase1<FD, false>(S, G, FX, FY, V, PJ, P);  // safe tile
     else stage_phase1<FD, true>(S, G, FX, FY, V, PJ, P);
     TPROBE(4);  // Phase 1 work
     __syncthreads();
@@ -380,7 +370,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
     // (a) + (b) as a generic lambda: CHK = false is the safe-tile form (DESIGN.md §3,
     // window B: every box value +-0 or of magnitude in [2^-100, 2^100), geometry and
     // constants checked at setup) with the FASTDIV window tests compiled out
-    const bool safe2 = FD && (entry & kTileSafe2);
+    const bool safe2 = FD && (entry & kTileSafe);
     auto phase2 = [&](auto chk_tag) {
         constexpr bool CHK = decltype(chk_tag)::value;
         const Rcp rNRc = mkrcp_const<FD, CHK>(P.N_R, P.r_NR);
@@ -532,7 +522,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
     const Rcp rdx = mkrcp_const<FD>(P.dxi, P.r_dxi);
     const Rcp rdy = mkrcp_const<FD>(P.deta, P.r_deta);
     unsigned long long obits = 0ull;
-    bool osafe = true, osafe2 = true;
+    bool osafe2 = true;
     if (p3) {
         const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
         const int X = p3x, Y = p3y;
@@ -656,7 +646,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
         }
 
         TPROBE(13);  // phase 3: Heun average
-        obits = cell_epilogue<FD, CORR>(un, rj, nZ, X, Y, P, sc, lam_local, A.out, fs, o3, osafe, osafe2);
+        obits = cell_epilogue<FD, CORR>(un, rj, nZ, X, Y, P, sc, lam_local, A.out, fs, o3, osafe2);
         TPROBE(14);  // phase 3: regularize, finite, lambda, stores
     }
 
@@ -693,7 +683,6 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
     // barrier (FX/FY/V/PJ/BR/cell box are rewritten by the next tile) publishes them
     {
         const unsigned fb = ((p3 && obits != 0ull) ? cell_flag_bits(threadIdx.x % TX, threadIdx.x / TX) : 0u) |
-                            (osafe ? 0u : static_cast<unsigned>(TF_UNSAFE)) |
                             (osafe2 ? 0u : static_cast<unsigned>(TF_UNSAFE2));
         const unsigned wf = __reduce_or_sync(0xffffffffu, fb);
         if ((threadIdx.x & 31) == 0 && wf) atomicOr(&s_flags, wf);
@@ -720,7 +709,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
 __device__ __forceinline__ void tiles_body(const TileArgs& a, int block) {
     const int ntiles = a.ntx * a.nty;
     const int t = block * blockDim.x + threadIdx.x;
-    bool active = false, safe = false, safe2 = false;
+    bool active = false, safe = false;
     if (t < ntiles) {
         const int tx = t % a.ntx, ty = t / a.ntx;
         const bool ring = tx == 0 || tx == a.ntx - 1 || ty == 0 || ty == a.nty - 1;
@@ -760,8 +749,7 @@ __device__ __forceinline__ void tiles_body(const TileArgs& a, int block) {
             if (xr && yl) u |= F[t - a.ntx + 1];
             if (xl && yr) u |= F[t + a.ntx - 1];
             if (xr && yr) u |= F[t + a.ntx + 1];
-            safe = (u & TF_UNSAFE) == 0u;
-            safe2 = a.safe2_ok && (u & TF_UNSAFE2) == 0u;
+            safe = (u & TF_UNSAFE2) == 0u;
         }
         if (skip && ring) {
 #pragma unroll
@@ -783,8 +771,7 @@ __device__ __forceinline__ void tiles_body(const TileArgs& a, int block) {
     if (lane == 0 && ms) atomicAdd(a.ntiles_active + 4, __popc(ms));
     base = __shfl_sync(0xffffffffu, base, 0);
     if (active)
-        a.tiles[base + __popc(m & ((1u << lane) - 1u))] = ((t / a.ntx) << 16) | (t % a.ntx) | (safe ? kTileSafe : 0) |
-                                                          (safe2 ? kTileSafe2 : 0);
+        a.tiles[base + __popc(m & ((1u << lane) - 1u))] = ((t / a.ntx) << 16) | (t % a.ntx) | (safe ? kTileSafe : 0);
 }
 
 __global__ void __launch_bounds__(NT) tiles_kernel(TileArgs a) {
@@ -1328,6 +1315,13 @@ __global__ void selftest_div_kernel(long long n, unsigned long long seed, unsign
         double fg = desing_factor_g(hh, 1e-6, okg);
         if (!okg) fg = desing_factor<true>(hh, 1e-6);
         if (__double_as_longlong(fg) != __double_as_longlong(desing_factor<false>(hh, 1e-6))) ++local;
+        // square root: the branch-free sequence (when accepted) vs sqrt, and acceptance on
+        // ordinary operands (+-0 included)
+        const double xs = (mode == 3 && (i & 7) == 0) ? a : fabs(a) * (mode == 2 ? 1e-300 : 1.0);
+        bool oks = true;
+        const double sf = dsqrt_fast(xs, oks);
+        if (oks && __double_as_longlong(sf) != __double_as_longlong(sqrt(xs))) ++local;
+        if (mode != 2 && !oks) ++local;
     }
     if (local) atomicAdd(bad, local);
 }

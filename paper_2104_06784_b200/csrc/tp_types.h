@@ -122,18 +122,16 @@ struct StageArgs {
 
 // Per-tile output flags: which regions of the tile's interior hold a value with a nonzero
 // bit (the 2-cell bands and 2x2 corners are what a neighbour's radius-2 box reads).
-// TF_UNSAFE: some output value is neither +-0 nor of magnitude in [2^-200, 2^200)
-// (window A of the "safe tile" form of Phase 1); TF_UNSAFE2: the same for
-// [2^-100, 2^100) (window B: Phase 2 and the Phase-3 divergence).
+// TF_UNSAFE2: some output value is neither +-0 nor of magnitude in [2^-100, 2^100), or a
+// thickness is negative (the "safe tile" window, DESIGN.md §3 item 6).
 enum TileFlag : unsigned {
     TF_ANY = 1u, TF_W = 2u, TF_E = 4u, TF_S = 8u, TF_N = 16u,
-    TF_SW = 32u, TF_SE = 64u, TF_NW = 128u, TF_NE = 256u, TF_UNSAFE = 512u, TF_UNSAFE2 = 1024u,
+    TF_SW = 32u, TF_SE = 64u, TF_NW = 128u, TF_NE = 256u, TF_UNSAFE2 = 1024u,
     TF_ALL = 0xffffu
 };
-// list-entry bits: every state value the tile's box reads is +-0 or in window A / B
+// list-entry bit: every state value the tile's box reads is +-0 or in the safe window
 // (entries: tile column in bits 0-15, tile row in bits 16-28)
 constexpr int kTileSafe = 1 << 30;
-constexpr int kTileSafe2 = 1 << 29;
 
 // Dry-tile classification before a stage.  flag_in: per-tile flags of the stage's input
 // buffer (the radius-2 box reads interior cells of the tile and the facing bands/corners
@@ -154,8 +152,7 @@ struct TileArgs {
     int skip;             // 0 = list every tile
     int ring_ineligible;  // 1 = ring tiles read non-copy ghosts (Mode-II inflow): never skip them
     int south_ineligible, north_ineligible;  // slab edges next to halo rows: never skip
-    int safe_ok;          // FASTDIV on and the context's geometry divisors in the window
-    int safe2_ok;         // and geometry + constants inside the window-B bounds (tp_capi.cpp)
+    int safe_ok;          // FASTDIV on, geometry and constants inside the safe-window bounds (tp_capi.cpp)
     int loop;
     DevScalars* sc;
 };

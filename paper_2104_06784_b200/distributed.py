@@ -119,16 +119,31 @@ class LocalComm:
     def allreduce_max(self, slabs, lams):
         import torch
         if isinstance(lams[0], torch.Tensor):
+            # the lambdas were written on the slabs' streams; torch works on its current
+            # stream: order both ways with host synchronisation (test-path backend)
+            for s in slabs:
+                s.synchronize()
             m = lams[0].clone()
             for x in lams[1:]:
                 m = torch.maximum(m, x.to(m.device))
-            return [m.to(x.device) for x in lams]
+            out = [m.to(x.device) for x in lams]
+            torch.cuda.synchronize()
+            return out
         m = max(lams)
         return [m] * len(lams)
 
     def allreduce_sum(self, arrs):
         s = np.sum(np.stack(arrs), axis=0)
         return s
+
+
+def _on_stream(slab):
+    """torch's current stream = the slab's stream (device slabs); no-op otherwise."""
+    import contextlib
+    st = getattr(slab, "stream", None)
+    if st is None:
+        return contextlib.nullcontext()
+    return slab.torch.cuda.stream(st)
 
 
 def _sync_between(a, b):
@@ -151,8 +166,12 @@ class TorchComm:
         self.world = dist.get_world_size(group)
 
     def exchange(self, slabs, buf: int):
-        dist = self.dist
         (s,) = slabs
+        with _on_stream(s):
+            self._exchange(s, buf)
+
+    def _exchange(self, s, buf: int):
+        dist = self.dist
         ops = []
         if self.rank > 0:
             ops.append(dist.P2POp(dist.isend, s.pack(buf, 0), self.rank - 1, self.group))
@@ -172,7 +191,8 @@ class TorchComm:
         import torch
         (lam,) = lams
         t = lam if isinstance(lam, torch.Tensor) else torch.tensor([lam], dtype=torch.float64)
-        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
+        with _on_stream(slabs[0]):  # collectives on the stream that wrote lambda
+            self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
         return [t if isinstance(lam, torch.Tensor) else float(t.item())]
 
     def allreduce_sum(self, arrs):
