@@ -168,7 +168,7 @@ struct tp_ctx {
     int graphK_steps = 0;
     long launches = 0;
     double t_next_last = 0.0;
-    CUtensorMap tmA{}, tmB{}, tmG{}, tmC{};
+    CUtensorMap tmA{}, tmB{}, tmG{}, tmC{}, tmU{};
 };
 
 namespace {
@@ -250,6 +250,7 @@ tpb::StageArgs stage_args(tp_ctx* c, bool corr, int loop) {
     a.tm_s = corr ? c->tmB : c->tmA;
     a.tm_g = c->tmG;
     a.tm_c = c->tmC;
+    a.tm_u = c->tmU;
     a.g = c->g;
     a.ph = c->ph;
     a.s = corr ? c->dB : c->dA;
@@ -716,6 +717,7 @@ void create_impl(tp_ctx* c, const tp_params* p, const tp_dem* dem, int row0, int
     // the maps cover the pad column too (x coordinate = logical column + 1)
     c->tmA = make_box_map(c->rawA, c->nx + 1, c->ny, c->pitch, c->fs, 6);
     c->tmB = make_box_map(c->rawB, c->nx + 1, c->ny, c->pitch, c->fs, 6);
+    c->tmU = make_box_map(c->rawA, c->nx + 1, c->ny, c->pitch, c->fs, 6, tpb::TX, tpb::TY, 6);
     c->tmG = make_box_map(c->rawGeo, c->nx + 1, c->ny, c->pitch, c->fs, tpb::NGBOX);
     c->tmC = make_box_map(c->rawGeo, c->nx + 1, c->ny, c->pitch, c->fs, tpb::G_COUNT, tpb::TX, tpb::TY,
                           tpb::G_COUNT - tpb::NGBOX);

@@ -249,6 +249,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
     extern __shared__ __align__(128) double sm[];
     __shared__ unsigned long long bar;   // state + stencil-geometry boxes
     __shared__ unsigned long long barc;  // per-cell geometry box
+    __shared__ unsigned long long baru;  // corrector: the u^n tile
     __shared__ int s_tile;               // list entry of the next tile (read by thread 0 at issue time)
     __shared__ unsigned s_flags;         // output-flag bits of the tile in flight
     __shared__ int s_nli[2];             // next list index, by iteration parity
@@ -289,6 +290,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
     if (threadIdx.x == 0) {
         mbar_init(&bar, 1);
         mbar_init(&barc, 1);
+        mbar_init(&baru, 1);
         if (static_cast<int>(blockIdx.x) < nact) {
             const int e = A.tiles[blockIdx.x];
             s_tile = e;
@@ -318,11 +320,6 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
     const int p3x = X0 + (threadIdx.x % TX), p3y = Y0 + (threadIdx.x / TX);
     const bool p3 = threadIdx.x < TX * TY && p3x <= nx - 4 && p3y <= ny - 4;
     const long long o3 = static_cast<long long>(p3y) * pitch + p3x;
-    // u^n of this thread's cell is read in Phase 3: warm L2 now (corrector)
-    if (CORR && p3) {
-#pragma unroll
-        for (int f = 0; f < 6; ++f) prefetch_l2(A.u0 + f * fs + o3);
-    }
     // thread 0 claims the next list entry now; it is consumed at issue time
     int nli = nact, next_entry = 0;
     if (threadIdx.x == 0) {
@@ -516,6 +513,10 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
     __syncthreads();
     TPROBE(8);  // Phase 2 barrier
     issue_next();
+    if (CORR && threadIdx.x == 0) {  // u^n of this tile into the (now dead) V region
+        mbar_expect_tx(&baru, kTmaUBytes);
+        tma_load_3d(sm + SM_U, &A.tm_u, X0 + 1, Y0, 0, &baru);
+    }
 
     // ---- Phase 3: divergence + viscous source + update + cap + [average] +
     //      regularize + [finite, lambda]
@@ -640,9 +641,11 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
         }
 
         TPROBE(12);  // phase 3: Coulomb cap
-        if (CORR) {  // Heun average (solver.cpp:538-541)
+        if (CORR) {  // Heun average (solver.cpp:538-541), u^n from the TMA-staged tile
+            mbar_wait(&baru, iter & 1u);
+            const double* U = sm + SM_U;
 #pragma unroll
-            for (int f = 0; f < 6; ++f) un[f] = 0.5 * (A.u0[f * fs + o3] + un[f]);
+            for (int f = 0; f < 6; ++f) un[f] = 0.5 * (U[f * TX * TY + threadIdx.x] + un[f]);
         }
 
         TPROBE(13);  // phase 3: Heun average

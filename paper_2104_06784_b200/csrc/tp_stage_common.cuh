@@ -20,6 +20,10 @@ constexpr int SM_FY = SM_FX + 6 * NFX;                    // [6][NFY] eta face f
 constexpr int SM_C = (((SM_FY + 6 * NFY) * 8 + 127) / 128) * 16;  // [NGCELL][TY][TX] per-cell geometry (TMA)
 constexpr int NGCELL = G_COUNT - NGBOX;                   // nX, nY, 6 x dn, RN(1/nZ)
 constexpr int SM_END = SM_C + NGCELL * TX * TY;
+// corrector: the u^n tile (6 x TY x TX, TMA) lands in the velocity region, dead after Phase 2
+constexpr int SM_U = ((SM_V * 8 + 127) / 128) * 16;
+static_assert(SM_U + 6 * TX * TY <= SM_PJ + BOX, "u^n tile must fit the V/PJ region");
+constexpr unsigned kTmaUBytes = 6 * TX * TY * 8;
 constexpr unsigned kTmaCellBytes = NGCELL * TX * TY * 8;
 static_assert((SM_C * 8) % 128 == 0, "cell-geometry TMA box must be 128-byte aligned");
 constexpr unsigned kTmaBytes = (6 + NGBOX) * BOX * 8;

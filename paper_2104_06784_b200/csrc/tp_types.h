@@ -101,6 +101,7 @@ struct StageArgs {
     CUtensorMap tm_s;                // TMA descriptor of the stage input state (6 fields)
     CUtensorMap tm_g;                // TMA descriptor of the NGBOX box geometry fields
     CUtensorMap tm_c;                // TMA descriptor of the per-cell geometry fields (G_NX..G_RNZ), tile box
+    CUtensorMap tm_u;                // corrector: TMA descriptor of u^n (6 fields), interior tile box
     GridDesc g;
     Phys ph;
     const double* __restrict__ s;    // stage input state (6 fields, ghosts filled)
