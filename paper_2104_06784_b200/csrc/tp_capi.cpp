@@ -39,6 +39,11 @@ cudaError_t init_kernels();
 cudaError_t launch_tiles(const TileArgs& a, cudaStream_t st);
 cudaError_t build_geometry_device(const double* dem_h, int ncols, int nrows, double L, double cellsize, int row0,
                                   int ny, const GridDesc& g, double* geo, cudaStream_t st);
+cudaError_t launch_init_thickness(const GridDesc& g, const double* geo, const double* h, int ncols, int nrows,
+                                  double H, double phi, double* s, cudaStream_t st);
+cudaError_t launch_init_velocity(const GridDesc& g, const double* geo, const double* vx, const double* vy,
+                                 int ncols, int nrows, double vu, double* s, cudaStream_t st);
+cudaError_t launch_geo_check(const GridDesc& g, const double* geo, int* ok, cudaStream_t st);
 cudaError_t launch_peer_lambda(const PeerLink& L, DevScalars* sc, cudaStream_t st);
 cudaError_t launch_peer_halo(const PeerLink& L, const GridDesc& g, const double* s, int buf, DevScalars* sc,
                              cudaStream_t st);
@@ -451,7 +456,7 @@ void raise_error_key(tp_ctx* c, unsigned long long key, const double* pred_buf) 
         const int p = static_cast<int>(key & 1ull);
         const double* buf = cls == 0 ? pred_buf : c->dA;
         const double w = read_cell(c, buf, p, X, Y);
-        const double jb = c->geo_h[static_cast<size_t>(tpb::R_JB) * c->nx * c->ny + static_cast<size_t>(Y) * c->nx + X];
+        const double jb = read_cell(c, c->dGeo, tpb::G_JB, X, Y);
         const double hp = w / jb;
         throw NumErr{std::string("negative ") + (p == 0 ? "solid" : "fluid") + " thickness " +
                      tpb::host::to_string_f(hp) + " at cell (" + std::to_string(X - kGhost) + ", " +
@@ -541,20 +546,52 @@ int fail(tp_ctx* c, int code, const std::string& msg) {
 // Window B of the safe-tile form (DESIGN.md §3 item 6): every geometry value 0 or of
 // magnitude in [2^-50, 2^50], jb <= 2^50, and the constants entering numerators within
 // 2^+-20 (eps_h within [2^-60, 2^20]).  n = padded cells of this context.
-void geo_window_b(tp_ctx* c, size_t n) {
+bool consts_window_b(const tp_ctx* c) {
     auto mag_ok = [](double v, double lo, double hi) {
         const double a = std::fabs(v);
         return a == 0.0 || (a >= lo && a <= hi);
     };
-    c->geo_safe2 = c->geo_safe;
-    for (size_t k = 0; k < 14 * n && c->geo_safe2; ++k)
-        c->geo_safe2 = std::isfinite(c->geo_h[k]) && mag_ok(c->geo_h[k], 0x1p-50, 0x1p50);
-    for (size_t k = 0; k < n && c->geo_safe2; ++k) c->geo_safe2 = c->geo_h[3 * n + k] <= 0x1p50;
     const tpb::Phys& P = c->ph;
     const double w20 = 0x1p20, n20 = 0x1p-20;
-    c->geo_safe2 = c->geo_safe2 && P.eps_h >= 0x1p-60 && P.eps_h <= w20 && P.eps >= n20 && P.eps <= w20 &&
-                   mag_ok(P.oma, n20, 1.0) && mag_ok(P.theta_b, n20, w20) && P.N_R >= n20 && P.N_R <= w20 &&
-                   P.dxi >= n20 && P.dxi <= w20 && P.deta >= n20 && P.deta <= w20;
+    return P.eps_h >= 0x1p-60 && P.eps_h <= w20 && P.eps >= n20 && P.eps <= w20 && mag_ok(P.oma, n20, 1.0) &&
+           mag_ok(P.theta_b, n20, w20) && P.N_R >= n20 && P.N_R <= w20 && P.dxi >= n20 && P.dxi <= w20 &&
+           P.deta >= n20 && P.deta <= w20;
+}
+
+void geo_window_b(tp_ctx* c, size_t n) {
+    // host twin of geo_check_kernel (tp_geometry.cu), for the host-geometry path
+    auto mag_ok = [](double v, double lo, double hi) {
+        const double a = std::fabs(v);
+        return a == 0.0 || (a >= lo && a <= hi);
+    };
+    const double* G = c->geo_h.data();
+    bool ok = true;
+    for (size_t k = 0; k < n && ok; ++k) {
+        const double jb = G[tpb::R_JB * n + k];
+        ok = jb >= 1.0 && jb <= 0x1p50;
+        for (int f : {tpb::R_A11, tpb::R_A12, tpb::R_A21, tpb::R_A22}) ok = ok && mag_ok(G[f * n + k], 0x1p-120, 0x1p50);
+        for (int f : {tpb::R_NX, tpb::R_NY}) ok = ok && mag_ok(G[f * n + k], 0x1p-200, 1.0);
+        for (int f : {tpb::R_NZ, tpb::R_DNX_DXI, tpb::R_DNY_DXI, tpb::R_DNZ_DXI, tpb::R_DNX_DETA, tpb::R_DNY_DETA,
+                      tpb::R_DNZ_DETA})
+            ok = ok && std::isfinite(G[f * n + k]);
+    }
+    c->geo_safe2 = c->geo_safe && ok && consts_window_b(c);
+}
+
+// host copy of the 14 reference geometry fields (terrain.hpp:59-63 order), on demand
+void ensure_geo_h(tp_ctx* c) {
+    if (!c->geo_h.empty()) return;
+    const size_t n = static_cast<size_t>(c->nx) * c->ny;
+    c->geo_h.resize(14 * n);
+    const int map[14] = {tpb::G_NX, tpb::G_NY, tpb::G_NZ, tpb::G_JB, tpb::G_A11, tpb::G_A12, tpb::G_A21,
+                         tpb::G_A22, tpb::G_DNX_DXI, tpb::G_DNY_DXI, tpb::G_DNZ_DXI, tpb::G_DNX_DETA,
+                         tpb::G_DNY_DETA, tpb::G_DNZ_DETA};
+    for (int k = 0; k < 14; ++k)
+        ck(cudaMemcpy2DAsync(c->geo_h.data() + k * n, c->nx * sizeof(double), c->dGeo + map[k] * c->fs,
+                             c->pitch * sizeof(double), c->nx * sizeof(double), c->ny, cudaMemcpyDeviceToHost,
+                             c->stream),
+           "geometry D2H");
+    ck(cudaStreamSynchronize(c->stream), "sync");
 }
 
 void create_impl(tp_ctx* c, const tp_params* p, const tp_dem* dem, int row0, int row1) {
@@ -693,26 +730,18 @@ void create_impl(tp_ctx* c, const tp_params* p, const tp_dem* dem, int row0, int
         ck(tpb::build_geometry_device(dem->z, dem->ncols, dem->nrows, p->L, dem->cellsize, row0, c->ny, c->g,
                                       c->dGeo, c->stream),
            "device geometry");
-        // host copy of the 14 reference fields (terrain.hpp:59-63 order) for the host-side
-        // initial conditions, error texts and tp_get_geometry
-        const size_t n = static_cast<size_t>(c->nx) * c->ny;
-        c->geo_h.resize(14 * n);
-        const int map[14] = {tpb::G_NX, tpb::G_NY, tpb::G_NZ, tpb::G_JB, tpb::G_A11, tpb::G_A12, tpb::G_A21,
-                             tpb::G_A22, tpb::G_DNX_DXI, tpb::G_DNY_DXI, tpb::G_DNZ_DXI, tpb::G_DNX_DETA,
-                             tpb::G_DNY_DETA, tpb::G_DNZ_DETA};
-        for (int k = 0; k < 14; ++k)
-            ck(cudaMemcpy2DAsync(c->geo_h.data() + k * n, c->nx * sizeof(double), c->dGeo + map[k] * c->fs,
-                                 c->pitch * sizeof(double), c->nx * sizeof(double), c->ny, cudaMemcpyDeviceToHost,
-                                 c->stream),
-               "geometry D2H");
+        // the geometry part of the safe-tile conditions, checked on the device; the host
+        // copy of the fields (geo_h) is only downloaded when asked for (ensure_geo_h)
+        int* dok = nullptr;
+        int ok = 1;
+        ck(cudaMalloc(&dok, sizeof(int)), "cudaMalloc");
+        ck(cudaMemcpyAsync(dok, &ok, sizeof(int), cudaMemcpyHostToDevice, c->stream), "H2D");
+        ck(tpb::launch_geo_check(c->g, c->dGeo, dok, c->stream), "geo_check_kernel");
+        ck(cudaMemcpyAsync(&ok, dok, sizeof(int), cudaMemcpyDeviceToHost, c->stream), "D2H");
         ck(cudaStreamSynchronize(c->stream), "sync");
-        c->geo_safe = true;
-        c->geo_safe2 = true;
-        for (size_t k = 0; k < n && c->geo_safe; ++k) {
-            const double jb = c->geo_h[3 * n + k];
-            c->geo_safe = jb >= 1.0 && jb <= 0x1p100;
-        }
-        geo_window_b(c, n);
+        cudaFree(dok);
+        c->geo_safe = ok != 0;
+        c->geo_safe2 = ok != 0 && consts_window_b(c);
     }
     // the maps cover the pad column too (x coordinate = logical column + 1)
     c->tmA = make_box_map(c->rawA, c->nx + 1, c->ny, c->pitch, c->fs, 6);
@@ -833,55 +862,45 @@ int tp_set_option(tp_ctx* c, const char* key, long value) {
 
 int tp_set_initial_thickness(tp_ctx* c, const double* h_m) {
     TP_GUARD(c, {
-        // Simulator::set_initial_thickness (solver.cpp:35-57)
-        std::vector<double> s = host_state(c);
-        const double phi = c->p.phi_s0;
-        const size_t n = static_cast<size_t>(c->nx) * c->ny;
-        const double* jbf = c->geo_h.data() + 3 * n;
-        for (int j = 0; j < c->nrows_g; ++j) {
-            for (int i = 0; i < c->ncols; ++i) {
-                double h = h_m[static_cast<size_t>(j) * c->ncols + i];
-                if (h < 0.0)
-                    throw ConfigErr{"initial state: negative thickness at column " + std::to_string(i) +
-                                    ", row " + std::to_string(j)};
-                if (j < c->row0 || j >= c->row1) continue;
-                double h_scaled = h / c->p.H;
-                const size_t k = static_cast<size_t>(j - c->row0 + kGhost) * c->nx + (i + kGhost);
-                double jb = jbf[k];
-                s[0 * n + k] = jb * h_scaled * phi;
-                s[1 * n + k] = jb * h_scaled * (1.0 - phi);
-                s[2 * n + k] = 0.0;
-                s[3 * n + k] = 0.0;
-                s[4 * n + k] = 0.0;
-                s[5 * n + k] = 0.0;
-            }
-        }
-        set_host_state(c, s);
+        // Simulator::set_initial_thickness (solver.cpp:35-57): the whole-grid check on the
+        // host (first offender in row-major order, the reference's message), then this
+        // slab's rows on the device (init_thickness_kernel)
+        const size_t total = static_cast<size_t>(c->ncols) * c->nrows_g;
+        for (size_t q = 0; q < total; ++q)
+            if (h_m[q] < 0.0)
+                throw ConfigErr{"initial state: negative thickness at column " + std::to_string(q % c->ncols) +
+                                ", row " + std::to_string(q / c->ncols)};
+        sync_ghosts(c);
+        double* d = dense_staging(c);
+        const size_t m = static_cast<size_t>(c->ncols) * c->nrows;
+        ck(cudaMemcpyAsync(d, h_m + static_cast<size_t>(c->row0) * c->ncols, sizeof(double) * m,
+                           cudaMemcpyHostToDevice, c->stream),
+           "thickness H2D");
+        ck(tpb::launch_init_thickness(c->g, c->dGeo, d, c->ncols, c->nrows, c->p.H, c->p.phi_s0, c->dA, c->stream),
+           "init_thickness_kernel");
+        invalidate_flags(c, true, false);
+        ck(cudaStreamSynchronize(c->stream), "sync");
+        c->lam_valid = false;
+        c->ghosts_in_B = false;
     })
 }
 
 int tp_set_initial_velocity(tp_ctx* c, const double* vx, const double* vy) {
     TP_GUARD(c, {
-        // Simulator::set_initial_velocity (solver.cpp:59-76)
-        std::vector<double> s = host_state(c);
-        const size_t n = static_cast<size_t>(c->nx) * c->ny;
-        const double* jbf = c->geo_h.data() + 3 * n;
-        const double vu = std::sqrt(c->p.g * c->p.L);
-        for (int j = c->row0; j < c->row1; ++j) {
-            for (int i = 0; i < c->ncols; ++i) {
-                const size_t k = static_cast<size_t>(j - c->row0 + kGhost) * c->nx + (i + kGhost);
-                double jb = jbf[k];
-                double hs = s[0 * n + k] / jb;
-                double hf = s[1 * n + k] / jb;
-                const size_t q = static_cast<size_t>(j) * c->ncols + i;
-                double ux = vx[q] / vu, uy = vy[q] / vu;
-                s[2 * n + k] = jb * hs * ux;
-                s[3 * n + k] = jb * hs * uy;
-                s[4 * n + k] = jb * hf * ux;
-                s[5 * n + k] = jb * hf * uy;
-            }
-        }
-        set_host_state(c, s);
+        // Simulator::set_initial_velocity (solver.cpp:59-76) on the device
+        sync_ghosts(c);
+        double* d = dense_staging(c);  // 6*ny*nx >= 2*nrows*ncols
+        const size_t m = static_cast<size_t>(c->ncols) * c->nrows;
+        const size_t off = static_cast<size_t>(c->row0) * c->ncols;
+        ck(cudaMemcpyAsync(d, vx + off, sizeof(double) * m, cudaMemcpyHostToDevice, c->stream), "vx H2D");
+        ck(cudaMemcpyAsync(d + m, vy + off, sizeof(double) * m, cudaMemcpyHostToDevice, c->stream), "vy H2D");
+        ck(tpb::launch_init_velocity(c->g, c->dGeo, d, d + m, c->ncols, c->nrows, std::sqrt(c->p.g * c->p.L), c->dA,
+                                     c->stream),
+           "init_velocity_kernel");
+        invalidate_flags(c, true, false);
+        ck(cudaStreamSynchronize(c->stream), "sync");
+        c->lam_valid = false;
+        c->ghosts_in_B = false;
     })
 }
 
@@ -979,7 +998,10 @@ int tp_set_state(tp_ctx* c, const double* in) {
 }
 
 int tp_get_geometry(tp_ctx* c, double* out) {
-    TP_GUARD(c, std::memcpy(out, c->geo_h.data(), sizeof(double) * c->geo_h.size()))
+    TP_GUARD(c, {
+        ensure_geo_h(c);
+        std::memcpy(out, c->geo_h.data(), sizeof(double) * c->geo_h.size());
+    })
 }
 
 int tp_apply_boundaries(tp_ctx* c, double t_scaled) {

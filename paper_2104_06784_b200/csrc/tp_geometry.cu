@@ -182,4 +182,89 @@ cudaError_t build_geometry_device(const double* dem_h, int ncols, int nrows, dou
     return e;
 }
 
+// ---- setup kernels on the device layout ------------------------------------------
+
+// Simulator::set_initial_thickness (solver.cpp:35-57) on the slab's interior cells; h is
+// the slab's rows of the thickness grid (dense ncols x nrows, metres).
+__global__ void init_thickness_kernel(GridDesc g, const double* __restrict__ geo, const double* __restrict__ h,
+                                      int ncols, int nrows, double H, double phi, double* s) {
+    const long long n = static_cast<long long>(ncols) * nrows;
+    for (long long q = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; q < n;
+         q += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const int j = static_cast<int>(q / ncols), i = static_cast<int>(q - static_cast<long long>(j) * ncols);
+        const long long k = static_cast<long long>(j + 3) * g.pitch + (i + 3);
+        const double jb = geo[G_JB * g.fs + k];
+        const double h_scaled = h[q] / H;
+        s[0 * g.fs + k] = jb * h_scaled * phi;
+        s[1 * g.fs + k] = jb * h_scaled * (1.0 - phi);
+        s[2 * g.fs + k] = 0.0;
+        s[3 * g.fs + k] = 0.0;
+        s[4 * g.fs + k] = 0.0;
+        s[5 * g.fs + k] = 0.0;
+    }
+}
+
+// Simulator::set_initial_velocity (solver.cpp:59-76) on the slab's interior cells.
+__global__ void init_velocity_kernel(GridDesc g, const double* __restrict__ geo, const double* __restrict__ vx,
+                                     const double* __restrict__ vy, int ncols, int nrows, double vu, double* s) {
+    const long long n = static_cast<long long>(ncols) * nrows;
+    for (long long q = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; q < n;
+         q += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const int j = static_cast<int>(q / ncols), i = static_cast<int>(q - static_cast<long long>(j) * ncols);
+        const long long k = static_cast<long long>(j + 3) * g.pitch + (i + 3);
+        const double jb = geo[G_JB * g.fs + k];
+        const double hs = s[0 * g.fs + k] / jb;
+        const double hf = s[1 * g.fs + k] / jb;
+        const double ux = vx[q] / vu, uy = vy[q] / vu;
+        s[2 * g.fs + k] = jb * hs * ux;
+        s[3 * g.fs + k] = jb * hs * uy;
+        s[4 * g.fs + k] = jb * hf * ux;
+        s[5 * g.fs + k] = jb * hf * uy;
+    }
+}
+
+// The geometry part of the safe-tile conditions (DESIGN.md §3 item 6): all 14 reference
+// fields finite; jb in [1, 2^50] (so nZ = 1/jb >= 2^-50); the metric coefficients a_ij 0 or
+// of magnitude in [2^-128, 2^50]; nX, nY 0 or of magnitude >= 2^-200.  (The normal
+// derivatives only enter curvature terms, never a numerator.)  *ok starts at 1 and is
+// cleared by any violation.
+__global__ void geo_check_kernel(GridDesc g, const double* __restrict__ geo, int* ok) {
+    const long long n = static_cast<long long>(g.ny) * g.nx;
+    bool good = true;
+    auto mag = [](double v, double lo, double hi) {
+        const double a = fabs(v);
+        return a == 0.0 || (a >= lo && a <= hi);  // NaN fails both
+    };
+    for (long long q = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; q < n;
+         q += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const int j = static_cast<int>(q / g.nx), i = static_cast<int>(q - static_cast<long long>(j) * g.nx);
+        const long long k = static_cast<long long>(j) * g.pitch + i;
+        const double jb = geo[G_JB * g.fs + k];
+        good = good && jb >= 1.0 && jb <= 0x1p50;
+        good = good && mag(geo[G_A11 * g.fs + k], 0x1p-120, 0x1p50) && mag(geo[G_A12 * g.fs + k], 0x1p-120, 0x1p50) &&
+               mag(geo[G_A21 * g.fs + k], 0x1p-120, 0x1p50) && mag(geo[G_A22 * g.fs + k], 0x1p-120, 0x1p50);
+        good = good && mag(geo[G_NX * g.fs + k], 0x1p-200, 1.0) && mag(geo[G_NY * g.fs + k], 0x1p-200, 1.0);
+        good = good && isfinite(geo[G_NZ * g.fs + k]) && isfinite(geo[G_DNX_DXI * g.fs + k]) &&
+               isfinite(geo[G_DNY_DXI * g.fs + k]) && isfinite(geo[G_DNZ_DXI * g.fs + k]) &&
+               isfinite(geo[G_DNX_DETA * g.fs + k]) && isfinite(geo[G_DNY_DETA * g.fs + k]) &&
+               isfinite(geo[G_DNZ_DETA * g.fs + k]);
+    }
+    if (!__all_sync(0xffffffffu, good) && (threadIdx.x & 31) == 0) atomicAnd(ok, 0);
+}
+
+cudaError_t launch_init_thickness(const GridDesc& g, const double* geo, const double* h, int ncols, int nrows,
+                                  double H, double phi, double* s, cudaStream_t st) {
+    init_thickness_kernel<<<1184, 256, 0, st>>>(g, geo, h, ncols, nrows, H, phi, s);
+    return cudaGetLastError();
+}
+cudaError_t launch_init_velocity(const GridDesc& g, const double* geo, const double* vx, const double* vy,
+                                 int ncols, int nrows, double vu, double* s, cudaStream_t st) {
+    init_velocity_kernel<<<1184, 256, 0, st>>>(g, geo, vx, vy, ncols, nrows, vu, s);
+    return cudaGetLastError();
+}
+cudaError_t launch_geo_check(const GridDesc& g, const double* geo, int* ok, cudaStream_t st) {
+    geo_check_kernel<<<592, 256, 0, st>>>(g, geo, ok);
+    return cudaGetLastError();
+}
+
 }  // namespace tpb
