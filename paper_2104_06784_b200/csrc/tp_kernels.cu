@@ -983,40 +983,49 @@ __device__ __forceinline__ int ring_tile(int ntx, int nty, int r) {
 __global__ void __launch_bounds__(NT) post_kernel(PostArgs a) {
     DevScalars* sc = a.sc;
     if (a.loop && sc->done) return;
-    __shared__ double red[4][NT];
+    // both stages' 4 tallies per ring tile: per-thread sums, warp shuffles, then the 8 warp
+    // partials in warp order (deterministic)
+    __shared__ double red[NT / 32][8];
     const int nring = ring_tile_count(a.ntx, a.nty);
-    for (int stage = 0; stage < 2; ++stage) {
-        const double* tal = stage == 0 ? a.tally_pred : a.tally_corr;
-        double acc[4] = {0.0, 0.0, 0.0, 0.0};
-        for (int r = threadIdx.x; r < nring; r += NT) {
-            const double* t = tal + 4ll * ring_tile(a.ntx, a.nty, r);
+    double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    for (int r = threadIdx.x; r < nring; r += NT) {
+        const long long o = 4ll * ring_tile(a.ntx, a.nty, r);
 #pragma unroll
-            for (int q = 0; q < 4; ++q) acc[q] += t[q];
+        for (int q = 0; q < 4; ++q) {
+            acc[q] += a.tally_pred[o + q];
+            acc[4 + q] += a.tally_corr[o + q];
         }
-#pragma unroll
-        for (int q = 0; q < 4; ++q) red[q][threadIdx.x] = acc[q];
-        __syncthreads();
-        for (int w = NT / 2; w > 0; w >>= 1) {
-            if (threadIdx.x < w)
-#pragma unroll
-                for (int q = 0; q < 4; ++q) red[q][threadIdx.x] += red[q][threadIdx.x + w];
-            __syncthreads();
-        }
-        if (threadIdx.x == 0) {
-            sc->audit[2] += red[0][0];  // solid injected
-            sc->audit[3] += red[1][0];  // solid outflow
-            sc->audit[7] += red[2][0];  // fluid injected
-            sc->audit[8] += red[3][0];  // fluid outflow
-        }
-        __syncthreads();
     }
-    if (threadIdx.x == 0 && a.loop) {
-        const double dt = sc->dt;
-        if (sc->dts) sc->dts[sc->steps] = dt;
-        sc->steps += 1;
-        sc->t = sc->hit ? sc->t_next : sc->t + dt;
-        sc->lam_cur = sc->lam_bits;
-        if (sc->err_key != kNoError || sc->hit || sc->steps >= sc->max_steps) sc->done = 1;
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) acc[q] += __shfl_down_sync(0xffffffffu, acc[q], d);
+    if ((threadIdx.x & 31) == 0)
+#pragma unroll
+        for (int q = 0; q < 8; ++q) red[threadIdx.x >> 5][q] = acc[q];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double tot[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            tot[q] = 0.0;
+            for (int w = 0; w < NT / 32; ++w) tot[q] += red[w][q];
+        }
+        // predictor then corrector, as the reference's two accumulate_boundary_fluxes calls
+        for (int st = 0; st < 2; ++st) {
+            sc->audit[2] += tot[4 * st + 0];  // solid injected
+            sc->audit[3] += tot[4 * st + 1];  // solid outflow
+            sc->audit[7] += tot[4 * st + 2];  // fluid injected
+            sc->audit[8] += tot[4 * st + 3];  // fluid outflow
+        }
+        if (a.loop) {
+            const double dt = sc->dt;
+            if (sc->dts) sc->dts[sc->steps] = dt;
+            sc->steps += 1;
+            sc->t = sc->hit ? sc->t_next : sc->t + dt;
+            sc->lam_cur = sc->lam_bits;
+            if (sc->err_key != kNoError || sc->hit || sc->steps >= sc->max_steps) sc->done = 1;
+        }
     }
 }
 
