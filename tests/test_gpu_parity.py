@@ -276,3 +276,50 @@ def test_full_tile_list_bitwise(gpu, oracle_kind, make):
     assert_bitwise(dts_g, dts_r, "dt sequence")
     assert_bitwise(sim.state(), ref.state(), "full-list state")
     np.testing.assert_allclose(sim.audit_array(), ref.audit(), rtol=1e-12, atol=1e-300)
+
+
+@pytest.mark.parametrize("seed", list(range(1, 9)))
+def test_random_api_sequences(gpu, oracle_kind, seed):
+    """Random interleavings of the public API (device loop, step pieces, regularize,
+    state uploads that wet, dry out, zero or shrink regions) stay bit-identical to the
+    reference: exercises the tile flags, the dry-tile lists and the safe-tile window
+    across every path that writes a state buffer."""
+    rng = np.random.default_rng(seed)
+    sc = scenarios.wet_valley(72, 60) if seed % 2 else scenarios.c1_hill(64)
+    ref, sim = _pair(sc, oracle_kind)
+    t = 0.0
+    for _ in range(12):
+        op = rng.choice(["loop", "pieces", "perturb", "regularize"])
+        if op == "loop":
+            k = int(rng.integers(1, 15))
+            t_r, _, _ = ref.steps(t, 1.0e9, k, t_end=1.0e9)
+            t_g, _, _ = sim.steps(t, 1.0e9, k, t_end=1.0e9)
+            assert t_r == t_g
+            t = t_r
+        elif op == "pieces":
+            ref.apply_boundaries(t)
+            sim.apply_boundaries(t)
+            dt_r, dt_g = ref.compute_dt(t, 1.0e9), sim.compute_dt(t, 1.0e9)
+            assert dt_r == dt_g
+            ref.advance_step(dt_r, t)
+            sim.advance_step(dt_g, t)
+            t = t + dt_r
+        elif op == "perturb":
+            s = ref.state()
+            j0, i0 = int(rng.integers(3, s.shape[1] - 20)), int(rng.integers(3, s.shape[2] - 20))
+            blk = (slice(None), slice(j0, j0 + 17), slice(i0, i0 + 17))
+            kind = rng.integers(0, 4)
+            if kind == 0:
+                s[blk] = 0.0                                        # dry out a block
+            elif kind == 1:
+                s[0:2][:, blk[1], blk[2]] += rng.uniform(0.0, 0.3, (2, 17, 17))  # wet it
+            elif kind == 2:
+                s[blk] *= 2.0 ** -110                               # below the safe window
+            else:
+                s[2:][:, blk[1], blk[2]] = -s[2:][:, blk[1], blk[2]]  # reverse the flow
+            ref.set_state(s)
+            sim.set_state(s)
+        else:
+            ref.regularize()
+            sim.regularize()
+        assert_bitwise(sim.state(), ref.state(), f"state after {op}")
