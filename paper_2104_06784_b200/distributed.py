@@ -321,8 +321,15 @@ def bench_main(args, metric: str, clock_sampler=None) -> None:
         dist.init_process_group("nccl" if ndev >= world else "gloo",
                                 **({"device_id": torch.device(f"cuda:{dev}")} if ndev >= world else {}))
     rows_per = args.nrows
-    sc = scenarios.SCENARIOS[args.config](args.ncols, rows_per * world) if args.config != "c1" \
-        else scenarios.c1_hill(args.ncols)
+    # weak scaling: every rank's slab is one copy of the single-GPU workload (the N=1 line's
+    # config), stacked along the rows; Mode-II (C3) stretches the channel instead
+    if args.config == "c1":
+        base = scenarios.c1_hill(args.ncols)
+    elif args.config == "c3":
+        base = scenarios.SCENARIOS["c3"](args.ncols, rows_per * world)
+    else:
+        base = scenarios.SCENARIOS[args.config](args.ncols, rows_per)
+    sc = base if args.config == "c3" else scenarios.stacked(base, world)
     rows = decompose(sc.nrows, world)[rank]
     stream = torch.cuda.Stream()
     slab = CudaSlab(sc, rows, device=dev, stream=stream)
@@ -381,8 +388,9 @@ def bench_main(args, metric: str, clock_sampler=None) -> None:
                "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 5),
                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
                "data": f"synthetic (deterministic {sc.name} generator in scenarios.py; no network data)",
-               "config": {"workload": f"{sc.name} {sc.ncols}x{sc.nrows} (weak: {rows_per} rows x {args.ncols} "
-                                      f"per GPU), row-block slabs joined by the device-resident exchange "
+               "config": {"workload": f"{sc.name} {sc.ncols}x{sc.nrows} (weak: one {args.ncols}x{rows_per} "
+                                      f"copy of the single-GPU workload per GPU, stacked along the rows), "
+                                      f"row-block slabs joined by the device-resident exchange "
                                       f"(halo rows stored into the neighbour's buffers over peer memory, "
                                       f"lambda all-reduce in device memory; tp_peer.cu)",
                           "grid": [sc.ncols, sc.nrows], "parallelism": f"slab{world}",

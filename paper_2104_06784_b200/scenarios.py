@@ -204,6 +204,17 @@ def wet_valley(ncols, nrows, t_end=1.0e4, dt_out=1.0e4) -> Scenario:
     return s
 
 
+def stacked(sc: Scenario, copies: int) -> Scenario:
+    """`copies` copies of a Mode-I scenario stacked along the rows (weak scaling: one copy per
+    row slab, so every GPU carries the single-GPU workload; the copies couple through the
+    shared rows at the seams).  Mode-II hydrographs are not stacked."""
+    if sc.hydrograph is not None:
+        raise ValueError("stacked: Mode-II scenarios are not supported")
+    tile = lambda a: None if a is None else np.ascontiguousarray(np.tile(a, (copies, 1)))  # noqa: E731
+    return Scenario(f"{sc.name}x{copies}", tile(sc.z), sc.cellsize, sc.config, h0=tile(sc.h0),
+                    vx0=tile(sc.vx0), vy0=tile(sc.vy0), xll=sc.xll, yll=sc.yll)
+
+
 SCENARIOS = {
     "c1": c1_hill,
     "c2": c2_valley,
