@@ -336,3 +336,23 @@ def test_small_and_ragged_grids(gpu, oracle_kind, shape):
     tg, dts_g, _ = sim.steps(0.0, 1.0e9, 25, t_end=1.0e9, record_dts=True)
     assert_bitwise(dts_g, dts_r, "dt sequence")
     assert_bitwise(sim.state(), ref.state(), f"state {ncols}x{nrows}")
+
+
+def test_config0_c1_1000_steps(gpu, oracle_kind):
+    """BASELINE configs[0] end to end: the 256^2 hill release for 1000 steps, every dt and
+    the final state bit-identical to the reference (plus the north-star 1e-9 gate)."""
+    sc = scenarios.c1_hill(256)
+    ref, sim = _pair(sc, oracle_kind)
+    tr, dts_r, _ = ref.steps(0.0, 1.0e9, 1000, t_end=1.0e9)
+    tg, dts_g, _ = sim.steps(0.0, 1.0e9, 1000, t_end=1.0e9, record_dts=True)
+    assert len(dts_r) == 1000
+    assert_bitwise(dts_g, dts_r, "1000 dts")
+    assert tg == tr
+    g, r = sim.state(), ref.state()
+    assert_bitwise(g, r, "state after 1000 steps")
+    for f in range(6):
+        l1, linf = rel_err(g[f], r[f])
+        assert l1 <= 1e-9 and linf <= 1e-9
+    ms_r, mf_r = ref.interior_mass()
+    ms_g, mf_g = sim.interior_mass()
+    assert (ms_g, mf_g) == (ms_r, mf_r)
