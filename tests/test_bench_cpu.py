@@ -1,0 +1,55 @@
+"""Host logic of bench.py and the weak-scaling workload, no GPU needed."""
+import numpy as np
+
+import bench
+from paper_2104_06784_b200 import scenarios
+
+
+class _FakeSim:
+    """Steps of fixed dt toward t_next with exact hits, like tp_steps (solver.cpp:637-649)."""
+
+    class _Cfg:
+        class scaling:
+            @staticmethod
+            def t_unit():
+                return 1.0
+        t_end = 10.0
+        dt_out = 1.0
+
+    def __init__(self, dt):
+        self.cfg = self._Cfg()
+        self.dt = dt
+        self.calls = []
+
+    def steps(self, t, t_next, k, t_end=None):
+        self.calls.append((t, t_next, k))
+        n, hit = 0, False
+        while n < k and t < t_end:
+            dt = min(self.dt, t_next - t)
+            hit = dt == t_next - t
+            t = t_next if hit else t + dt
+            n += 1
+            if hit:
+                break
+        return t, n, hit
+
+
+def test_runclock_follows_output_schedule():
+    sim = _FakeSim(0.3)
+    clock = bench.RunClock(sim)
+    assert clock.advance(7) == 7
+    # 0.3, 0.6, 0.9, hit at 1.0 (next_out -> 2.0), 1.3, 1.6, 1.9
+    assert abs(clock.t - 1.9) < 1e-12
+    assert clock.next_out == 2.0
+    assert sim.calls[0][1] == 1.0 and sim.calls[1][1] == 2.0
+    # stops at t_end
+    assert clock.advance(1000) < 1000 and clock.t == 10.0
+
+
+def test_stacked_scenario_copies_rows():
+    base = scenarios.c2_valley(40, 24)
+    st = scenarios.stacked(base, 3)
+    assert st.z.shape == (72, 40) and st.h0.shape == (72, 40)
+    for k in range(3):
+        np.testing.assert_array_equal(st.z[24 * k:24 * (k + 1)], base.z)
+        np.testing.assert_array_equal(st.h0[24 * k:24 * (k + 1)], base.h0)
