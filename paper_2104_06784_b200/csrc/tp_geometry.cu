@@ -164,19 +164,20 @@ cudaError_t build_geometry_device(const double* dem_h, int ncols, int nrows, dou
     const int g0 = row0 - 2 < 0 ? 0 : row0 - 2;
     const int g1 = row0 + ny + 2 > NY ? NY : row0 + ny + 2;
     double *d_dem = nullptr, *d_z = nullptr, *d_p1 = nullptr;
-    cudaError_t e;
     const size_t dem_b = sizeof(double) * static_cast<size_t>(ncols) * nrows;
-    if ((e = cudaMalloc(&d_dem, dem_b)) != cudaSuccess) return e;
-    if ((e = cudaMalloc(&d_z, sizeof(double) * static_cast<size_t>(NX) * NY)) != cudaSuccess) return e;
-    if ((e = cudaMalloc(&d_p1, sizeof(double) * 8ull * (g1 - g0) * NX)) != cudaSuccess) return e;
-    if ((e = cudaMemcpyAsync(d_dem, dem_h, dem_b, cudaMemcpyHostToDevice, st)) != cudaSuccess) return e;
-    geo_extend_we_kernel<<<1184, 256, 0, st>>>(d_dem, ncols, nrows, d_z);
-    geo_extend_ns_kernel<<<64, 256, 0, st>>>(ncols, nrows, d_z);
-    geo_pass1_kernel<<<1184, 256, 0, st>>>(Ext{d_z, NX, NY}, L, dxi, deta, g0, g1, d_p1);
-    geo_pass2_kernel<<<1184, 256, 0, st>>>(d_p1, NX, NY, g0, g1, row0, ny, dxi, deta, g, geo);
-    e = cudaGetLastError();
+    cudaError_t e = cudaMalloc(&d_dem, dem_b);
+    if (e == cudaSuccess) e = cudaMalloc(&d_z, sizeof(double) * static_cast<size_t>(NX) * NY);
+    if (e == cudaSuccess) e = cudaMalloc(&d_p1, sizeof(double) * 8ull * (g1 - g0) * NX);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d_dem, dem_h, dem_b, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) {
+        geo_extend_we_kernel<<<1184, 256, 0, st>>>(d_dem, ncols, nrows, d_z);
+        geo_extend_ns_kernel<<<64, 256, 0, st>>>(ncols, nrows, d_z);
+        geo_pass1_kernel<<<1184, 256, 0, st>>>(Ext{d_z, NX, NY}, L, dxi, deta, g0, g1, d_p1);
+        geo_pass2_kernel<<<1184, 256, 0, st>>>(d_p1, NX, NY, g0, g1, row0, ny, dxi, deta, g, geo);
+        e = cudaGetLastError();
+    }
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-    cudaFree(d_dem);
+    cudaFree(d_dem);  // null-safe
     cudaFree(d_z);
     cudaFree(d_p1);
     return e;
