@@ -356,3 +356,38 @@ def test_config0_c1_1000_steps(gpu, oracle_kind):
     ms_r, mf_r = ref.interior_mass()
     ms_g, mf_g = sim.interior_mass()
     assert (ms_g, mf_g) == (ms_r, mf_r)
+
+
+@pytest.mark.parametrize("case", ["negative", "nonfinite"])
+def test_step_errors_match(gpu, oracle_kind, case):
+    """NumericsError raised inside a step (regularize after the predictor/corrector,
+    solver.cpp:147-152; check_finite, :482-494): same message as the reference, through
+    the device loop and through the step API."""
+    from oracle.oracle import OracleError
+    sc = scenarios.c1_hill(48)
+    for api in ("loop", "pieces"):
+        ref, sim = _pair(sc, oracle_kind)
+        s = ref.state()
+        if case == "negative":
+            # negative thickness in a dry corner: it survives the predictor and its regularize throws
+            s[0, 8, 9] = -1e-6
+            s[1, 40, 10] = -3e-6
+        else:
+            # non-finite values inside the release (regularize would zero momenta of dry cells)
+            s[0, 27, 37] = np.inf
+            s[2, 26, 36] = np.nan
+        ref.set_state(s)
+        sim.set_state(s)
+        with pytest.raises(OracleError) as er:
+            if api == "loop":
+                ref.steps(0.0, 1.0e9, 5, t_end=1.0e9)
+            else:
+                ref.apply_boundaries(0.0)
+                ref.advance_step(ref.compute_dt(0.0, 1.0e9), 0.0)
+        with pytest.raises(NumericsError) as eg:
+            if api == "loop":
+                sim.steps(0.0, 1.0e9, 5, t_end=1.0e9)
+            else:
+                sim.apply_boundaries(0.0)
+                sim.advance_step(sim.compute_dt(0.0, 1.0e9), 0.0)
+        assert str(eg.value) == str(er.value), api
