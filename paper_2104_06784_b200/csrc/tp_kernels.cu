@@ -355,8 +355,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
 
     // ---- Phase 2: (a) the cell-local source terms of this thread's Phase-3 cell
     // (solver.cpp:406-445 minus the viscous divergence, which needs neighbours'
-    // brackets) and (b) the viscous brackets of the tile's cross neighbours, spread
-    // so that the 16 threads without a cell take the 62 extra brackets.
+    // brackets) and (b) the viscous brackets of the tile's cross neighbours.
     const Rcp r2x = mkrcp_const<FD>(P.two_dxi, P.r_two_dxi);
     const Rcp r2y = mkrcp_const<FD>(P.two_deta, P.r_two_deta);
     // partial rhs sums in the reference's order: rhs[2] = div + ((sn + sf) + sv),
@@ -454,9 +453,10 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
         if (!P.adv_only) {
             constexpr int NB1 = (TX + 2) * TY;  // rows 2..TY+1, cols 1..TX+2
             constexpr int NB = NB1 + 2 * TX;    // + rows 1 and TY+2, cols 2..TX+1
-            // threads with a Phase-3 cell: one bracket each; the rest stride over the remainder
-            const int stride = threadIdx.x < TX * TY ? NB : NT - TX * TY;
-            for (int it = threadIdx.x; it < NB; it += stride) {
+            // one bracket per thread (the 16 threads without a Phase-3 cell included), the
+            // NB - NT remaining ones on the first warps: every warp costs sources + 1 bracket
+            // pass and only two warps a second pass (a warp's cost is per pass, not per lane)
+            for (int it = threadIdx.x; it < NB; it += NT) {
                 int bx, by;
                 if (it < NB1) {
                     bx = 1 + it % (TX + 2);
