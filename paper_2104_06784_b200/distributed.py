@@ -301,6 +301,24 @@ def assemble(states: Sequence[np.ndarray]) -> np.ndarray:
 # ---------------------------------------------------------------------------
 # bench.py --gpus N (torchrun): weak scaling, one slab per rank, device-resident exchange
 # ---------------------------------------------------------------------------
+def _slab_roofline(cells: int, world: int, steps: int, ms: float) -> dict:
+    """Per-GPU HBM roofline of a slab run: 464 algorithmic bytes per cell-update
+     of this GPU's share of the cells over the step time (the two stage
+    kernels are >= 96 % of it), against MEASURED_PEAKS.json hbm_gbs."""
+    import json
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    peak, src = 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+    pp = os.path.join(root, "MEASURED_PEAKS.json")
+    if os.path.exists(pp):
+        with open(pp) as f:
+            peak, src = float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    achieved = 464.0 * (cells / world) * steps / (ms / 1e3) / 1e9
+    return {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(achieved / peak, 4), "traffic": None,
+            "kernel": "whole step per GPU (stage_kernel<pred>+stage_kernel<corr> dominate)",
+            "peak_source": src}
+
+
 def bench_main(args, metric: str, clock_sampler=None) -> None:
     """Each rank owns a [rows_per x ncols] slab of one (ncols x rows_per*N) grid of the
     chosen scenario; slabs are joined by the device-resident exchange (tp_peer.cu over
@@ -401,6 +419,7 @@ def bench_main(args, metric: str, clock_sampler=None) -> None:
                "e2e": {"value": round(e2e_v, 4), "unit": "GCUPS", "h2d_bytes_per_step": nbytes // max(ne, 1),
                        "d2h_bytes_per_step": nbytes // max(ne, 1),
                        "mode": f"per rank: tp_set_state(pinned host) + tp_steps({ne}) + tp_get_state, max over ranks"},
+               "roofline": _slab_roofline(cells, world, args.steps, ms),
                "clocks": clocks.summary() if clocks else None,
                "gpu_launches": launches}
         print(json.dumps(out))
