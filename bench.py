@@ -252,7 +252,8 @@ def run_b200(args):
     import ctypes as C
     nbytes = 6 * sim.ny * sim.nx * 8
     h_in = torch.empty(6 * sim.ny * sim.nx, dtype=torch.float64, pin_memory=True)
-    h_out = torch.empty_like(h_in)
+    h_out = torch.empty_like(h_in, pin_memory=True)  # empty_like alone is pageable
+    assert h_in.is_pinned() and h_out.is_pinned()
     sim._check(sim.L.tp_get_state(sim.h, C.cast(h_in.data_ptr(), C.POINTER(C.c_double))))
     # first DMA into a freshly pinned buffer pays ~80 ms of page setup: touch h_out at setup
     sim._check(sim.L.tp_get_state(sim.h, C.cast(h_out.data_ptr(), C.POINTER(C.c_double))))

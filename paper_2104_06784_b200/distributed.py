@@ -386,7 +386,8 @@ def bench_main(args, metric: str, clock_sampler=None) -> None:
     # e2e: the same steps through the C ABI with this rank's state from / to pinned host memory
     nbytes = 6 * sim.ny * sim.nx * 8
     h_in = torch.empty(6 * sim.ny * sim.nx, dtype=torch.float64, pin_memory=True)
-    h_out = torch.empty_like(h_in)
+    h_out = torch.empty_like(h_in, pin_memory=True)  # empty_like alone is pageable
+    assert h_in.is_pinned() and h_out.is_pinned()
     dp = C.POINTER(C.c_double)
     sim._check(sim.L.tp_get_state(sim.h, C.cast(h_in.data_ptr(), dp)))
     sim._check(sim.L.tp_get_state(sim.h, C.cast(h_out.data_ptr(), dp)))
