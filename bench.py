@@ -235,8 +235,12 @@ def run_b200(args):
         ((t_pred + t_corr) / 1e3) / 1e9
     traffic = None
     nt = ncu_traffic()
-    if nt and nt.get("grid") == [sc.ncols, sc.nrows] and nt.get("config") == args.config:
-        traffic = nt["dram_bytes_per_step"]
+    prof = None
+    for cand in (nt, (nt or {}).get("wet")):
+        if cand and cand.get("grid") == [sc.ncols, sc.nrows] and cand.get("config") == args.config:
+            prof = cand
+    if prof:
+        traffic = prof["dram_bytes_per_step"]
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic,
                 "kernel": "stage_kernel<pred>+stage_kernel<corr> per step",
@@ -247,6 +251,13 @@ def run_b200(args):
                 "achieved_processed_tiles": round(achieved_proc, 1),
                 "frac_processed_tiles": round(achieved_proc / peak, 4),
                 "step_frac": round(achieved * (t_pred + t_corr) / (ms / args.steps) / peak, 4)}
+    if prof and prof.get("fp64_pipe_active_pct"):
+        # the processed tiles are FP64-issue bound: the co-bound from the same capture
+        roofline["co_bound"] = {"pipe": "fp64", "fp64_pipe_active_pct": prof["fp64_pipe_active_pct"],
+                                "issue_active_pct": prof["issue_active_pct"],
+                                "dram_throughput_pct": prof["dram_throughput_pct"],
+                                "kernels": ["stage_kernel<pred>", "stage_kernel<corr>"],
+                                "source": nt.get("source")}
 
     # e2e leg: through the C ABI with HOST (pinned) buffers, copies inside the timed region
     import ctypes as C

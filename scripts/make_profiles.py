@@ -34,9 +34,13 @@ for cfg in ("c2", "wet"):
         v = float(g(r, k)); u = units[hdr.index(k)]
         return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[u]
     traffic = sum(tobytes(r, "dram__bytes_read.sum") + tobytes(r, "dram__bytes_write.sum") for r in data)
+    pct = lambda k: [round(float(g(r, k)), 2) for r in data] if k in hdr else None  # noqa: E731
     summary[cfg] = {"config": cfg, "grid": [2048, 2048], "dram_bytes_per_step": traffic,
                     "alg_bytes_per_step": 464 * 2048 * 2048,
-                    "kernels": [g(r, "Kernel Name") for r in data]}
+                    "kernels": [g(r, "Kernel Name") for r in data],
+                    "fp64_pipe_active_pct": pct("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
+                    "issue_active_pct": pct("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                    "dram_throughput_pct": pct("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed")}
     lines.append(f"\nDRAM traffic per step (pred+corr): {traffic/1e6:.1f} MB; algorithmic 464 B x 2048^2 = "
                  f"{464*2048*2048/1e6:.1f} MB (ratio {traffic/(464*2048*2048):.3f}).\n")
 # launch list
