@@ -391,3 +391,44 @@ def test_step_errors_match(gpu, oracle_kind, case):
                 sim.apply_boundaries(0.0)
                 sim.advance_step(sim.compute_dt(0.0, 1.0e9), 0.0)
         assert str(eg.value) == str(er.value), api
+
+
+@pytest.mark.parametrize("seed", list(range(8)))
+def test_random_parameters_bitwise(gpu, oracle_kind, seed):
+    """Non-default model parameters, scaling (ε = H/L ≠ 1, χ ≠ 1), CFL, h_dry and eps_h:
+    every host-hoisted constant (tan δb, ε^χ, 1−α, ε·N_R, ...) and the safe-tile constant
+    window must reproduce the reference's per-cell evaluation bit for bit."""
+    rng = np.random.default_rng(700 + seed)
+    kind = seed % 3
+    if kind == 0:
+        sc = scenarios.c4_terrain(56, 44, seed=2104 + seed)
+    elif kind == 1:
+        sc = scenarios.wet_valley(50, 46)
+    else:
+        sc = scenarios.c3_channel(64, 40, t_end=30.0, dt_out=0.5)
+    p, s, cfg = sc.config.params, sc.config.scaling, sc.config
+    p.delta_b = float(rng.uniform(5.0, 35.0))
+    p.C_d = float(rng.uniform(0.0, 10.0))
+    p.N_R = float(rng.uniform(20.0, 800.0))
+    p.theta_b = float(rng.uniform(0.0, 10.0))
+    p.phi_s0 = float(rng.uniform(0.2, 0.8))
+    p.alpha_rho = float(rng.uniform(0.2, 1.0))
+    p.chi = float(rng.choice([0.5, 1.0, 1.5, 2.0]))
+    s.L = float(rng.choice([1.0, 2.0, 10.0]))
+    s.H = float(rng.choice([0.5, 1.0, 4.0]))
+    cfg.cfl = float(rng.uniform(0.05, 0.125))
+    cfg.h_dry = float(10.0 ** rng.uniform(-12, -7))
+    cfg.eps_h = float(10.0 ** rng.uniform(-8, -4))
+    cfg.validate()
+    ref, sim = _pair(sc, oracle_kind)
+    assert_bitwise(sim.state(), ref.state(), "initial state")
+    tu = s.t_unit()
+    t_r = t_g = 0.0
+    for k in range(1, 4):
+        t_next = k * cfg.dt_out / tu if cfg.inflow else 1e9
+        t_r, dts_r, _ = ref.steps(t_r, t_next, 20, t_end=cfg.t_end / tu)
+        t_g, dts_g, _ = sim.steps(t_g, t_next, 20, t_end=cfg.t_end / tu, record_dts=True)
+        assert_bitwise(dts_g, dts_r, f"dt sequence, leg {k}")
+        assert t_r == t_g
+    assert_bitwise(sim.state(), ref.state(), "state")
+    np.testing.assert_allclose(sim.audit_array(), ref.audit(), rtol=1e-12, atol=1e-300)
