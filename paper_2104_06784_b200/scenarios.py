@@ -215,10 +215,24 @@ def stacked(sc: Scenario, copies: int) -> Scenario:
                     vx0=tile(sc.vx0), vy0=tile(sc.vy0), xll=sc.xll, yll=sc.yll)
 
 
+def moving_release(ncols, nrows, t_end=1.0e4, dt_out=1.0e4, seed=7) -> Scenario:
+    """Mode-I release with an initial velocity field (set_initial_velocity, solver.cpp:57-81):
+    the C4 terrain with a swirling, noisy velocity everywhere (zero-thickness cells included)."""
+    sc = c4_terrain(ncols, nrows, t_end=t_end, dt_out=dt_out, seed=2104 + seed)
+    rng = np.random.default_rng(seed)
+    y, x = np.mgrid[0:nrows, 0:ncols].astype(np.float64)
+    cx, cy = 0.5 * ncols, 0.5 * nrows
+    sc.vx0 = -3.0 * (y - cy) / max(nrows, 1) + rng.normal(0.0, 0.5, (nrows, ncols))
+    sc.vy0 = 3.0 * (x - cx) / max(ncols, 1) + rng.normal(0.0, 0.5, (nrows, ncols))
+    sc.name = "moving-release"
+    return sc
+
+
 SCENARIOS = {
     "c1": c1_hill,
     "c2": c2_valley,
     "c3": c3_channel,
     "c4": c4_terrain,
     "wet": wet_valley,
+    "moving": moving_release,
 }

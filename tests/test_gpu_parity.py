@@ -432,3 +432,17 @@ def test_random_parameters_bitwise(gpu, oracle_kind, seed):
         assert t_r == t_g
     assert_bitwise(sim.state(), ref.state(), "state")
     np.testing.assert_allclose(sim.audit_array(), ref.audit(), rtol=1e-12, atol=1e-300)
+
+
+@pytest.mark.parametrize("shape", [(64, 48), (37, 29)])
+def test_initial_velocity_bitwise(gpu, oracle_kind, shape):
+    """set_initial_velocity (solver.cpp:57-81, init_velocity_kernel on the device): the
+    initial momenta and 40 steps from a moving release are bit-identical."""
+    sc = scenarios.moving_release(*shape)
+    ref, sim = _pair(sc, oracle_kind)
+    assert_bitwise(sim.state(), ref.state(), "initial state with velocity")
+    tr, dts_r, _ = ref.steps(0.0, 1.0e9, 40, t_end=1.0e9)
+    tg, dts_g, _ = sim.steps(0.0, 1.0e9, 40, t_end=1.0e9, record_dts=True)
+    assert_bitwise(dts_g, dts_r, "dt sequence")
+    assert tg == tr
+    assert_bitwise(sim.state(), ref.state(), "state after 40 steps")
