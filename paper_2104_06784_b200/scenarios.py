@@ -228,6 +228,21 @@ def moving_release(ncols, nrows, t_end=1.0e4, dt_out=1.0e4, seed=7) -> Scenario:
     return sc
 
 
+def four_side_inflow(ncols, nrows, t_end=30.0, dt_out=0.5) -> Scenario:
+    """Mode-II inflow through all four sides (solver.cpp:108-136: per-side ghost rows and
+    inward velocity), both cells of the SE corner listed on two sides, a hydrograph that
+    starts wet at t=0 and ends (zero after the last sample) before t_end."""
+    cs = 5.0
+    z = bowl_dem(ncols, nrows, cs, depth=30.0)
+    cells = [(0, j, "W") for j in range(nrows // 4, nrows // 4 + 6)]
+    cells += [(i, nrows - 1, "N") for i in range(ncols // 3, ncols // 3 + 7)]
+    cells += [(i, 0, "S") for i in range(ncols - 5, ncols)]
+    cells += [(ncols - 1, j, "E") for j in range(0, 4)]
+    samples = [(0.0, 0.5, 0.6, 1.0), (8.0, 3.0, 0.45, 4.0), (20.0, 0.0, 0.5, 0.0)]
+    cfg = SimConfig(mode="inflow", t_end=t_end, dt_out=dt_out)
+    return Scenario("four-side-inflow", z, cs, cfg, hydrograph=Hydrograph(cells=cells, samples=samples))
+
+
 SCENARIOS = {
     "c1": c1_hill,
     "c2": c2_valley,
@@ -235,4 +250,5 @@ SCENARIOS = {
     "c4": c4_terrain,
     "wet": wet_valley,
     "moving": moving_release,
+    "inflow4": four_side_inflow,
 }

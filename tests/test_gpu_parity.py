@@ -446,3 +446,23 @@ def test_initial_velocity_bitwise(gpu, oracle_kind, shape):
     assert_bitwise(dts_g, dts_r, "dt sequence")
     assert tg == tr
     assert_bitwise(sim.state(), ref.state(), "state after 40 steps")
+
+
+def test_four_side_inflow_bitwise(gpu, oracle_kind):
+    """Mode-II inflow on W, N, S and E boundary cells (the SE corner cell on two sides),
+    through and past the end of the hydrograph: dt, state and audit bit-identical."""
+    sc = scenarios.four_side_inflow(48, 40)
+    sc.hydrograph.validate(sc.ncols, sc.nrows)
+    ref, sim = _pair(sc, oracle_kind)
+    tu = sc.config.scaling.t_unit()
+    t_r = t_g = 0.0
+    t_end = sc.config.t_end / tu
+    for k in range(1, 61):
+        t_next = min(k * sc.config.dt_out / tu, t_end)
+        t_r, dts_r, _ = ref.steps(t_r, t_next, 100_000, t_end=t_end)
+        t_g, dts_g, _ = sim.steps(t_g, t_next, 100_000, t_end=t_end, record_dts=True)
+        assert_bitwise(dts_g, dts_r, f"dts interval {k}")
+        assert t_r == t_g
+    assert t_g == t_end
+    assert_bitwise(sim.state(), ref.state(), "four-side inflow state")
+    np.testing.assert_allclose(sim.audit_array(), ref.audit(), rtol=1e-12, atol=1e-300)
