@@ -129,9 +129,11 @@ def test_mode2_channel_inflow(gpu, oracle_kind):
     np.testing.assert_allclose(sim.audit_array(), ref.audit(), rtol=1e-12, atol=1e-300)
 
 
-def test_run_report_matches(gpu, oracle_kind):
-    """Simulator::run end to end: steps, snapshot times, audit (solver.cpp:619-659)."""
-    sc = scenarios.c1_hill(48, t_end=4.0, dt_out=1.0)
+@pytest.mark.parametrize("t_end,dt_out", [(4.0, 1.0), (2.0, 0.7)])
+def test_run_report_matches(gpu, oracle_kind, t_end, dt_out):
+    """Simulator::run end to end: steps, snapshot times (incl. a last output at t_end that is
+    not a multiple of dt_out), audit (solver.cpp:619-659)."""
+    sc = scenarios.c1_hill(48, t_end=t_end, dt_out=dt_out)
     ref, sim = _pair(sc, oracle_kind)
     rep_r, snaps_r = ref.run()
     times = []
@@ -466,3 +468,30 @@ def test_four_side_inflow_bitwise(gpu, oracle_kind):
     assert t_g == t_end
     assert_bitwise(sim.state(), ref.state(), "four-side inflow state")
     np.testing.assert_allclose(sim.audit_array(), ref.audit(), rtol=1e-12, atol=1e-300)
+
+
+def test_regularize_clips_small_negatives(gpu, oracle_kind):
+    """regularize (solver.cpp:139-166): -1e-12 <= hp < 0 is clipped to 0 with its mass in the
+    audit's 'clipped' slot, and the momenta of the now-dry phase are zeroed; then the run
+    continues bit-identically."""
+    sc = scenarios.wet_valley(40, 36)
+    ref, sim = _pair(sc, oracle_kind)
+    s = ref.state()
+    rng = np.random.default_rng(5)
+    for _ in range(30):
+        f, j, i = int(rng.integers(0, 2)), int(rng.integers(3, 39)), int(rng.integers(3, 43))
+        s[f, j, i] = -float(rng.uniform(1e-15, 9e-13))
+    ref.set_state(s)
+    sim.set_state(s)
+    ref.reset_audit()
+    sim.reset_audit()
+    ref.regularize()
+    sim.regularize()
+    assert_bitwise(sim.state(), ref.state(), "after regularize")
+    a_r, a_g = ref.audit(), sim.audit_array()
+    assert a_r[4] != 0.0 and a_r[9] != 0.0
+    np.testing.assert_allclose(a_g, a_r, rtol=1e-12, atol=1e-300)
+    tr, dts_r, _ = ref.steps(0.0, 1.0e9, 20, t_end=1.0e9)
+    tg, dts_g, _ = sim.steps(0.0, 1.0e9, 20, t_end=1.0e9, record_dts=True)
+    assert_bitwise(dts_g, dts_r, "dt sequence")
+    assert_bitwise(sim.state(), ref.state(), "state after 20 steps")
