@@ -113,10 +113,11 @@ class ClockSampler:
                 "reasons": names, "samples": len(self.samples)}
 
 
-def cpu_reference(config, ncols, nrows, steps, lanes, timeout=600):
-    """The reference (oracle/_ref, else the C port) timed on this host, in a child process."""
+def cpu_reference(config, ncols, nrows, steps, lanes, timeout=600, stack=1):
+    """The reference (oracle/_ref, else the C port) timed on this host, in a child process.
+    stack > 1: the weak-scaling grid of `bench.py --gpus stack` (row-stacked copies)."""
     cmd = [sys.executable, "-m", "oracle.cpu_bench", "--config", config, "--ncols", str(ncols),
-           "--nrows", str(nrows), "--steps", str(steps), "--lanes", str(lanes)]
+           "--nrows", str(nrows), "--steps", str(steps), "--lanes", str(lanes), "--stack", str(stack)]
     try:
         out = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=timeout)
         line = [l for l in out.stdout.splitlines() if l.startswith("{")]
@@ -130,7 +131,7 @@ def cpu_reference(config, ncols, nrows, steps, lanes, timeout=600):
     except Exception as e:  # crash of the racy pool (App. B1) -> serial
         err = str(e)
     if lanes > 1:
-        r = cpu_reference(config, ncols, nrows, max(1, steps // 4), 1, timeout)
+        r = cpu_reference(config, ncols, nrows, max(1, steps // 4), 1, timeout, stack)
         r["note"] = f"DataParallel({lanes}) failed ({err.strip()[:120]}); serial backend"
         return r
     raise RuntimeError("CPU reference failed: " + err)
@@ -319,19 +320,27 @@ def run_b200(args):
 
 
 def run_reference(args):
-    """--impl reference: the reference's own CPU implementation on this host's cores."""
+    """--impl reference: the reference's own CPU implementation on this host's cores, on the
+    grid our arm runs at this N (N=1: the config's grid; N>1: the weak-scaling grid of N
+    row-stacked copies, distributed.bench_main).  Under torchrun only rank 0 runs."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    world = max(args.gpus, int(os.environ.get("WORLD_SIZE", "1")))
     sc = scenario_for(args.config, args.ncols, args.nrows)
+    if world > 1:
+        from paper_2104_06784_b200 import scenarios
+        sc = (scenarios.SCENARIOS["c3"](args.ncols, args.nrows * world) if args.config == "c3"
+              else scenarios.stacked(sc, world))
     lanes = os.cpu_count() or 1
     # bounded sample: at most ~2 minutes of CPU work
     steps = args.steps
-    probe = cpu_reference(args.config, sc.ncols, sc.nrows, 1, lanes)
+    probe = cpu_reference(args.config, args.ncols, args.nrows, 1, lanes, stack=world)
     per_step = probe["seconds"] / max(probe["steps"], 1)
     if per_step * steps > 120:
         steps = max(1, int(120 / per_step))
-    c = cpu_reference(args.config, sc.ncols, sc.nrows, steps, lanes)
+    c = cpu_reference(args.config, args.ncols, args.nrows, steps, lanes, stack=world)
+    assert c["grid"] == [sc.ncols, sc.nrows], (c["grid"], sc.ncols, sc.nrows)
     v = round(c["value"] / 1e9, 6)
     cpu = {"value": v, "unit": "GCUPS", "cores": c["lanes"],
            "kind": "reference" if c["kind"] == "ref" else "port",

@@ -29,6 +29,8 @@ def main() -> None:
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--lanes", type=int, default=os.cpu_count() or 1)
     ap.add_argument("--kind", default="auto")
+    ap.add_argument("--stack", type=int, default=1,
+                    help="weak-scaling grid of bench.py --gpus N: N row-stacked copies (C3: N x the rows)")
     ap.add_argument("--check-serial", type=int, default=1,
                     help="steps of a serial run the parallel state must match bitwise (App. B1)")
     a = ap.parse_args()
@@ -42,8 +44,12 @@ def main() -> None:
         kind = "ref" if (orc.available("ref") or os.path.exists(orc.REF_SOURCES)) else "port"
     if a.config == "c1":
         sc = scenarios.c1_hill(a.ncols)
+    elif a.config == "c3":
+        sc = scenarios.SCENARIOS["c3"](a.ncols, a.nrows * a.stack)
     else:
         sc = scenarios.SCENARIOS[a.config](a.ncols, a.nrows)
+    if a.stack > 1 and a.config != "c3":
+        sc = scenarios.stacked(sc, a.stack)
     lanes = max(1, a.lanes)
     t0 = time.perf_counter()
     sim = orc.OracleSim(sc, kind, lanes=lanes if lanes > 1 else 0)

@@ -53,3 +53,24 @@ def test_stacked_scenario_copies_rows():
     for k in range(3):
         np.testing.assert_array_equal(st.z[24 * k:24 * (k + 1)], base.z)
         np.testing.assert_array_equal(st.h0[24 * k:24 * (k + 1)], base.h0)
+
+
+def test_reference_arm_runs_the_weak_scaling_grid():
+    """--impl reference at --gpus N times the reference on the grid our arm runs at N
+    (N row-stacked copies), rank 0 only; one JSON line with the reference keys."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--gpus", "2", "--steps", "2",
+                          "--warmup", "3", "--ncols", "96", "--nrows", "64"],
+                         cwd=root, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-500:]
+    d = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+    assert d["impl"] == "reference" and d["config"]["grid"] == [96, 128]
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["value"] == d["value"]
+    env = dict(os.environ, RANK="1", WORLD_SIZE="2")
+    quiet = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--gpus", "2", "--steps", "1"],
+                           cwd=root, capture_output=True, text=True, timeout=600, env=env)
+    assert quiet.returncode == 0 and not quiet.stdout.strip()
