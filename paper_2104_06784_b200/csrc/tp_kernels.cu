@@ -176,7 +176,11 @@ __device__ __forceinline__ void stage_phase1(const double* __restrict__ S, const
     {
         const int it = threadIdx.x;
         const bool hx = it < NFX, hy = it < NFY;
-        const int fx = it % (TX + 1), tyx = it / (TX + 1);
+        // xi faces: threads 0..TX*TY-1 take faces 0..TX-1 of each row (a warp = two 16-face
+        // row segments: conflict-free 8-byte smem loads; a 17-face row walk cost 1.5x the
+        // wavefronts), threads TX*TY.. the last face (fx = TX) of each row
+        const int fx = it < TX * TY ? it % TX : TX;
+        const int tyx = it < TX * TY ? it / TX : it - TX * TY;
         const int kx = hx ? (tyx + 2) * W2 + fx + 1 : 2 * W2 + 2;  // xi face between kx and kx+1
         const int txy = it % TX, fy = it / TX;
         const int ky = hy ? (fy + 1) * W2 + txy + 2 : 2 * W2 + 2;  // eta face between ky and ky+W2
@@ -201,7 +205,7 @@ __device__ __forceinline__ void stage_phase1(const double* __restrict__ S, const
                              G[G_A21 * BOX + ky], G[G_A21 * BOX + ky + W2], G[G_RJBFY * BOX + ky], P, oy);
         if (hx) {
 #pragma unroll
-            for (int f = 0; f < 6; ++f) FX[f * NFX + it] = ox[f];
+            for (int f = 0; f < 6; ++f) FX[f * NFX + tyx * (TX + 1) + fx] = ox[f];
         }
         if (hy) {
 #pragma unroll
@@ -451,20 +455,25 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
             Pf5 = sn_fy + -coeff * vfy + ephf * Avy + sv_fy;
         }
         if (!P.adv_only) {
-            constexpr int NB1 = (TX + 2) * TY;  // rows 2..TY+1, cols 1..TX+2
-            constexpr int NB = NB1 + 2 * TX;    // + rows 1 and TY+2, cols 2..TX+1
+            constexpr int NB = (TX + 2) * TY + 2 * TX;  // rows 2..TY+1 x cols 1..TX+2, rows 1, TY+2 x cols 2..TX+1
             // one bracket per thread (the 16 threads without a Phase-3 cell included), the
             // NB - NT remaining ones on the first warps: every warp costs sources + 1 bracket
             // pass and only two warps a second pass (a warp's cost is per pass, not per lane)
             for (int it = threadIdx.x; it < NB; it += NT) {
+                // interior cells in 16-wide row segments first (conflict-free smem walks), then
+                // rows 1 and TY+2, then columns 1 and TX+2
                 int bx, by;
-                if (it < NB1) {
-                    bx = 1 + it % (TX + 2);
-                    by = 2 + it / (TX + 2);
-                } else {
-                    const int r = it - NB1;
+                if (it < TX * TY) {
+                    bx = 2 + it % TX;
+                    by = 2 + it / TX;
+                } else if (it < TX * TY + 2 * TX) {
+                    const int r = it - TX * TY;
                     bx = 2 + r % TX;
                     by = (r < TX) ? 1 : TY + 2;
+                } else {
+                    const int r = it - TX * TY - 2 * TX;
+                    bx = (r < TY) ? 1 : TX + 2;
+                    by = 2 + (r < TY ? r : r - TY);
                 }
                 const int k = by * W2 + bx;
                 const double jb = G[G_JB * BOX + k];
