@@ -127,7 +127,7 @@ int main(int argc, char** argv) {
             for (int i = 0; i < 3; ++i) (*fr[k])(i, j) = (*fb[k])(i, j) = 0.1234567 * (k + 1) * (i - j) + 1e-7 * k;
     }
     const std::string dr = dir + "/ref", db = dir + "/b200";
-    std::system(("mkdir -p " + dr + " " + db).c_str());
+    if (std::system(("mkdir -p " + dr + " " + db).c_str()) != 0) std::fprintf(stderr, "mkdir failed\n");
     auto pr = tpflow::io::write_snapshot(sr, demr, dr);
     auto pb = tpflow_b200::io::write_snapshot(sb, demb, db);
     EXPECT(pr.size() == pb.size(), "snapshot file count");

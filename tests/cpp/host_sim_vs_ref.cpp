@@ -43,7 +43,7 @@ static void write_grid(const std::string& path, const tpflow_b200::ElevationGrid
 static void run_case(const std::string& dir, const std::string& name, const std::string& par) {
     const std::string pfile = dir + "/" + name + ".par";
     { std::ofstream o(pfile); o << par; }
-    std::system(("mkdir -p " + dir + "/out_ref_" + name + " " + dir + "/out_b200_" + name).c_str());
+    if (std::system(("mkdir -p " + dir + "/out_ref_" + name + " " + dir + "/out_b200_" + name).c_str()) != 0) std::fprintf(stderr, "mkdir failed\n");
     // the reference: tpflow::run_simulation with the serial backend (goldens)
     tpflow::SimConfig cr = tpflow::io::parse_par_list(pfile);
     cr.out_dir = dir + "/out_ref_" + name;
@@ -80,7 +80,7 @@ static void run_case(const std::string& dir, const std::string& name, const std:
 
 int main(int argc, char** argv) {
     const std::string dir = argc > 1 ? argv[1] : "/tmp/tpb_host";
-    std::system(("mkdir -p " + dir).c_str());
+    if (std::system(("mkdir -p " + dir).c_str()) != 0) std::fprintf(stderr, "mkdir failed\n");
     // Mode-I: hill on an incline (input files written with %.17g so both read identical values)
     {
         auto dem = tpflow_b200::scenarios::incline_dem(72, 60, 5.0, 15.0);
