@@ -508,20 +508,6 @@ void sync_ghosts(tp_ctx* c) {
     }
 }
 
-std::vector<double> host_state(tp_ctx* c) {
-    sync_ghosts(c);
-    std::vector<double> s(6ull * c->nx * c->ny);
-    download_state(c, s.data(), c->dA);
-    return s;
-}
-
-void set_host_state(tp_ctx* c, const std::vector<double>& s) {
-    upload_state(c, c->dA, s.data());
-    invalidate_flags(c, true, false);
-    ck(cudaStreamSynchronize(c->stream), "sync");
-    c->lam_valid = false;
-    c->ghosts_in_B = false;
-}
 
 int fail(tp_ctx* c, int code, const std::string& msg) {
     if (c) c->err = msg;
