@@ -135,6 +135,7 @@ struct tp_ctx {
     double* dTallyP = nullptr;
     double* dTallyC = nullptr;
     signed char* dSide = nullptr;
+    unsigned char* dInflowTiles = nullptr;  // per tile: its radius-2 box reads an inflow ghost
     double* dSamples = nullptr;
     double* dDts = nullptr;
     long dts_cap = 0;
@@ -287,10 +288,14 @@ tpb::TileArgs tile_args(tp_ctx* c, const tpb::StageArgs& a, bool corr) {
     t.tally = a.tally;
     t.ntx = c->ntx;
     t.nty = c->nty;
+    t.nxi = c->nx - 6;
+    t.nyi = c->ny - 6;
     t.skip = c->skip_dry ? 1 : 0;
     // ring boxes read ghost cells: only plain zero-gradient copies refreshed right before
-    // the stage (the device loop) keep the 3x3 flag rule exact
-    t.ring_ineligible = (c->inflow_active || !a.loop) ? 1 : 0;
+    // the stage (the device loop) keep the 3x3 flag rule exact; Mode-II inflow ghosts are
+    // not copies, so the ring tiles whose boxes reach them are always listed (and unsafe)
+    t.ring_ineligible = a.loop ? 0 : 1;
+    t.inflow_tiles = c->inflow_active ? c->dInflowTiles : nullptr;
     t.south_ineligible = c->g.has_south ? 0 : 1;
     t.north_ineligible = c->g.has_north ? 0 : 1;
     t.safe_ok = (c->fastdiv && c->geo_safe && c->geo_safe2) ? 1 : 0;
@@ -783,6 +788,7 @@ void tp_destroy(tp_ctx* c) {
     cudaFree(c->dSc);
     cudaFree(c->dTallyP);
     cudaFree(c->dTallyC);
+    cudaFree(c->dInflowTiles);
     cudaFree(c->dSide);
     cudaFree(c->dSamples);
     cudaFree(c->dDts);
@@ -923,6 +929,7 @@ int tp_set_hydrograph(tp_ctx* c, int n_cells, const int* ci, const int* cj, cons
         const long nband = (c->g.has_south ? 3L * c->nx : 0) + (c->g.has_north ? 3L * c->nx : 0) +
                            6L * (c->ny - 6);
         std::vector<signed char> map(static_cast<size_t>(nband), 0);
+        std::vector<unsigned char> itiles(static_cast<size_t>(c->ntx) * c->nty, 0);
         for (int k = 0; k < n_cells; ++k) {
             int di = 0, dj = 0;
             switch (side[k]) {
@@ -940,12 +947,26 @@ int tp_set_hydrograph(tp_ctx* c, int n_cells, const int* ci, const int* cj, cons
                 if (dj == 0 && (gj < kGhost || gj >= c->ny - kGhost)) continue;
                 const long b = band_index(c, gi, gj);
                 if (b >= 0) map[static_cast<size_t>(b)] = static_cast<signed char>(side[k]);
+                // tiles whose radius-2 box (padded X0-2 .. X0+TX+1, Y0-2 .. Y0+TY+1 with
+                // X0 = 3 + tx*TX, Y0 = 3 + ty*TY) contains this ghost cell
+                for (int ty = 0; ty < c->nty; ++ty) {
+                    const int y0 = kGhost + ty * tpb::TY;
+                    if (gj < y0 - 2 || gj > y0 + tpb::TY + 1) continue;
+                    for (int tx = 0; tx < c->ntx; ++tx) {
+                        const int x0 = kGhost + tx * tpb::TX;
+                        if (gi >= x0 - 2 && gi <= x0 + tpb::TX + 1) itiles[static_cast<size_t>(ty) * c->ntx + tx] = 1;
+                    }
+                }
             }
         }
         cudaFree(c->dSide);
         cudaFree(c->dSamples);
+        cudaFree(c->dInflowTiles);
         c->dSide = nullptr;
         c->dSamples = nullptr;
+        c->dInflowTiles = nullptr;
+        ck(cudaMalloc(&c->dInflowTiles, itiles.size()), "cudaMalloc inflow tiles");
+        ck(cudaMemcpy(c->dInflowTiles, itiles.data(), itiles.size(), cudaMemcpyHostToDevice), "inflow tiles H2D");
         ck(cudaMalloc(&c->dSide, std::max<size_t>(1, map.size())), "cudaMalloc side map");
         if (!map.empty())
             ck(cudaMemcpy(c->dSide, map.data(), map.size(), cudaMemcpyHostToDevice), "side map H2D");

@@ -724,11 +724,17 @@ __device__ __forceinline__ void tiles_body(const TileArgs& a, int block) {
     bool active = false, safe = false;
     if (t < ntiles) {
         const int tx = t % a.ntx, ty = t / a.ntx;
-        const bool ring = tx == 0 || tx == a.ntx - 1 || ty == 0 || ty == a.nty - 1;
+        const bool ring = tx == 0 || tx == a.ntx - 1 || ty == 0 || ty == a.nty - 1;  // owns boundary faces
+        // the radius-2 box (padded X0-2 .. X0+TX+1, X0 = 3 + tx*TX; rows alike) reaches the
+        // W / E ghost columns, the S / N ghost (or halo) rows
+        const bool reach_s = ty == 0, reach_n = (ty + 1) * TY + 1 >= a.nyi;
+        const bool ghost_box = tx == 0 || (tx + 1) * TX + 1 >= a.nxi || reach_s || reach_n;
+        // boxes that read a Mode-II inflow ghost (values the flags do not see; exact per tile)
+        const bool inflow_box = a.inflow_tiles && a.inflow_tiles[t];
         bool skip = a.skip && a.flag_out[t] == 0;
-        if (ring && a.ring_ineligible) skip = false;
-        if (ty == 0 && a.south_ineligible) skip = false;
-        if (ty == a.nty - 1 && a.north_ineligible) skip = false;
+        if ((ghost_box && a.ring_ineligible) || inflow_box) skip = false;
+        if (reach_s && a.south_ineligible) skip = false;
+        if (reach_n && a.north_ineligible) skip = false;
         if (skip) {
             // the radius-2 box reads this tile's interior, the facing 2-cell band of each
             // edge neighbour and the facing 2x2 corner of each diagonal neighbour
@@ -746,8 +752,8 @@ __device__ __forceinline__ void tiles_body(const TileArgs& a, int block) {
             skip = need == 0u;
         }
         active = !skip;
-        if (active && a.safe_ok && !(ring && a.ring_ineligible) && !(ty == 0 && a.south_ineligible) &&
-            !(ty == a.nty - 1 && a.north_ineligible)) {
+        if (active && a.safe_ok && !(ghost_box && a.ring_ineligible) && !inflow_box && !(reach_s && a.south_ineligible) &&
+            !(reach_n && a.north_ineligible)) {
             // safe: no value the box reads (this tile and the facing parts of its 8
             // neighbours; ghosts are clamp copies of them) is outside the window
             const unsigned short* F = a.flag_in;

@@ -150,8 +150,11 @@ struct TileArgs {
     int* work;            // this stage's dynamic tile scheduler counter (zeroed here)
     double* tally;
     int ntx, nty;
+    int nxi, nyi;         // interior columns / rows of this context (a tile's box may reach the ghost band
+                          // or the halo rows without being an edge tile: a last tile of one column / row)
     int skip;             // 0 = list every tile
-    int ring_ineligible;  // 1 = ring tiles read non-copy ghosts (Mode-II inflow): never skip them
+    int ring_ineligible;  // 1 = ring tiles read ghosts not refreshed as copies (outside the device loop)
+    const unsigned char* inflow_tiles;  // per tile: its box reads a Mode-II inflow ghost (never skip, never safe); may be null
     int south_ineligible, north_ineligible;  // slab edges next to halo rows: never skip
     int safe_ok;          // FASTDIV on, geometry and constants inside the safe-window bounds (tp_capi.cpp)
     int loop;
