@@ -152,6 +152,9 @@ int tp_active_tiles(tp_ctx* c, int* pred, int* corr, int* total);
 /* how many tiles of the last corrector list were "safe" (every value their box reads is
  * +-0 or of magnitude in [2^-200, 2^200): FASTDIV window tests compiled out) */
 int tp_safe_tiles(tp_ctx* c, int* corr);
+/* peer-joined slabs: how many tiles listed only because their box reads halo rows were
+ * skipped because the neighbour's pushed rows were +0.0 there (cumulative) */
+int tp_cond_skipped_tiles(tp_ctx* c, unsigned long long* n);
 /* development probe: per-phase warp cycles of the stage kernels [2][19] (pred, corr;
  * slot 16 counts warps, 17/18 sum warp lifetimes in cycles / ns); all zero unless the library was built with `make timing` */
 int tp_debug_phase_cycles(unsigned long long* out, int reset);

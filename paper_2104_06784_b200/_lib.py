@@ -82,6 +82,7 @@ SIGNATURES = {
     "tp_peer_connect_local": (C.c_int, [_vp, C.c_int, C.c_int, C.POINTER(_vp)]),
     "tp_steps_group": (C.c_int, [C.POINTER(_vp), C.c_int, C.c_double, C.c_double, C.c_long, _dp, _lp, _ip]),
     "tp_safe_tiles": (C.c_int, [_vp, _ip]),
+    "tp_cond_skipped_tiles": (C.c_int, [_vp, C.POINTER(C.c_ulonglong)]),
     "tp_debug_phase_cycles": (C.c_int, [C.POINTER(C.c_ulonglong), C.c_int]),
 }
 

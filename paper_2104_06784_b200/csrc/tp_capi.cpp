@@ -274,6 +274,13 @@ tpb::StageArgs stage_args(tp_ctx* c, bool corr, int loop) {
     a.flag_out = corr ? c->dFlagA : c->dFlagB;
     a.nact_stat = c->dNact + 2;
     a.work = c->dNact + 6 + (corr ? 1 : 0);
+    // device loop of a peer-joined slab: the neighbours' halo_nz of this stage's buffer
+    // (kTileCond tiles, listed by tiles_kernel only then: tile_args cond_halo)
+    const int buf = corr ? 1 : 0;
+    for (int side = 0; side < 2; ++side)
+        a.halo_nz[side] = (loop && c->peered && c->ntx <= tpb::kMaxTileCols && c->link.nbr_state[buf][side])
+                              ? c->dBox->halo_nz[buf][side]
+                              : nullptr;
     return a;
 }
 
@@ -299,6 +306,7 @@ tpb::TileArgs tile_args(tp_ctx* c, const tpb::StageArgs& a, bool corr) {
     t.south_ineligible = c->g.has_south ? 0 : 1;
     t.north_ineligible = c->g.has_north ? 0 : 1;
     t.safe_ok = (c->fastdiv && c->geo_safe && c->geo_safe2) ? 1 : 0;
+    t.cond_halo = (a.loop && c->peered && c->ntx <= tpb::kMaxTileCols) ? 1 : 0;
     t.loop = a.loop;
     t.sc = c->dSc;
     return t;
@@ -1598,6 +1606,10 @@ int tp_safe_tiles(tp_ctx* c, int* corr) {
         ck(cudaMemcpyAsync(corr, c->dNact + 5, sizeof(int), cudaMemcpyDeviceToHost, c->stream), "tiles D2H");
         ck(cudaStreamSynchronize(c->stream), "sync");
     })
+}
+
+int tp_cond_skipped_tiles(tp_ctx* c, unsigned long long* n) {
+    TP_GUARD(c, { *n = read_scalars(c).cond_skips; })
 }
 
 int tp_active_tiles(tp_ctx* c, int* pred, int* corr, int* total) {

@@ -291,30 +291,50 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
         }
     };
     (void)ntiles;
+    // kTileCond entries (thread 0, at claim time): skipped when the neighbours' pushed halo
+    // rows are +0.0 over the box's columns - the tile is then a bitwise no-op (DESIGN.md §3
+    // item 5); a ring tile still zeroes its tally slot
+    auto cond_skip = [&](int e) -> bool {
+        if (!(e & kTileCond)) return false;
+        const int tx = e & 0xffff, ty = (e >> 16) & 0x1fff;
+        if (ty == 0 && !g.has_south && (!A.halo_nz[0] || A.halo_nz[0][tx])) return false;
+        if ((ty + 1) * TY + 1 >= ny - 6 && !g.has_north && (!A.halo_nz[1] || A.halo_nz[1][tx])) return false;
+        if (tx == 0 || tx == A.ntx - 1 || ty == 0 || ty == A.nty - 1) {
+            double* t4 = A.tally + 4ll * (ty * A.ntx + tx);
+            t4[0] = t4[1] = t4[2] = t4[3] = 0.0;
+        }
+        atomicAdd(&sc->cond_skips, 1ull);
+        return true;
+    };
     if (threadIdx.x == 0) {
         mbar_init(&bar, 1);
         mbar_init(&barc, 1);
         mbar_init(&baru, 1);
-        if (static_cast<int>(blockIdx.x) < nact) {
-            const int e = A.tiles[blockIdx.x];
+        int li0 = static_cast<int>(blockIdx.x);
+        while (li0 < nact && cond_skip(A.tiles[li0])) li0 = static_cast<int>(gridDim.x) + atomicAdd(A.work, 1);
+        s_nli[1] = li0;  // the first list entry of this CTA (read after the barrier below)
+        if (li0 < nact) {
+            const int e = A.tiles[li0];
             s_tile = e;
             const int bx0 = 1 + (e & 0xffff) * TX, by0 = 1 + ((e >> 16) & 0x1fff) * TY;
             mbar_expect_tx(&bar, kTmaBytes);
             // x coordinate + 1: the leading pad column of the device layout (tp_capi.cpp)
             tma_load_3d(S, &A.tm_s, bx0 + 1, by0, 0, &bar);
             tma_load_3d(sm + SM_G, &A.tm_g, bx0 + 1, by0, 0, &bar);
-            issue_cell(blockIdx.x, e);
+            issue_cell(li0, e);
         }
     }
     if (threadIdx.x == 0) s_flags = 0u;
     __syncthreads();  // barrier init visible to all threads
+    const int li_first = s_nli[1];
+    __syncthreads();  // s_nli is rewritten by the first iteration
     double lam_local = 0.0;
     unsigned iter = 0;
     TPROBE_DECL
     // Dynamic tile scheduler: every CTA starts on list entry blockIdx.x, then claims the
     // next entry with one atomic per tile (claimed a tile ahead, so the TMA prefetch still
     // has a target) - CTAs that drew cheap, partially dry tiles take more of them.
-    for (int li = blockIdx.x; li < nact; ++iter) {
+    for (int li = li_first; li < nact; ++iter) {
     const int entry = s_tile;  // written by thread 0 before the previous end-of-tile barrier
     const int tix = entry & 0xffff, tiy = (entry >> 16) & 0x1fff;
     const int tile = tiy * A.ntx + tix;
@@ -327,8 +347,12 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
     // thread 0 claims the next list entry now; it is consumed at issue time
     int nli = nact, next_entry = 0;
     if (threadIdx.x == 0) {
-        nli = static_cast<int>(gridDim.x) + atomicAdd(A.work, 1);
-        if (nli < nact) next_entry = A.tiles[nli];
+        for (;;) {
+            nli = static_cast<int>(gridDim.x) + atomicAdd(A.work, 1);
+            if (nli >= nact) break;
+            next_entry = A.tiles[nli];
+            if (!cond_skip(next_entry)) break;
+        }
         s_nli[iter & 1u] = nli;
     }
     // next tile's boxes into S/G (call only once they are dead)
@@ -721,7 +745,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
 __device__ __forceinline__ void tiles_body(const TileArgs& a, int block) {
     const int ntiles = a.ntx * a.nty;
     const int t = block * blockDim.x + threadIdx.x;
-    bool active = false, safe = false;
+    bool active = false, safe = false, cond = false;
     if (t < ntiles) {
         const int tx = t % a.ntx, ty = t / a.ntx;
         const bool ring = tx == 0 || tx == a.ntx - 1 || ty == 0 || ty == a.nty - 1;  // owns boundary faces
@@ -733,8 +757,7 @@ __device__ __forceinline__ void tiles_body(const TileArgs& a, int block) {
         const bool inflow_box = a.inflow_tiles && a.inflow_tiles[t];
         bool skip = a.skip && a.flag_out[t] == 0;
         if ((ghost_box && a.ring_ineligible) || inflow_box) skip = false;
-        if (reach_s && a.south_ineligible) skip = false;
-        if (reach_n && a.north_ineligible) skip = false;
+        const bool halo_reach = (reach_s && a.south_ineligible) || (reach_n && a.north_ineligible);
         if (skip) {
             // the radius-2 box reads this tile's interior, the facing 2-cell band of each
             // edge neighbour and the facing 2x2 corner of each diagonal neighbour
@@ -750,6 +773,10 @@ __device__ __forceinline__ void tiles_body(const TileArgs& a, int block) {
             if (xl && yr) need |= F[t + a.ntx - 1] & TF_SE;
             if (xr && yr) need |= F[t + a.ntx + 1] & TF_SW;
             skip = need == 0u;
+        }
+        if (skip && halo_reach) {  // the halo rows decide: listed, conditional when peer-joined
+            skip = false;
+            cond = a.cond_halo != 0;
         }
         active = !skip;
         if (active && a.safe_ok && !(ghost_box && a.ring_ineligible) && !inflow_box && !(reach_s && a.south_ineligible) &&
@@ -789,7 +816,8 @@ __device__ __forceinline__ void tiles_body(const TileArgs& a, int block) {
     if (lane == 0 && ms) atomicAdd(a.ntiles_active + 4, __popc(ms));
     base = __shfl_sync(0xffffffffu, base, 0);
     if (active)
-        a.tiles[base + __popc(m & ((1u << lane) - 1u))] = ((t / a.ntx) << 16) | (t % a.ntx) | (safe ? kTileSafe : 0);
+        a.tiles[base + __popc(m & ((1u << lane) - 1u))] =
+            ((t / a.ntx) << 16) | (t % a.ntx) | (safe ? kTileSafe : 0) | (cond ? kTileCond : 0);
 }
 
 __global__ void __launch_bounds__(NT) tiles_kernel(TileArgs a) {

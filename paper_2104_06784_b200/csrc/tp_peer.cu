@@ -126,6 +126,21 @@ __global__ void peer_halo_push_kernel(PeerLink L, GridDesc g, const double* __re
         dst[f * dfs + static_cast<long long>(dst_row + dr) * g.pitch + i] =
             s[f * g.fs + static_cast<long long>(src_row + dr) * g.pitch + i];
     }
+    // per tile column of the receiver (same columns): does any pushed value inside the box
+    // columns X0-2 .. X0+TX+1 have a bit other than +0.0 (its kTileCond tiles, stage_kernel)
+    const int ntx = (g.nx - 6 + TX - 1) / TX;
+    unsigned int* nz = L.nbr_box[side]->halo_nz[buf][side == 0 ? 1 : 0];
+    for (int tx = blockIdx.x * blockDim.x + threadIdx.x; tx < ntx && tx < kMaxTileCols;
+         tx += gridDim.x * blockDim.x) {
+        const int x0 = 3 + tx * TX - 2, x1 = min(3 + tx * TX + TX + 1, g.nx - 1);
+        unsigned long long bits = 0ull;
+        for (int f = 0; f < 6; ++f)
+            for (int dr = 0; dr < 2; ++dr) {
+                const double* row = s + f * g.fs + static_cast<long long>(src_row + dr) * g.pitch;
+                for (int x = x0; x <= x1; ++x) bits |= static_cast<unsigned long long>(__double_as_longlong(row[x]));
+            }
+        nz[tx] = bits != 0ull ? 1u : 0u;
+    }
     __threadfence_system();
     __syncthreads();
     if (threadIdx.x == 0) {

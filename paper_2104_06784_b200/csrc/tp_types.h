@@ -69,6 +69,7 @@ struct DevScalars {
     double audit[10];             // solid {initial, final, injected, outflow, clipped}, fluid {...}
     double* dts;                  // optional per-step dt record (device)
     unsigned long long peer_base; // sequence base of the slab exchange (tp_peer.cu)
+    unsigned long long cond_skips;  // kTileCond tiles skipped by the stage kernels (cumulative)
 };
 
 struct GridDesc {
@@ -119,6 +120,7 @@ struct StageArgs {
     unsigned short* flag_out;        // per-tile TileFlag bits of `out` (nonzero bits per region)
     int* nact_stat;                  // [2] list length of the last predictor / corrector launch
     int* work;                       // dynamic tile scheduler counter of this stage (zeroed by tiles_kernel)
+    const unsigned int* halo_nz[2];  // [side 0 south, 1 north] this stage's PeerBox::halo_nz, null = none
 };
 
 // Per-tile output flags: which regions of the tile's interior hold a value with a nonzero
@@ -133,6 +135,11 @@ enum TileFlag : unsigned {
 // list-entry bit: every state value the tile's box reads is +-0 or in the safe window
 // (entries: tile column in bits 0-15, tile row in bits 16-28)
 constexpr int kTileSafe = 1 << 30;
+// Listed only because its box reads halo rows of a peer-joined slab, the tile is otherwise a
+// bitwise no-op: the stage kernel skips it when the neighbour's pushed rows are +0.0 over
+// the box's columns (PeerBox::halo_nz, written by peer_halo_push_kernel before the release).
+constexpr int kTileCond = 1 << 29;
+constexpr int kMaxTileCols = 2048;  // halo_nz entries per side (ncols <= 32768)
 
 // Dry-tile classification before a stage.  flag_in: per-tile flags of the stage's input
 // buffer (the radius-2 box reads interior cells of the tile and the facing bands/corners
@@ -157,6 +164,7 @@ struct TileArgs {
     const unsigned char* inflow_tiles;  // per tile: its box reads a Mode-II inflow ghost (never skip, never safe); may be null
     int south_ineligible, north_ineligible;  // slab edges next to halo rows: never skip
     int safe_ok;          // FASTDIV on, geometry and constants inside the safe-window bounds (tp_capi.cpp)
+    int cond_halo;        // peer-joined slab: halo-reaching tiles that are otherwise no-ops are listed kTileCond
     int loop;
     DevScalars* sc;
 };
@@ -200,6 +208,9 @@ struct PeerBox {
     unsigned long long stop_val[kMaxRanks];     // 1 if the rank stopped (error)
     unsigned int push_done[2][2];               // local: CTAs finished pushing [buf][side]
     unsigned int pad[4];
+    // [buf][side][tile column]: 1 if the 2 pushed rows hold a bit other than +0.0 within the
+    // columns tile tx's box reads (X0-2 .. X0+TX+1); written before halo_seq is released
+    unsigned int halo_nz[2][2][kMaxTileCols];
 };
 // Where this slab's neighbours live (pointers valid in this process: own allocations,
 // allocations of contexts in this process, or CUDA-IPC mappings of other processes').

@@ -112,3 +112,26 @@ def test_peer_two_processes_ipc(gpu, oracle_kind, make_name, tmp_path):
     for m in metas:
         assert m[0] == t1 and int(m[1]) == len(d1)
     assert_bitwise(assemble(states), ref.state()[:, 3:-3, 3:-3], "interior (2 processes)")
+
+
+def test_peer_halo_tiles_skipped_when_halo_dry(gpu, oracle_kind):
+    """Tiles listed only because their box reads halo rows (kTileCond) are skipped when the
+    neighbour's pushed rows are +0.0 over their columns (PeerBox::halo_nz): the count is
+    positive on a release that crosses the slab boundary in a few columns only, and the
+    result stays bit-identical to the reference."""
+    import ctypes as C
+    import torch
+    from oracle.oracle import OracleSim
+    sc = scenarios.c1_hill(96)
+    ref = OracleSim(sc, oracle_kind)
+    t1, d1, _ = ref.steps(0.0, 1e9, 30, t_end=1e9)
+    slabs = [CudaSlab(sc, r, stream=torch.cuda.Stream()) for r in decompose(sc.nrows, 3)]
+    t2, n2, _ = PeerGroup(slabs).steps(0.0, 1e9, 30, t_end=1e9)
+    assert n2 == len(d1) and t2 == t1
+    assert_bitwise(assemble([s.state() for s in slabs]), ref.state()[:, 3:-3, 3:-3], "interior")
+    skipped = []
+    for s in slabs:
+        n = C.c_ulonglong()
+        s.sim._check(s.L.tp_cond_skipped_tiles(s.h, C.byref(n)))
+        skipped.append(n.value)
+    assert sum(skipped) > 0, skipped
