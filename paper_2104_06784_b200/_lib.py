@@ -109,7 +109,12 @@ def lib():
                               "(make -C paper_2104_06784_b200/csrc); there is no CPU fallback")
         L = C.CDLL(LIB_PATH)
         for name, (res, args) in SIGNATURES.items():
-            f = getattr(L, name)
+            try:
+                f = getattr(L, name)
+            except AttributeError:
+                if "TPFLOW_B200_LIB" in os.environ:  # an older build under test (A/B timing)
+                    continue
+                raise
             f.restype = res
             f.argtypes = args
         _LIB = L

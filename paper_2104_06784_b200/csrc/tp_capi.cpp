@@ -46,7 +46,7 @@ cudaError_t launch_init_velocity(const GridDesc& g, const double* geo, const dou
 cudaError_t launch_geo_check(const GridDesc& g, const double* geo, int* ok, cudaStream_t st);
 cudaError_t launch_peer_lambda(const PeerLink& L, DevScalars* sc, cudaStream_t st);
 cudaError_t launch_peer_halo(const PeerLink& L, const GridDesc& g, const double* s, int buf, DevScalars* sc,
-                             cudaStream_t st);
+                             const CondArgs& ca, cudaStream_t st);
 cudaError_t launch_pack_state(const GridDesc& g, const double* src, double* dst, bool unpack, cudaStream_t st);
 cudaError_t launch_mass(const GridDesc& g, const double* s, double* part, int blocks, cudaStream_t st);
 cudaError_t launch_snapshot(const GridDesc& g, const double* s, const double* geo, double* out, int ncols,
@@ -136,6 +136,8 @@ struct tp_ctx {
     double* dTallyC = nullptr;
     signed char* dSide = nullptr;
     unsigned char* dInflowTiles = nullptr;  // per tile: its radius-2 box reads an inflow ghost
+    int* dCond = nullptr;   // conditional tiles of the stage in flight (peer-joined slabs)
+    int* dNcond = nullptr;
     double* dSamples = nullptr;
     double* dDts = nullptr;
     long dts_cap = 0;
@@ -274,14 +276,20 @@ tpb::StageArgs stage_args(tp_ctx* c, bool corr, int loop) {
     a.flag_out = corr ? c->dFlagA : c->dFlagB;
     a.nact_stat = c->dNact + 2;
     a.work = c->dNact + 6 + (corr ? 1 : 0);
-    // device loop of a peer-joined slab: the neighbours' halo_nz of this stage's buffer
-    // (kTileCond tiles, listed by tiles_kernel only then: tile_args cond_halo)
-    const int buf = corr ? 1 : 0;
-    for (int side = 0; side < 2; ++side)
-        a.halo_nz[side] = (loop && c->peered && c->ntx <= tpb::kMaxTileCols && c->link.nbr_state[buf][side])
-                              ? c->dBox->halo_nz[buf][side]
-                              : nullptr;
     return a;
+}
+
+tpb::CondArgs cond_args(tp_ctx* c, const tpb::StageArgs& a, bool corr) {
+    tpb::CondArgs ca{};
+    ca.tiles = c->dTiles;
+    ca.ntiles_active = c->dNact + (corr ? 1 : 0);
+    ca.cond_tiles = c->dCond;
+    ca.ncond = c->dNcond;
+    ca.tally = a.tally;
+    ca.ntx = c->ntx;
+    ca.nty = c->nty;
+    ca.nyi = c->ny - 6;
+    return ca;
 }
 
 tpb::TileArgs tile_args(tp_ctx* c, const tpb::StageArgs& a, bool corr) {
@@ -307,6 +315,8 @@ tpb::TileArgs tile_args(tp_ctx* c, const tpb::StageArgs& a, bool corr) {
     t.north_ineligible = c->g.has_north ? 0 : 1;
     t.safe_ok = (c->fastdiv && c->geo_safe && c->geo_safe2) ? 1 : 0;
     t.cond_halo = (a.loop && c->peered && c->ntx <= tpb::kMaxTileCols) ? 1 : 0;
+    t.cond_tiles = c->dCond;
+    t.ncond = c->dNcond;
     t.loop = a.loop;
     t.sc = c->dSc;
     return t;
@@ -391,7 +401,9 @@ void enqueue_loop_step(tp_ctx* c, cudaEvent_t* ev = nullptr) {
         // halo rows after apply_boundaries (solver.cpp:639, :523), straight into the
         // neighbours' buffers, then wait for theirs
         if (c->peered)
-            ck(tpb::launch_peer_halo(c->link, c->g, corr ? c->dB : c->dA, corr, c->dSc, c->stream), "peer halo");
+            ck(tpb::launch_peer_halo(c->link, c->g, corr ? c->dB : c->dA, corr, c->dSc, cond_args(c, sa, corr != 0),
+                                     c->stream),
+               "peer halo");
         if (ev) ck(cudaEventRecordWithFlags(ev[2 * corr], c->stream, cudaEventRecordExternal), "event");
         ck(tpb::launch_stage(sa, c->fastdiv, corr != 0, c->stream), corr ? "corrector" : "predictor");
         if (ev) ck(cudaEventRecordWithFlags(ev[2 * corr + 1], c->stream, cudaEventRecordExternal), "event");
@@ -678,6 +690,9 @@ void create_impl(tp_ctx* c, const tp_params* p, const tp_dem* dem, int row0, int
     ck(cudaMalloc(&c->dBox, sizeof(tpb::PeerBox)), "cudaMalloc mailbox");
     ck(cudaMemsetAsync(c->dBox, 0, sizeof(tpb::PeerBox), c->stream), "memset");
     ck(cudaMalloc(&c->dNact, 8 * sizeof(int)), "cudaMalloc tiles");
+    ck(cudaMalloc(&c->dCond, sizeof(int) * ntiles), "cudaMalloc cond tiles");
+    ck(cudaMalloc(&c->dNcond, sizeof(int)), "cudaMalloc cond count");
+    ck(cudaMemsetAsync(c->dNcond, 0, sizeof(int), c->stream), "memset");
     ck(cudaMemsetAsync(c->dNact, 0, 8 * sizeof(int), c->stream), "memset");
     invalidate_flags(c, true, true);
     if (c->host_geometry) {
@@ -797,6 +812,8 @@ void tp_destroy(tp_ctx* c) {
     cudaFree(c->dTallyP);
     cudaFree(c->dTallyC);
     cudaFree(c->dInflowTiles);
+    cudaFree(c->dCond);
+    cudaFree(c->dNcond);
     cudaFree(c->dSide);
     cudaFree(c->dSamples);
     cudaFree(c->dDts);

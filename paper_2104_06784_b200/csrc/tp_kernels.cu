@@ -291,50 +291,30 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
         }
     };
     (void)ntiles;
-    // kTileCond entries (thread 0, at claim time): skipped when the neighbours' pushed halo
-    // rows are +0.0 over the box's columns - the tile is then a bitwise no-op (DESIGN.md §3
-    // item 5); a ring tile still zeroes its tally slot
-    auto cond_skip = [&](int e) -> bool {
-        if (!(e & kTileCond)) return false;
-        const int tx = e & 0xffff, ty = (e >> 16) & 0x1fff;
-        if (ty == 0 && !g.has_south && (!A.halo_nz[0] || A.halo_nz[0][tx])) return false;
-        if ((ty + 1) * TY + 1 >= ny - 6 && !g.has_north && (!A.halo_nz[1] || A.halo_nz[1][tx])) return false;
-        if (tx == 0 || tx == A.ntx - 1 || ty == 0 || ty == A.nty - 1) {
-            double* t4 = A.tally + 4ll * (ty * A.ntx + tx);
-            t4[0] = t4[1] = t4[2] = t4[3] = 0.0;
-        }
-        atomicAdd(&sc->cond_skips, 1ull);
-        return true;
-    };
     if (threadIdx.x == 0) {
         mbar_init(&bar, 1);
         mbar_init(&barc, 1);
         mbar_init(&baru, 1);
-        int li0 = static_cast<int>(blockIdx.x);
-        while (li0 < nact && cond_skip(A.tiles[li0])) li0 = static_cast<int>(gridDim.x) + atomicAdd(A.work, 1);
-        s_nli[1] = li0;  // the first list entry of this CTA (read after the barrier below)
-        if (li0 < nact) {
-            const int e = A.tiles[li0];
+        if (static_cast<int>(blockIdx.x) < nact) {
+            const int e = A.tiles[blockIdx.x];
             s_tile = e;
             const int bx0 = 1 + (e & 0xffff) * TX, by0 = 1 + ((e >> 16) & 0x1fff) * TY;
             mbar_expect_tx(&bar, kTmaBytes);
             // x coordinate + 1: the leading pad column of the device layout (tp_capi.cpp)
             tma_load_3d(S, &A.tm_s, bx0 + 1, by0, 0, &bar);
             tma_load_3d(sm + SM_G, &A.tm_g, bx0 + 1, by0, 0, &bar);
-            issue_cell(li0, e);
+            issue_cell(blockIdx.x, e);
         }
     }
     if (threadIdx.x == 0) s_flags = 0u;
     __syncthreads();  // barrier init visible to all threads
-    const int li_first = s_nli[1];
-    __syncthreads();  // s_nli is rewritten by the first iteration
     double lam_local = 0.0;
     unsigned iter = 0;
     TPROBE_DECL
     // Dynamic tile scheduler: every CTA starts on list entry blockIdx.x, then claims the
     // next entry with one atomic per tile (claimed a tile ahead, so the TMA prefetch still
     // has a target) - CTAs that drew cheap, partially dry tiles take more of them.
-    for (int li = li_first; li < nact; ++iter) {
+    for (int li = blockIdx.x; li < nact; ++iter) {
     const int entry = s_tile;  // written by thread 0 before the previous end-of-tile barrier
     const int tix = entry & 0xffff, tiy = (entry >> 16) & 0x1fff;
     const int tile = tiy * A.ntx + tix;
@@ -347,12 +327,8 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
     // thread 0 claims the next list entry now; it is consumed at issue time
     int nli = nact, next_entry = 0;
     if (threadIdx.x == 0) {
-        for (;;) {
-            nli = static_cast<int>(gridDim.x) + atomicAdd(A.work, 1);
-            if (nli >= nact) break;
-            next_entry = A.tiles[nli];
-            if (!cond_skip(next_entry)) break;
-        }
+        nli = static_cast<int>(gridDim.x) + atomicAdd(A.work, 1);
+        if (nli < nact) next_entry = A.tiles[nli];
         s_nli[iter & 1u] = nli;
     }
     // next tile's boxes into S/G (call only once they are dead)
@@ -808,16 +784,21 @@ __device__ __forceinline__ void tiles_body(const TileArgs& a, int block) {
         a.ntiles_reset[4] = 0;  // the other stage's safe-tile count (diagnostics)
         *a.work = 0;            // this stage's dynamic tile scheduler (its previous launch is done)
     }
-    const unsigned m = __ballot_sync(0xffffffffu, active);
+    // conditional tiles go to their own list: peer_wait_kernel appends the ones whose halo
+    // columns are not dry once the neighbours' rows have arrived (tp_peer.cu)
+    const unsigned m = __ballot_sync(0xffffffffu, active && !cond);
     const unsigned ms = __ballot_sync(0xffffffffu, active && safe);
+    const unsigned mc = __ballot_sync(0xffffffffu, cond);
     const int lane = threadIdx.x & 31;
-    int base = 0;
+    int base = 0, cbase = 0;
     if (lane == 0 && m) base = atomicAdd(a.ntiles_active, __popc(m));
     if (lane == 0 && ms) atomicAdd(a.ntiles_active + 4, __popc(ms));
+    if (lane == 0 && mc) cbase = atomicAdd(a.ncond, __popc(mc));
     base = __shfl_sync(0xffffffffu, base, 0);
-    if (active)
-        a.tiles[base + __popc(m & ((1u << lane) - 1u))] =
-            ((t / a.ntx) << 16) | (t % a.ntx) | (safe ? kTileSafe : 0) | (cond ? kTileCond : 0);
+    cbase = __shfl_sync(0xffffffffu, cbase, 0);
+    const int entry = ((t / a.ntx) << 16) | (t % a.ntx);
+    if (active && !cond) a.tiles[base + __popc(m & ((1u << lane) - 1u))] = entry | (safe ? kTileSafe : 0);
+    if (cond) a.cond_tiles[cbase + __popc(mc & ((1u << lane) - 1u))] = entry;
 }
 
 __global__ void __launch_bounds__(NT) tiles_kernel(TileArgs a) {

@@ -127,7 +127,7 @@ __global__ void peer_halo_push_kernel(PeerLink L, GridDesc g, const double* __re
             s[f * g.fs + static_cast<long long>(src_row + dr) * g.pitch + i];
     }
     // per tile column of the receiver (same columns): does any pushed value inside the box
-    // columns X0-2 .. X0+TX+1 have a bit other than +0.0 (its kTileCond tiles, stage_kernel)
+    // columns X0-2 .. X0+TX+1 have a bit other than +0.0 (its conditional tiles, peer_wait_kernel)
     const int ntx = (g.nx - 6 + TX - 1) / TX;
     unsigned int* nz = L.nbr_box[side]->halo_nz[buf][side == 0 ? 1 : 0];
     for (int tx = blockIdx.x * blockDim.x + threadIdx.x; tx < ntx && tx < kMaxTileCols;
@@ -154,15 +154,42 @@ __global__ void peer_halo_push_kernel(PeerLink L, GridDesc g, const double* __re
     }
 }
 
-// Wait for the halo rows of buffer `buf` from both neighbours.
-__global__ void peer_wait_kernel(PeerLink L, DevScalars* sc, int buf) {
-    if (*(volatile int*)&sc->done) return;
+// Wait for the halo rows of buffer `buf` from both neighbours, then filter this stage's
+// conditional tiles (tiles_kernel: bitwise no-ops except that their box reads halo rows):
+// a tile is appended to the stage's active list only if a neighbour's pushed rows hold a
+// bit other than +0.0 within its box columns (halo_nz); a skipped ring tile zeroes its
+// tally slot.  The conditional list is reset for the next stage in every case.
+__global__ void peer_wait_kernel(PeerLink L, DevScalars* sc, int buf, CondArgs ca) {
+    const bool live = !*(volatile int*)&sc->done;
     const int side = threadIdx.x;
-    if (side > 1 || !L.nbr_state[buf][side]) return;
-    if (!wait_seq(&L.my_box->halo_seq[buf][side], seq_of(sc, 1 + buf))) {
-        atomicMin(&sc->err_key, kPeerTimeoutKey);
-        sc->done = 1;
+    if (live && side < 2 && L.nbr_state[buf][side]) {
+        if (!wait_seq(&L.my_box->halo_seq[buf][side], seq_of(sc, 1 + buf))) {
+            atomicMin(&sc->err_key, kPeerTimeoutKey);
+            sc->done = 1;
+        }
     }
+    __syncthreads();
+    const int n = *ca.ncond;
+    for (int i = threadIdx.x; live && i < n; i += blockDim.x) {
+        const int e = ca.cond_tiles[i];
+        const int tx = e & 0xffff, ty = (e >> 16) & 0x1fff;
+        const volatile unsigned int* nz_s = L.my_box->halo_nz[buf][0];  // rows from the south neighbour
+        const volatile unsigned int* nz_n = L.my_box->halo_nz[buf][1];
+        bool keep = false;
+        if (ty == 0) keep |= !L.nbr_state[buf][0] || nz_s[tx] != 0u;
+        if ((ty + 1) * TY + 1 >= ca.nyi) keep |= !L.nbr_state[buf][1] || nz_n[tx] != 0u;
+        if (keep) {
+            ca.tiles[atomicAdd(ca.ntiles_active, 1)] = e;
+        } else {
+            if (tx == 0 || tx == ca.ntx - 1 || ty == 0 || ty == ca.nty - 1) {
+                double* t4 = ca.tally + 4ll * (static_cast<long long>(ty) * ca.ntx + tx);
+                t4[0] = t4[1] = t4[2] = t4[3] = 0.0;
+            }
+            atomicAdd(&sc->cond_skips, 1ull);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) *ca.ncond = 0;
 }
 
 cudaError_t launch_peer_lambda(const PeerLink& L, DevScalars* sc, cudaStream_t st) {
@@ -170,11 +197,11 @@ cudaError_t launch_peer_lambda(const PeerLink& L, DevScalars* sc, cudaStream_t s
     return cudaGetLastError();
 }
 cudaError_t launch_peer_halo(const PeerLink& L, const GridDesc& g, const double* s, int buf, DevScalars* sc,
-                             cudaStream_t st) {
+                             const CondArgs& ca, cudaStream_t st) {
     peer_halo_push_kernel<<<dim3(16, 2), 256, 0, st>>>(L, g, s, buf, sc);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    peer_wait_kernel<<<1, 32, 0, st>>>(L, sc, buf);
+    peer_wait_kernel<<<1, 256, 0, st>>>(L, sc, buf, ca);
     return cudaGetLastError();
 }
 

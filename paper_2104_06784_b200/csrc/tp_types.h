@@ -69,7 +69,7 @@ struct DevScalars {
     double audit[10];             // solid {initial, final, injected, outflow, clipped}, fluid {...}
     double* dts;                  // optional per-step dt record (device)
     unsigned long long peer_base; // sequence base of the slab exchange (tp_peer.cu)
-    unsigned long long cond_skips;  // kTileCond tiles skipped by the stage kernels (cumulative)
+    unsigned long long cond_skips;  // conditional tiles left off the list by peer_wait_kernel (cumulative)
 };
 
 struct GridDesc {
@@ -120,7 +120,6 @@ struct StageArgs {
     unsigned short* flag_out;        // per-tile TileFlag bits of `out` (nonzero bits per region)
     int* nact_stat;                  // [2] list length of the last predictor / corrector launch
     int* work;                       // dynamic tile scheduler counter of this stage (zeroed by tiles_kernel)
-    const unsigned int* halo_nz[2];  // [side 0 south, 1 north] this stage's PeerBox::halo_nz, null = none
 };
 
 // Per-tile output flags: which regions of the tile's interior hold a value with a nonzero
@@ -135,10 +134,9 @@ enum TileFlag : unsigned {
 // list-entry bit: every state value the tile's box reads is +-0 or in the safe window
 // (entries: tile column in bits 0-15, tile row in bits 16-28)
 constexpr int kTileSafe = 1 << 30;
-// Listed only because its box reads halo rows of a peer-joined slab, the tile is otherwise a
-// bitwise no-op: the stage kernel skips it when the neighbour's pushed rows are +0.0 over
-// the box's columns (PeerBox::halo_nz, written by peer_halo_push_kernel before the release).
-constexpr int kTileCond = 1 << 29;
+// A tile of a peer-joined slab that is a bitwise no-op except that its box reads halo rows
+// goes to TileArgs::cond_tiles; peer_wait_kernel lists it only if the neighbour's pushed
+// rows hold a bit other than +0.0 in its box columns (PeerBox::halo_nz, tp_peer.cu).
 constexpr int kMaxTileCols = 2048;  // halo_nz entries per side (ncols <= 32768)
 
 // Dry-tile classification before a stage.  flag_in: per-tile flags of the stage's input
@@ -164,7 +162,9 @@ struct TileArgs {
     const unsigned char* inflow_tiles;  // per tile: its box reads a Mode-II inflow ghost (never skip, never safe); may be null
     int south_ineligible, north_ineligible;  // slab edges next to halo rows: never skip
     int safe_ok;          // FASTDIV on, geometry and constants inside the safe-window bounds (tp_capi.cpp)
-    int cond_halo;        // peer-joined slab: halo-reaching tiles that are otherwise no-ops are listed kTileCond
+    int cond_halo;        // peer-joined slab: halo-reaching tiles that are otherwise no-ops go to cond_tiles
+    int* cond_tiles;      // their list (consumed and reset by peer_wait_kernel)
+    int* ncond;
     int loop;
     DevScalars* sc;
 };
@@ -214,6 +214,15 @@ struct PeerBox {
 };
 // Where this slab's neighbours live (pointers valid in this process: own allocations,
 // allocations of contexts in this process, or CUDA-IPC mappings of other processes').
+// peer_wait_kernel's filter of the conditional tiles of one stage
+struct CondArgs {
+    int* tiles;           // the stage's active-tile list (TileArgs::tiles)
+    int* ntiles_active;
+    const int* cond_tiles;
+    int* ncond;           // reset to 0 after the filter
+    double* tally;        // the stage's ring tally (skipped ring tiles write zeros)
+    int ntx, nty, nyi;
+};
 struct PeerLink {
     double* nbr_state[2][2];     // [buf A/B][side 0 = rank-1 (south), 1 = rank+1 (north)]; null = none
     long long nbr_fs[2];
