@@ -50,9 +50,10 @@ __device__ __forceinline__ void face_flux(const double (&L)[6], const double (&R
         celL = sqrt(P.eps * cf * smax(htL, 0.0));
         celR = sqrt(P.eps * cf * smax(htR, 0.0));
     } else {  // safe tile: the argument is +-0 or >= 2^-274, so the branch-free sequence is IEEE sqrt
+        // (and htL, htR are +0 or positive: max(h, 0.0) is h itself, see below)
         bool oks = true;
-        celL = dsqrt_fast(P.eps * cf * smax(htL, 0.0), oks);
-        celR = dsqrt_fast(P.eps * cf * smax(htR, 0.0), oks);
+        celL = dsqrt_fast(P.eps * cf * htL, oks);
+        celR = dsqrt_fast(P.eps * cf * htR, oks);
     }
     // normal / transverse momenta (solver.cpp:259-262)
     const double qnL0 = XI ? L[2] : L[3], qtL0 = XI ? L[3] : L[2];
@@ -69,8 +70,12 @@ __device__ __forceinline__ void face_flux(const double (&L)[6], const double (&R
         dfix<FD>(jL1, qnL1, rj);
         dfix<FD>(jR1, qnR1, rj);
     }
-    const double dL0 = smax(hL0, 0.0), dR0 = smax(hR0, 0.0);
-    const double dL1 = smax(hL1, 0.0), dR1 = smax(hR1, 0.0);
+    // safe tile (CHK = false): every thickness of the box is +-0 or positive (TF_UNSAFE2), so
+    // each minmod edge value uc + (+-0.5)*slope is +0 or positive (a nonzero slope has the sign
+    // of both differences, so the exact sum is >= 0; a zero slope or uc = -0 gives +0), and so
+    // are hL = edge / jbf and htL = hL0 + hL1: std::max(h, 0.0) returns h bit for bit
+    const double dL0 = CHK ? smax(hL0, 0.0) : hL0, dR0 = CHK ? smax(hR0, 0.0) : hR0;
+    const double dL1 = CHK ? smax(hL1, 0.0) : hL1, dR1 = CHK ? smax(hR1, 0.0) : hR1;
     double fL0, fR0, fL1, fR1;
     if (FD) {  // four desingularisation divisions, one shared slow-path branch
         bool okf = true;

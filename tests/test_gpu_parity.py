@@ -236,6 +236,25 @@ def test_signed_zero_state(gpu, oracle_kind):
     assert_bitwise(sim.state(), ref.state(), "state with signed zeros")
 
 
+def test_signed_zero_thickness_in_wet_region(gpu, oracle_kind):
+    """-0.0 thickness cells beside wet ones (allowed in safe tiles): the safe-tile face code
+    relies on every minmod edge of a non-negative thickness field being +0 or positive."""
+    sc = scenarios.wet_valley(64, 60)
+    ref, sim = _pair(sc, oracle_kind)
+    s = ref.state()
+    s[0:2, 20:24, 10:50] = -0.0
+    s[2:, 20:24, 10:50] = -0.0
+    s[1, 40:42, 30:33] = -0.0
+    ref.set_state(s)
+    sim.set_state(s)
+    for k in range(3):
+        tr, dts_r, _ = ref.steps(0.0 if k == 0 else tr, 1.0e9, 15, t_end=1.0e9)
+        tg, dts_g, _ = sim.steps(0.0 if k == 0 else tg, 1.0e9, 15, t_end=1.0e9, record_dts=True)
+        assert_bitwise(dts_g, dts_r, f"dt sequence {k}")
+        assert_bitwise(sim.state(), ref.state(), f"state after leg {k}")
+    assert sim.safe_tiles() > 0
+
+
 def test_safe_window_edges(gpu, oracle_kind):
     """Values outside the safe-tile window (nonzero magnitudes below 2^-200 or
     at/above 2^200, subnormals) mark their tile and its neighbours unsafe, which then take
