@@ -79,10 +79,11 @@ __device__ __forceinline__ void face_flux(const double (&L)[6], const double (&R
     double fL0, fR0, fL1, fR1;
     if (FD) {  // four desingularisation divisions, one shared slow-path branch
         bool okf = true;
-        fL0 = desing_factor_g<CHK>(dL0, P.eps_h, okf);
-        fR0 = desing_factor_g<CHK>(dR0, P.eps_h, okf);
-        fL1 = desing_factor_g<CHK>(dL1, P.eps_h, okf);
-        fR1 = desing_factor_g<CHK>(dR1, P.eps_h, okf);
+        // safe tile: the d's are +0 or positive (above), so no signed-zero select is needed
+        fL0 = desing_factor_g<CHK, !CHK>(dL0, P.eps_h, okf);
+        fR0 = desing_factor_g<CHK, !CHK>(dR0, P.eps_h, okf);
+        fL1 = desing_factor_g<CHK, !CHK>(dL1, P.eps_h, okf);
+        fR1 = desing_factor_g<CHK, !CHK>(dR1, P.eps_h, okf);
         if (!okf) {
             fL0 = desing_factor<FD>(dL0, P.eps_h);
             fR0 = desing_factor<FD>(dR0, P.eps_h);
