@@ -101,7 +101,11 @@ __device__ __forceinline__ void face_flux(const double (&L)[6], const double (&R
     const double vnL1 = jL1 * fL1;
     const double vnR1 = jR1 * fR1;
     double a = 0.0;
-    a = smax(a, smax(fabs(vnL0) + celL, fabs(vnR0) + celR));
+    if (CHK) {
+        a = smax(a, smax(fabs(vnL0) + celL, fabs(vnR0) + celR));
+    } else {  // safe tile: |v| + cel is +0 or positive and never NaN, so max(0.0, x) is x bit for bit
+        a = smax(fabs(vnL0) + celL, fabs(vnR0) + celR);
+    }
     a = smax(a, smax(fabs(vnL1) + celL, fabs(vnR1) + celR));
 
     // solver.cpp:288-296
