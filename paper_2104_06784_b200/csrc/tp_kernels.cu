@@ -157,8 +157,9 @@ __device__ __forceinline__ unsigned long long cell_epilogue(double (&un)[6], con
         bits |= static_cast<unsigned long long>(__double_as_longlong(un[f]));
         inwin2 = inwin2 && in_safe_window2(un[f]);
     }
-    // window B also needs non-negative thicknesses (no cancellation in hs + hf)
-    inwin2 = inwin2 && (__double2hiint(un[0]) >= 0 || un[0] == 0.0) && (__double2hiint(un[1]) >= 0 || un[1] == 0.0);
+    // window B also needs thicknesses that are +0 or positive (no cancellation in hs + hf;
+    // no -0, so the safe forms can drop the signed-zero selects)
+    inwin2 = inwin2 && __double2hiint(un[0]) >= 0 && __double2hiint(un[1]) >= 0;
     safe2_out = inwin2;
     return bits;  // feeds the tile's output flags
 }
@@ -235,7 +236,8 @@ __device__ __forceinline__ void stage_phase1(const double* __restrict__ S, const
             }
             const double h = hs + hf;
             double fsld, fflu;
-            desing_pair<FD, CHK>(hs, hf, P.eps_h, fsld, fflu);
+            // safe tile: thicknesses are +0 or positive (TF_UNSAFE2 excludes -0), so are hs, hf
+            desing_pair<FD, CHK, !CHK>(hs, hf, P.eps_h, fsld, fflu);
             V[0 * BOX + k] = jsx * fsld;
             V[1 * BOX + k] = jsy * fsld;
             V[2 * BOX + k] = jfx * fflu;

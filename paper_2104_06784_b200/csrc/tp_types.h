@@ -125,7 +125,7 @@ struct StageArgs {
 // Per-tile output flags: which regions of the tile's interior hold a value with a nonzero
 // bit (the 2-cell bands and 2x2 corners are what a neighbour's radius-2 box reads).
 // TF_UNSAFE2: some output value is neither +-0 nor of magnitude in [2^-100, 2^100), or a
-// thickness is negative (the "safe tile" window, DESIGN.md §3 item 6).
+// thickness is negative or -0 (the "safe tile" window, DESIGN.md §3 item 6).
 enum TileFlag : unsigned {
     TF_ANY = 1u, TF_W = 2u, TF_E = 4u, TF_S = 8u, TF_N = 16u,
     TF_SW = 32u, TF_SE = 64u, TF_NW = 128u, TF_NE = 256u, TF_UNSAFE2 = 1024u,
