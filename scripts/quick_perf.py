@@ -23,6 +23,6 @@ t1 = time.perf_counter()
 t, n_, hit = sim.steps(t, 1e9, steps, t_end=1e9)
 sim.synchronize()
 t2 = time.perf_counter()
-cu = sc.ncols * sc.nrows * n_ / (t2 - t1)
-print(f"k{os.environ.get('TP_KERNEL','d')} {name} {sc.ncols}x{sc.nrows} fastdiv={fastdiv} steps={n_} {1e3*(t2-t1)/n_:.3f} ms/step  {cu/1e9:.3f} GCUPS  "
+cu = sc.ncols * sc.nrows * n_ / (t2 - t1) if n_ else 0.0
+print(f"k{os.environ.get('TP_KERNEL','d')} {name} {sc.ncols}x{sc.nrows} fastdiv={fastdiv} steps={n_} {1e3*(t2-t1)/max(n_, 1):.3f} ms/step  {cu/1e9:.3f} GCUPS  "
       f"HBM-frac {cu*464/6449.1e9:.3f}  launches={sim.kernel_launches()}")
