@@ -15,7 +15,6 @@ t0 = time.time()
 sim = Simulator.from_scenario(sc, fastdiv=bool(fastdiv))
 sim.set_option("graph_steps", gs)
 import os
-if os.environ.get("TP_KERNEL"): sim.set_option("kernel", int(os.environ["TP_KERNEL"]))
 print(f"setup {time.time()-t0:.2f}s  grid {sc.ncols}x{sc.nrows} wet frac {np.mean(sc.h0 > 0) if sc.h0 is not None else 0:.3f}")
 t, n_, hit = sim.steps(0.0, 1e9, 8, t_end=1e9)   # warmup
 sim.synchronize()
@@ -24,5 +23,5 @@ t, n_, hit = sim.steps(t, 1e9, steps, t_end=1e9)
 sim.synchronize()
 t2 = time.perf_counter()
 cu = sc.ncols * sc.nrows * n_ / (t2 - t1) if n_ else 0.0
-print(f"k{os.environ.get('TP_KERNEL','d')} {name} {sc.ncols}x{sc.nrows} fastdiv={fastdiv} steps={n_} {1e3*(t2-t1)/max(n_, 1):.3f} ms/step  {cu/1e9:.3f} GCUPS  "
+print(f"{name} {sc.ncols}x{sc.nrows} fastdiv={fastdiv} steps={n_} {1e3*(t2-t1)/max(n_, 1):.3f} ms/step  {cu/1e9:.3f} GCUPS  "
       f"HBM-frac {cu*464/6449.1e9:.3f}  launches={sim.kernel_launches()}")
