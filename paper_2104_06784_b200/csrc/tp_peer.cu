@@ -168,7 +168,7 @@ __global__ void peer_wait_kernel(PeerLink L, DevScalars* sc, int buf, CondArgs c
             sc->done = 1;
         }
     }
-    __syncthreads();
+    __syncwarp();  // one warp: nothing else of the CTA sits at a barrier while lanes 0/1 spin
     const int n = *ca.ncond;
     for (int i = threadIdx.x; live && i < n; i += blockDim.x) {
         const int e = ca.cond_tiles[i];
@@ -188,7 +188,7 @@ __global__ void peer_wait_kernel(PeerLink L, DevScalars* sc, int buf, CondArgs c
             atomicAdd(&sc->cond_skips, 1ull);
         }
     }
-    __syncthreads();
+    __syncwarp();
     if (threadIdx.x == 0) *ca.ncond = 0;
 }
 
@@ -201,7 +201,7 @@ cudaError_t launch_peer_halo(const PeerLink& L, const GridDesc& g, const double*
     peer_halo_push_kernel<<<dim3(16, 2), 256, 0, st>>>(L, g, s, buf, sc);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    peer_wait_kernel<<<1, 256, 0, st>>>(L, sc, buf, ca);
+    peer_wait_kernel<<<1, 32, 0, st>>>(L, sc, buf, ca);
     return cudaGetLastError();
 }
 
