@@ -244,6 +244,17 @@ void build_phys(tp_ctx* c) {
     P.r_NR = 1.0 / P.N_R;
     P.adv_only = c->adv_only;
     P.cap_on = !(c->adv_only || P.tan_d == 0.0) ? 1 : 0;  // solver.cpp:454
+    // mkrcp_const's divisor test (tp_math.cuh): b positive in [2^-200, 2^200]
+    auto window = [](double b) {
+        uint64_t u;
+        std::memcpy(&u, &b, sizeof(u));
+        const unsigned eb = static_cast<unsigned>(u >> 52);
+        return (eb - (1023u - 200u)) <= 400u ? 1 : 0;
+    };
+    P.ok_dxi = window(P.dxi);
+    P.ok_deta = window(P.deta);
+    P.ok_two_dxi = window(P.two_dxi);
+    P.ok_two_deta = window(P.two_deta);
 }
 
 void drop_graphs(tp_ctx* c) {

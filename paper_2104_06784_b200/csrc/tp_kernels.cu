@@ -362,8 +362,8 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
     // ---- Phase 2: (a) the cell-local source terms of this thread's Phase-3 cell
     // (solver.cpp:406-445 minus the viscous divergence, which needs neighbours'
     // brackets) and (b) the viscous brackets of the tile's cross neighbours.
-    const Rcp r2x = mkrcp_const<FD>(P.two_dxi, P.r_two_dxi);
-    const Rcp r2y = mkrcp_const<FD>(P.two_deta, P.r_two_deta);
+    const Rcp r2x{P.two_dxi, P.r_two_dxi, FD && P.ok_two_dxi != 0};  // window tested on the host
+    const Rcp r2y{P.two_deta, P.r_two_deta, FD && P.ok_two_deta != 0};
     // partial rhs sums in the reference's order: rhs[2] = div + ((sn + sf) + sv),
     // rhs[4] = div + ((((sn + sd) + sf) + sv) + svis)  (solver.cpp:442-445)
     double Ps2 = 0.0, Ps3 = 0.0, Pf4 = 0.0, Pf5 = 0.0, visc = 0.0;
@@ -531,8 +531,8 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
 
     // ---- Phase 3: divergence + viscous source + update + cap + [average] +
     //      regularize + [finite, lambda]
-    const Rcp rdx = mkrcp_const<FD>(P.dxi, P.r_dxi);
-    const Rcp rdy = mkrcp_const<FD>(P.deta, P.r_deta);
+    const Rcp rdx{P.dxi, P.r_dxi, FD && P.ok_dxi != 0};  // window tested on the host
+    const Rcp rdy{P.deta, P.r_deta, FD && P.ok_deta != 0};
     unsigned long long obits = 0ull;
     bool osafe2 = true;
     if (p3) {

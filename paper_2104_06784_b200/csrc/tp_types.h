@@ -24,6 +24,8 @@ struct Phys {
     double cfl;
     // RN(1/x) of the constant divisors (FASTDIV)
     double r_dxi, r_deta, r_two_dxi, r_two_deta, r_eps_NR, r_NR;
+    // FASTDIV divisor window of the four grid constants (mkrcp_const's test, evaluated once)
+    int ok_dxi, ok_deta, ok_two_dxi, ok_two_deta;
     int adv_only;      // Simulator::set_advection_only (solver.hpp:60-62)
     int cap_on;        // !(adv_only || tan_delta_b() == 0.0)  (solver.cpp:454)
 };
