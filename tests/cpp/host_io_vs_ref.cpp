@@ -1,5 +1,6 @@
 // TEST (CPU): tpflow_b200's host I/O against the UNMODIFIED reference (tpflow::, oracle/_ref
 // objects) in one process — parsed values, error messages and written file bytes must match.
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <fstream>
@@ -136,6 +137,40 @@ int main(int argc, char** argv) {
     const std::string cr = tpflow::io::write_contour_csv(sr, demr, dr), cb = tpflow_b200::io::write_contour_csv(sb, demb, db);
     EXPECT(slurp(cr) == slurp(cb), "contour csv bytes");
     EXPECT(tpflow::io::time_tag(181.82) == tpflow_b200::io::time_tag(181.82), "time tag");
+    {
+        // a grid large enough for the multi-threaded writers (row blocks on every host thread)
+        const int NC = 211, NR = 157;
+        std::string text = "ncols " + std::to_string(NC) + "\nnrows " + std::to_string(NR) +
+                           "\nxllcorner 100.5\nyllcorner -20\ncellsize 2.5\nnodata_value -9999\n";
+        for (int j = 0; j < NR; ++j) {
+            for (int i = 0; i < NC; ++i) text += std::to_string((i * 7 + j * 3) % 50) + (i + 1 < NC ? " " : "\n");
+        }
+        tpflow::ElevationGrid gr = tpflow::parse_dem_text(text, "big");
+        tpflow_b200::ElevationGrid gb = tpflow_b200::parse_dem_text(text, "big");
+        tpflow::SimSnapshot br; tpflow_b200::SimSnapshot bb;
+        br.t = bb.t = 3600.0;
+        tpflow::Field* gfr[6] = {&br.h_total, &br.phi_s, &br.vX_s, &br.vY_s, &br.vX_f, &br.vY_f};
+        tpflow_b200::Field* gfb[6] = {&bb.h_total, &bb.phi_s, &bb.vX_s, &bb.vY_s, &bb.vX_f, &bb.vY_f};
+        unsigned long long r = 2104;
+        for (int k = 0; k < 6; ++k) {
+            *gfr[k] = tpflow::Field(NC, NR); *gfb[k] = tpflow_b200::Field(NC, NR);
+            for (int j = 0; j < NR; ++j)
+                for (int i = 0; i < NC; ++i) {
+                    r = r * 6364136223846793005ull + 1442695040888963407ull;
+                    const double u = static_cast<double>(r >> 11) * (1.0 / 9007199254740992.0);
+                    const double v = (i + j) % 17 == 0 ? -0.0 : (u - 0.4) * std::pow(10.0, (k + i) % 9 - 4);
+                    (*gfr[k])(i, j) = (*gfb[k])(i, j) = v;
+                }
+        }
+        const std::string dr2 = dir + "/ref_big", db2 = dir + "/b200_big";
+        if (std::system(("mkdir -p " + dr2 + " " + db2).c_str()) != 0) std::fprintf(stderr, "mkdir failed\n");
+        auto qr = tpflow::io::write_snapshot(br, gr, dr2);
+        auto qb = tpflow_b200::io::write_snapshot(bb, gb, db2);
+        for (std::size_t k = 0; k < qr.size() && k < qb.size(); ++k)
+            EXPECT(slurp(qr[k]) == slurp(qb[k]) && !slurp(qr[k]).empty(), ("large snapshot bytes " + qr[k]).c_str());
+        EXPECT(slurp(tpflow::io::write_contour_csv(br, gr, dr2)) == slurp(tpflow_b200::io::write_contour_csv(bb, gb, db2)),
+               "large contour csv bytes");
+    }
     std::printf("%s: %d failures\n", argv[0], failures);
     return failures ? 1 : 0;
 }
