@@ -16,7 +16,8 @@ pytestmark = pytest.mark.gpu
                                   lambda: scenarios.c3_channel(80, 48, t_end=30.0, dt_out=0.5),
                                   lambda: scenarios.wet_valley(96, 70),
                                   lambda: scenarios.moving_release(70, 52),
-                                  lambda: scenarios.four_side_inflow(48, 40)])
+                                  lambda: scenarios.four_side_inflow(48, 40),
+                                  lambda: scenarios.four_side_inflow(49, 46)])
 def test_cuda_slabs_equal_single_device(gpu, oracle_kind, make, parts):
     import torch
     from oracle.oracle import OracleSim
@@ -40,7 +41,8 @@ def test_cuda_slabs_equal_single_device(gpu, oracle_kind, make, parts):
                                   lambda: scenarios.c3_channel(80, 48, t_end=30.0, dt_out=0.5),
                                   lambda: scenarios.wet_valley(96, 70),
                                   lambda: scenarios.moving_release(70, 52),
-                                  lambda: scenarios.four_side_inflow(48, 40)])
+                                  lambda: scenarios.four_side_inflow(48, 40),
+                                  lambda: scenarios.four_side_inflow(49, 46)])
 def test_peer_slabs_equal_single_device(gpu, oracle_kind, make, parts):
     """Device-resident exchange (tp_peer.cu): halo rows stored into the neighbours'
     buffers and lambda reduced in device memory inside the step graphs."""
