@@ -517,3 +517,68 @@ def test_regularize_clips_small_negatives(gpu, oracle_kind):
     tg, dts_g, _ = sim.steps(0.0, 1.0e9, 20, t_end=1.0e9, record_dts=True)
     assert_bitwise(dts_g, dts_r, "dt sequence")
     assert_bitwise(sim.state(), ref.state(), "state after 20 steps")
+
+
+def _fuzz_scenario(seed):
+    """A random small scenario: grid shape, terrain, release or four-side inflow, parameters."""
+    from paper_2104_06784_b200.config import Hydrograph, SimConfig
+    rng = np.random.default_rng(9000 + seed)
+    nc, nr = int(rng.integers(3, 75)), int(rng.integers(2, 70))
+    cs = float(rng.choice([1.0, 2.5, 5.0, 10.0]))
+    z = scenarios.fractal_dem(nc, nr, cs, seed=int(rng.integers(1, 10_000)), relief=float(rng.uniform(5, 200)),
+                              slope_deg=float(rng.uniform(0, 25)))
+    inflow = bool(rng.integers(0, 2))
+    cfg = SimConfig(mode="inflow" if inflow else "release", t_end=float(rng.uniform(5, 40)), dt_out=float(rng.uniform(0.3, 3)))
+    p = cfg.params
+    p.delta_b, p.C_d, p.N_R = float(rng.uniform(5, 35)), float(rng.uniform(0, 10)), float(rng.uniform(20, 800))
+    p.theta_b, p.phi_s0, p.alpha_rho = float(rng.uniform(0, 10)), float(rng.uniform(0.2, 0.8)), float(rng.uniform(0.2, 1.0))
+    cfg.cfl = float(rng.uniform(0.05, 0.125))
+    if inflow:
+        cells = []
+        for side in ("W", "E", "S", "N"):
+            if rng.integers(0, 2):
+                n_side = nr if side in "WE" else nc
+                a = int(rng.integers(0, n_side))
+                b = min(n_side, a + int(rng.integers(1, 6)))
+                for k in range(a, b):
+                    cells.append({"W": (0, k, "W"), "E": (nc - 1, k, "E"), "S": (k, 0, "S"), "N": (k, nr - 1, "N")}[side])
+        if not cells:
+            cells = [(0, 0, "W")]
+        t1 = float(rng.uniform(2, 20))
+        samples = [(0.0, float(rng.uniform(0, 1)), 0.5, 1.0), (t1, float(rng.uniform(0.5, 4)), float(rng.uniform(0.3, 0.7)),
+                                                               float(rng.uniform(0, 6))), (2 * t1, 0.0, 0.5, 0.0)]
+        return scenarios.Scenario(f"fuzz{seed}", z, cs, cfg, hydrograph=Hydrograph(cells=cells, samples=samples))
+    h0 = scenarios.paraboloid_release(nc, nr, h0=float(rng.uniform(0.5, 10)), rx=max(1.0, nc * rng.uniform(0.1, 0.5)),
+                                      ry=max(1.0, nr * rng.uniform(0.1, 0.5)), cx=nc * rng.uniform(0.2, 0.8),
+                                      cy=nr * rng.uniform(0.2, 0.8))
+    return scenarios.Scenario(f"fuzz{seed}", z, cs, cfg, h0=h0)
+
+
+@pytest.mark.parametrize("seed", list(range(40)))
+def test_fuzz_scenarios_bitwise(gpu, oracle_kind, seed):
+    """Random small scenarios (shape, terrain, release or inflow on random sides, parameters)
+    through the run loop's output schedule: every dt and the final state bit-identical."""
+    sc = _fuzz_scenario(seed)
+    ref, sim = _pair(sc, oracle_kind)
+    tu = sc.config.scaling.t_unit()
+    t_end, dt_out = sc.config.t_end / tu, sc.config.dt_out / tu
+    t_r = t_g = 0.0
+    k, done = 1, 0
+    from oracle.oracle import OracleError
+    while done < 150 and t_r < t_end:
+        t_next = min(k * dt_out, t_end)
+        try:
+            t_r, dts_r, hit_r = ref.steps(t_r, t_next, 150 - done, t_end=t_end)
+        except OracleError as er:  # the reference itself stops (e.g. regularize): same error here
+            with pytest.raises(NumericsError) as eg:
+                sim.steps(t_g, t_next, 150 - done, t_end=t_end)
+            assert str(eg.value) == str(er)
+            return
+        t_g, dts_g, hit_g = sim.steps(t_g, t_next, 150 - done, t_end=t_end, record_dts=True)
+        assert_bitwise(np.asarray(dts_g), np.asarray(dts_r), f"dts interval {k}")
+        assert t_r == t_g
+        done += len(dts_r)
+        if hit_r:
+            k += 1
+    assert_bitwise(sim.state(), ref.state(), f"state ({sc.ncols}x{sc.nrows}, {sc.config.mode})")
+    np.testing.assert_allclose(sim.audit_array(), ref.audit(), rtol=1e-11, atol=1e-300)
