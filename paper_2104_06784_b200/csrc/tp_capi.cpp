@@ -623,6 +623,10 @@ void create_impl(tp_ctx* c, const tp_params* p, const tp_dem* dem, int row0, int
     if (!(dem->cellsize > 0.0)) throw ConfigErr{"cellsize must be positive"};
     if (row0 < 0 || row1 > dem->nrows || row1 - row0 < 2)
         throw ConfigErr{"slab rows out of range (need at least 2 rows)"};
+    // active-tile list entries pack (tile row << 16) | tile column, 13 + 16 bits
+    if (dem->ncols > tpb::TX * 65535 || row1 - row0 > tpb::TY * 8191)
+        throw ConfigErr{"grid too large for one context (at most " + std::to_string(tpb::TX * 65535) + " columns and " +
+                        std::to_string(tpb::TY * 8191) + " rows per slab)"};
     c->p = *p;
     c->device = p->device;
     ck(cudaSetDevice(c->device), "cudaSetDevice");
