@@ -1275,6 +1275,11 @@ void peer_finish(tp_ctx* c, int rank, int nranks) {
     c->link.rank = rank;
     c->link.nranks = nranks;
     c->link.my_box = c->dBox;
+    {
+        const char* e = std::getenv("TPFLOW_PEER_TIMEOUT_S");
+        const double sec = e ? std::atof(e) : 60.0;
+        c->link.timeout_ns = static_cast<unsigned long long>((sec > 0.0 ? sec : 60.0) * 1e9);
+    }
     c->peered = nranks > 1;
     c->peer_base = 0;
     ck(cudaMemsetAsync(c->dBox, 0, sizeof(tpb::PeerBox), c->stream), "memset");

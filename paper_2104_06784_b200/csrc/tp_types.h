@@ -233,6 +233,7 @@ struct PeerLink {
     PeerBox* box[kMaxRanks];     // every rank's mailbox (lambda all-reduce)
     PeerBox* my_box;
     int rank, nranks;
+    unsigned long long timeout_ns;  // a wait without progress this long reports an error (TPFLOW_PEER_TIMEOUT_S, default 60)
 };
 
 }  // namespace tpb

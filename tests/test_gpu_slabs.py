@@ -73,12 +73,13 @@ def _peer_rank_main(rank, world, port, make_name, steps, outdir):
     import torch
     import torch.distributed as dist
     from paper_2104_06784_b200.distributed import CudaSlab, decompose, peer_connect_ranks
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), TPFLOW_PEER_TIMEOUT_S="10")
     dist.init_process_group("gloo", rank=rank, world_size=world)
     torch.cuda.set_device(0)
     sc = _MAKERS[make_name]()
     slab = CudaSlab(sc, decompose(sc.nrows, world)[rank], stream=torch.cuda.Stream())
     peer_connect_ranks(slab)
+    dist.barrier()  # start the exchanges together (one GPU time-sliced between the ranks)
     t_next = 0.5 / sc.config.scaling.t_unit() if sc.config.inflow else 1e9
     t, n, hit = slab.sim.steps(0.0, t_next, steps, t_end=1e9)
     np.save(os.path.join(outdir, f"state{rank}.npy"), slab.state())
@@ -101,9 +102,9 @@ def test_peer_two_processes_ipc(gpu, oracle_kind, make_name, tmp_path):
     from oracle.oracle import OracleSim
     steps = 4
     # Two contexts time-slicing one GPU: a context whose wait kernel spins can occasionally
-    # hold the GPU long enough for the 60 s exchange timeout to fire (never with one GPU per
-    # rank); such a run is repeated, any other failure is not.
-    for attempt in range(3):
+    # hold the GPU long enough for the exchange timeout (10 s here) to fire (never with one
+    # GPU per rank); such a run is repeated, any other failure is not.
+    for attempt in range(6):
         with socket.socket() as so:
             so.bind(("127.0.0.1", 0))
             port = so.getsockname()[1]
@@ -112,7 +113,7 @@ def test_peer_two_processes_ipc(gpu, oracle_kind, make_name, tmp_path):
                                start_method="spawn")
             break
         except mp.ProcessRaisedException as e:
-            if "did not arrive within the timeout" not in str(e) or attempt == 2:
+            if "did not arrive within the timeout" not in str(e) or attempt == 5:
                 raise
     sc = _MAKERS[make_name]()
     ref = OracleSim(sc, oracle_kind)
