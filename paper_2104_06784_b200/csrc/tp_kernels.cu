@@ -640,7 +640,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
                     if (FD) {
                         bool okq = true;
                         frac = ddiv_fast(num, qnorm, okq);
-                        if (!okq) frac = num / qnorm;
+                        if (!okq) frac = div_ieee_slow(num, qnorm);  // rare: out of line
                     } else {
                         frac = num / qnorm;
                     }
