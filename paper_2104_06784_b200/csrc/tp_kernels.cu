@@ -71,6 +71,35 @@ __device__ __forceinline__ bool in_safe_window2(double x) {
     return ((hi2 - ((1023u - 100u) << 21)) < (200u << 21)) | ((hi2 | lo) == 0u);
 }
 
+// Boundary mass tally of one ring tile (solver.cpp:352-376), phase p = solid / fluid:
+// outward-positive mass flux through the physical edges of the tile, times dt/2.
+static __device__ __noinline__ void ring_tally(const double* FX, const double* FY, int X0, int Y0, int nx, int ny,
+                                               int has_south, int has_north, double dxi, double deta, double dt,
+                                               double* t, int p) {
+    const bool w_edge = X0 == 3;
+    const bool e_edge = (nx - 4) >= X0 && (nx - 4) < X0 + TX;
+    const bool s_edge = has_south && Y0 == 3;
+    const bool n_edge = has_north && (ny - 4) >= Y0 && (ny - 4) < Y0 + TY;
+    const double wdt = dt * 0.5;  // weight_dt = dt / 2.0 (solver.cpp:512, :526)
+    double in = 0.0, outf = 0.0;
+    auto add = [&](double outward) {
+        if (outward >= 0.0) outf += outward;
+        else in += -outward;
+    };
+    const int fxE = nx - 3 - X0;  // xi face index of the east boundary face
+    for (int ty = 0; ty < TY && Y0 + ty <= ny - 4; ++ty) {
+        if (w_edge) add(-FX[p * NFX + ty * (TX + 1) + 0] * deta * wdt);
+        if (e_edge) add(FX[p * NFX + ty * (TX + 1) + fxE] * deta * wdt);
+    }
+    const int fyN = ny - 3 - Y0;
+    for (int tx = 0; tx < TX && X0 + tx <= nx - 4; ++tx) {
+        if (s_edge) add(-FY[p * NFY + 0 * TX + tx] * dxi * wdt);
+        if (n_edge) add(FY[p * NFY + fyN * TX + tx] * dxi * wdt);
+    }
+    t[2 * p + 0] = in;
+    t[2 * p + 1] = outf;
+}
+
 // regularize + [check_finite + lambda] + store of one updated cell: the tail of
 // advance_step's stages (solver.cpp:139-166, :482-494, :556-573).
 template <bool FD, bool CORR>
@@ -665,34 +694,10 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
     }
 
     // ---- boundary mass tally of this stage (solver.cpp:352-376), ring tiles only
-    const bool w_edge = X0 == 3;
-    const bool e_edge = (nx - 4) >= X0 && (nx - 4) < X0 + TX;
-    const bool s_edge = g.has_south && Y0 == 3;
-    const bool n_edge = g.has_north && (ny - 4) >= Y0 && (ny - 4) < Y0 + TY;
-    const bool ring = tix == 0 || tix == A.ntx - 1 || tiy == 0 ||
-                      tiy == A.nty - 1;  // every ring tile writes its slot (zeros if no edge)
-    if (ring && threadIdx.x < 2) {
-        const int p = threadIdx.x;
-        const double wdt = dt * 0.5;  // weight_dt = dt / 2.0 (solver.cpp:512, :526)
-        double in = 0.0, outf = 0.0;
-        auto add = [&](double outward) {
-            if (outward >= 0.0) outf += outward;
-            else in += -outward;
-        };
-        const int fxE = nx - 3 - X0;  // xi face index of the east boundary face
-        for (int ty = 0; ty < TY && Y0 + ty <= ny - 4; ++ty) {
-            if (w_edge) add(-FX[p * NFX + ty * (TX + 1) + 0] * P.deta * wdt);
-            if (e_edge) add(FX[p * NFX + ty * (TX + 1) + fxE] * P.deta * wdt);
-        }
-        const int fyN = ny - 3 - Y0;
-        for (int tx = 0; tx < TX && X0 + tx <= nx - 4; ++tx) {
-            if (s_edge) add(-FY[p * NFY + 0 * TX + tx] * P.dxi * wdt);
-            if (n_edge) add(FY[p * NFY + fyN * TX + tx] * P.dxi * wdt);
-        }
-        double* t = A.tally + 4ll * tile;
-        t[2 * p + 0] = in;
-        t[2 * p + 1] = outf;
-    }
+    // (every ring tile writes its slot, zeros if no edge; out of line: a few tiles only)
+    if ((tix == 0 || tix == A.ntx - 1 || tiy == 0 || tiy == A.nty - 1) && threadIdx.x < 2)
+        ring_tally(FX, FY, X0, Y0, nx, ny, g.has_south, g.has_north, P.dxi, P.deta, dt,
+                   A.tally + 4ll * tile, static_cast<int>(threadIdx.x));
     // the tile's output flags: warp OR, one shared atomic per warp; the end-of-tile
     // barrier (FX/FY/V/PJ/BR/cell box are rewritten by the next tile) publishes them
     {
