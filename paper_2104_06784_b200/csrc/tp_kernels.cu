@@ -373,6 +373,9 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
             tma_load_3d(sm + SM_G, &A.tm_g, bx0n + 1, by0n, 0, &bar);
         }
     };
+    // corrector: u^n of this tile into L2 now; its shared-memory copy (after Phase 2, into the
+    // then dead V region) is waited for in Phase 3
+    if (CORR && threadIdx.x == 0) tma_prefetch_3d(&A.tm_u, X0 + 1, Y0, 0);
     TPROBE(0);  // loop-top bookkeeping
     mbar_wait(&bar, iter & 1u);
     TPROBE(1);  // wait for the state/geometry boxes

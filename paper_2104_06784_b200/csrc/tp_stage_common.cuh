@@ -84,6 +84,13 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phas
         "r"(phase)
         : "memory");
 }
+// TMA prefetch of a 3-D box into L2 (no shared-memory destination, no barrier)
+__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* tm, int x, int y, int z) {
+    asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
+                     reinterpret_cast<unsigned long long>(tm)),
+                 "r"(x), "r"(y), "r"(z)
+                 : "memory");
+}
 __device__ __forceinline__ void prefetch_l2(const void* p) {
     asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
