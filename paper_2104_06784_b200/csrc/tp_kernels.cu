@@ -242,7 +242,9 @@ __device__ __forceinline__ void stage_phase1(const double* __restrict__ S, const
             for (int f = 0; f < 6; ++f) FY[f * NFY + it] = oy[f];
         }
     }
-    for (int k = threadIdx.x; k < BOX; k += NT) {
+    // box cell k = (thread ^ 128) + pass * NT: the BOX - NT cells of the second pass go to
+    // warps 4-7, as the second bracket pass of Phase 2 goes to warps 0-1
+    for (int k = threadIdx.x ^ 128; k < BOX; k += NT) {
         {
             // cell fields (solver.cpp:172-184) on box cell k
             if (P.adv_only) continue;  // velocities/pjb feed sources and brackets only
