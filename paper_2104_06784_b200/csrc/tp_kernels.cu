@@ -204,7 +204,9 @@ __device__ __forceinline__ void stage_phase1(const double* __restrict__ S, const
     // faces: thread t owns xi face t and eta face t, written as one straight-line
     // block so the two independent dependency chains interleave (ILP)
     {
-        const int it = threadIdx.x;
+        // face index: the 15 last xi faces of the rows (a conflicted column walk) on warp 0,
+        // which carries no second cell pass (that is warps 4-7)
+        const int it = (threadIdx.x + TX * TY) & (NT - 1);
         const bool hx = it < NFX, hy = it < NFY;
         // xi faces: threads 0..TX*TY-1 take faces 0..TX-1 of each row (a warp = two 16-face
         // row segments: conflict-free 8-byte smem loads; a 17-face row walk cost 1.5x the
