@@ -369,7 +369,7 @@ def main():
     ap.add_argument("--nrows", type=int, default=2048)
     ap.add_argument("--graph-steps", type=int, default=16)
     ap.add_argument("--roofline-reps", type=int, default=20)
-    ap.add_argument("--cpu-steps", type=int, default=6)
+    ap.add_argument("--cpu-steps", type=int, default=60)  # ~10 s of the reference on 16 cores at C2
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
