@@ -147,6 +147,7 @@ class RunClock:
         self.t_end = sim.cfg.t_end / tu
         self.dt_out = sim.cfg.dt_out / tu
         self.next_out = self.dt_out
+        self.steps = 0  # steps taken through this clock
 
     def advance(self, k):
         done = 0
@@ -156,6 +157,7 @@ class RunClock:
             done += n
             if hit and t_next == self.next_out:
                 self.next_out += self.dt_out
+        self.steps += done
         return done
 
 
@@ -163,7 +165,7 @@ def time_stages(sim, n=20):
     """Per-stage kernel time in the production context: n steps of the device loop replayed
     from a one-step CUDA graph with events recorded on the launching stream right around
     the predictor and corrector kernels (tp_steps_timed).  Returns mean ms per launch and
-    the tiles the last step processed."""
+    the mean tiles per launch the two stages processed over those steps."""
     import ctypes as C
     t = C.c_double(sim._bench_t)
     steps, hit = C.c_long(), C.c_int()
@@ -173,8 +175,10 @@ def time_stages(sim, n=20):
                                     C.byref(hit), C.byref(pm), C.byref(cm)))
     sim._bench_t = t.value
     k = max(steps.value, 1)
-    p_, c_, _ = sim.active_tiles()
-    return pm.value / k, cm.value / k, p_, c_
+    tp_, tc_ = C.c_longlong(), C.c_longlong()
+    sim._check(sim.L.tp_timed_tiles(sim.h, C.byref(tp_), C.byref(tc_)))
+    sim._bench_steps = steps.value
+    return pm.value / k, cm.value / k, tp_.value / k, tc_.value / k
 
 
 def ncu_traffic():
@@ -187,9 +191,75 @@ def ncu_traffic():
     return d
 
 
-def run_b200(args):
+def workload_config(sc) -> dict:
+    """The `config` keys both arms print for a scenario (identical strings, so the driver
+    can match the reference arm's line to ours)."""
+    return {"workload": f"{sc.name} {'Mode-II inflow' if sc.config.inflow else 'Mode-I release'}, "
+                        f"{sc.ncols}x{sc.nrows} interior cells, cellsize {sc.cellsize:g} m, Table-1 "
+                        f"parameters, CFL {sc.config.cfl:g}, output every {sc.config.dt_out:g} s",
+            "grid": [sc.ncols, sc.nrows]}
+
+
+def wet_fraction(sim) -> float:
+    """Fraction of interior cells with a nonzero thickness (state downloaded once)."""
+    s = sim.state()
+    h = s[0, 3:-3, 3:-3] + s[1, 3:-3, 3:-3]
+    return float((h != 0.0).mean())
+
+
+def timed_steps(sim, clock, stream, steps):
+    """CUDA-event time (ms) of `steps` device-loop steps along the run schedule."""
+    import torch
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    n = clock.advance(steps)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    assert n == steps, (n, steps)
+    return e0.elapsed_time(e1)
+
+
+def stage_roofline(sim, clock, cells, reps, peak):
+    """Roofline of the dominant kernel (the two stage kernels of a step), timed in the
+    production context (tp_steps_timed: CUDA events on the launching stream around each
+    stage kernel of a one-step graph, `reps` steps).  `achieved` counts the algorithmic
+    bytes (208 B predictor + 256 B corrector per cell-update) of the tiles
+    the kernels processed (dry tiles whose stage is a bitwise no-op are not read, DESIGN.md
+    §3); `effective_*` counts every interior cell as updated."""
+    sim._bench_t = clock.t
+    sim._bench_t_next = min(clock.next_out, clock.t_end)
+    t_pred, t_corr, tp_p, tp_c = time_stages(sim, n=reps)
+    clock.t = sim._bench_t
+    clock.steps += sim._bench_steps
+    while clock.next_out <= clock.t:  # an output hit inside this leg
+        clock.next_out += clock.dt_out
+    _, _, ntiles = sim.active_tiles()
+    frac_p, frac_c = tp_p / ntiles, tp_c / ntiles
+    kms = t_pred + t_corr
+    alg_proc = ALG_BYTES_PRED * cells * frac_p + ALG_BYTES_CORR * cells * frac_c
+    achieved = alg_proc / (kms / 1e3) / 1e9
+    eff = ALG_BYTES_PER_CELL_UPDATE * cells / (kms / 1e3) / 1e9
+    return {"achieved": round(achieved, 1), "frac": round(achieved / peak, 4),
+            "alg_bytes_per_step": int(alg_proc), "kernel_ms_per_step": round(kms, 4),
+            "pred_ms": round(t_pred, 4), "corr_ms": round(t_corr, 4),
+            "processed_tile_frac": [round(frac_p, 4), round(frac_c, 4)],
+            "effective_achieved": round(eff, 1), "effective_frac": round(eff / peak, 4)}
+
+
+def make_sim(sc, graph_steps):
     import torch
     from paper_2104_06784_b200.simulator import Simulator
+    t0 = time.perf_counter()
+    sim = Simulator.from_scenario(sc, device=0)
+    sim.set_option("graph_steps", graph_steps)
+    stream = torch.cuda.Stream()
+    sim.set_stream(stream.cuda_stream)
+    return sim, stream, time.perf_counter() - t0
+
+
+def run_b200(args):
+    import torch
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if world > 1 or args.gpus > 1:
@@ -197,43 +267,23 @@ def run_b200(args):
         return distributed.bench_main(args, METRIC, clock_sampler=ClockSampler)
 
     torch.cuda.set_device(0)
+    peak, peak_src = load_peaks()
     sc = scenario_for(args.config, args.ncols, args.nrows)
     cells = sc.ncols * sc.nrows
-    t_setup = time.perf_counter()
-    sim = Simulator.from_scenario(sc, device=0)
-    sim.set_option("graph_steps", args.graph_steps)
-    stream = torch.cuda.Stream()
-    sim.set_stream(stream.cuda_stream)
-    setup_s = time.perf_counter() - t_setup
+    sim, stream, setup_s = make_sim(sc, args.graph_steps)
 
     clock = RunClock(sim)
     clock.advance(args.warmup)
     torch.cuda.synchronize()
     clocks = ClockSampler(0)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with clocks:
-        torch.cuda.synchronize()
-        e0.record(stream)
-        n = clock.advance(args.steps)
-        e1.record(stream)
-        torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1)
+        ms = timed_steps(sim, clock, stream, args.steps)
     launches = sim.kernel_launches()
     act_p, act_c, ntiles = sim.active_tiles()
-    assert n == args.steps, (n, args.steps)
     value = cells * args.steps / (ms / 1e3) / 1e9
 
     # roofline leg: the two stage kernels (the dominant kernel of the step)
-    sim._bench_t = clock.t
-    sim._bench_t_next = min(clock.next_out, clock.t_end)
-    t_pred, t_corr, tp_p, tp_c = time_stages(sim, n=args.roofline_reps)
-    peak, peak_src = load_peaks()
-    achieved = ALG_BYTES_PER_CELL_UPDATE * cells / ((t_pred + t_corr) / 1e3) / 1e9
-    # the same bytes restricted to the tiles the kernels actually processed (dry tiles whose
-    # stage is a bitwise no-op are skipped): the kernel's own bandwidth
-    frac_p, frac_c = tp_p / ntiles, tp_c / ntiles
-    achieved_proc = (ALG_BYTES_PRED * cells * frac_p + ALG_BYTES_CORR * cells * frac_c) / \
-        ((t_pred + t_corr) / 1e3) / 1e9
+    rl = stage_roofline(sim, clock, cells, args.roofline_reps, peak)
     traffic = None
     nt = ncu_traffic()
     prof = None
@@ -242,16 +292,13 @@ def run_b200(args):
             prof = cand
     if prof:
         traffic = prof["dram_bytes_per_step"]
-    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(achieved / peak, 4), "traffic": traffic,
-                "kernel": "stage_kernel<pred>+stage_kernel<corr> per step",
-                "alg_bytes_per_launch": ALG_BYTES_PER_CELL_UPDATE * cells,
-                "kernel_ms_per_step": round(t_pred + t_corr, 4), "pred_ms": round(t_pred, 4),
-                "corr_ms": round(t_corr, 4), "peak_source": peak_src,
-                "processed_tile_frac": [round(frac_p, 4), round(frac_c, 4)],
-                "achieved_processed_tiles": round(achieved_proc, 1),
-                "frac_processed_tiles": round(achieved_proc / peak, 4),
-                "step_frac": round(achieved * (t_pred + t_corr) / (ms / args.steps) / peak, 4)}
+    roofline = {"bound": "hbm", "achieved": rl["achieved"], "peak": peak, "unit": "GB/s",
+                "frac": rl["frac"], "traffic": traffic,
+                "kernel": "stage_kernel<pred>+stage_kernel<corr> per step (achieved: algorithmic "
+                          "bytes of the processed tiles / their CUDA-event time)",
+                "peak_source": peak_src}
+    roofline.update({k: v for k, v in rl.items() if k not in ("achieved", "frac")})
+    roofline["step_frac"] = round(rl["frac"] * rl["kernel_ms_per_step"] / (ms / args.steps), 4)
     if prof and prof.get("fp64_pipe_active_pct"):
         # the processed tiles are FP64-issue bound: the co-bound from the same capture
         roofline["co_bound"] = {"pipe": "fp64", "fp64_pipe_active_pct": prof["fp64_pipe_active_pct"],
@@ -272,15 +319,23 @@ def run_b200(args):
     torch.cuda.synchronize()
     w0 = time.perf_counter()
     sim._check(sim.L.tp_set_state(sim.h, C.cast(h_in.data_ptr(), C.POINTER(C.c_double))))
-    clock.t = sim._bench_t
-    while clock.next_out <= clock.t:  # an output hit inside the roofline leg
-        clock.next_out += clock.dt_out
     ne = clock.advance(args.steps)
     sim._check(sim.L.tp_get_state(sim.h, C.cast(h_out.data_ptr(), C.POINTER(C.c_double))))
     w1 = time.perf_counter()
     e2e = {"value": round(cells * ne / (w1 - w0) / 1e9, 4), "unit": "GCUPS",
            "h2d_bytes_per_step": nbytes // max(ne, 1), "d2h_bytes_per_step": nbytes // max(ne, 1),
            "mode": f"tp_set_state(pinned host) + tp_steps({ne}) + tp_get_state(pinned host), wall clock"}
+    del h_in, h_out
+
+    extra = {}
+    if not args.no_extra:
+        # a representative window of a whole run: after the release has spread
+        extra["long_run"] = long_run_leg(sim, clock, stream, cells, peak, args)
+        sim.close()
+        del sim
+        torch.cuda.empty_cache()
+        # the north-star grid (BASELINE.json configs[4]): C5 8192^2, N=1
+        extra["c5_8192"] = c5_leg(args, peak)
 
     cpu = None
     if not args.no_cpu:
@@ -295,51 +350,101 @@ def run_b200(args):
         if "note" in c:
             cpu["note"] = c["note"]
 
+    cfg = workload_config(sc)
+    cfg.update({"wet_fraction_t0": round(float((sc.h0 > 0).mean()), 4) if sc.h0 is not None else None,
+                "l2": "inputs larger than L2 (state 2x%.0f MB + geometry %.0f MB > 126 MB)"
+                      % (nbytes / 1e6, 18 * (nbytes // 48) * 8 / 1e6),
+                "parallelism": "single device", "graph_steps": args.graph_steps,
+                "window": f"steps {args.warmup + 1}..{args.warmup + args.steps} from t=0",
+                "active_tiles_last_step": [act_p, act_c, ntiles],
+                "hbm_roofline_gcups": round(peak / ALG_BYTES_PER_CELL_UPDATE, 3),
+                "setup_seconds": round(setup_s, 2)})
     out = {
         "metric": METRIC, "value": round(value, 4), "unit": "GCUPS", "n_gpus": 1,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 5),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": f"synthetic (deterministic {sc.name} generator in scenarios.py: DEM + "
                 f"{'inflow hydrograph' if sc.config.inflow else 'compact release'}; no network data)",
-        "config": {"workload": f"{sc.name} {'Mode-II inflow' if sc.config.inflow else 'Mode-I release'}, "
-                               f"{sc.ncols}x{sc.nrows} interior cells, cellsize {sc.cellsize:g} m, Table-1 "
-                               f"parameters, CFL {sc.config.cfl:g}, output every {sc.config.dt_out:g} s",
-                   "grid": [sc.ncols, sc.nrows], "wet_fraction_t0": round(float((sc.h0 > 0).mean()), 4)
-                   if sc.h0 is not None else None,
-                   "l2": "inputs larger than L2 (state 2x%.0f MB + geometry %.0f MB > 126 MB)"
-                         % (nbytes / 1e6, 18 * sim.ny * sim.nx * 8 / 1e6),
-                   "parallelism": "single device", "graph_steps": args.graph_steps,
-                   "active_tiles_last_step": [act_p, act_c, ntiles],
-                   "hbm_roofline_gcups": round(peak / ALG_BYTES_PER_CELL_UPDATE, 3),
-                   "hbm_frac_of_step": round(value / (peak / ALG_BYTES_PER_CELL_UPDATE), 4),
-                   "setup_seconds": round(setup_s, 2)},
-        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+        "config": cfg, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
         "clocks": clocks.summary(), "gpu_launches": launches,
     }
+    out.update(extra)
     print(json.dumps(out))
+
+
+def long_run_leg(sim, clock, stream, cells, peak, args):
+    """GCUPS and the stage kernels' roofline on a window after the release has spread:
+    the run continues to step `--long-start`, then `--long-steps` steps are timed; the wet
+    fraction (cells with a nonzero thickness) is reported at the window's start and end."""
+    while clock.steps < args.long_start:
+        if clock.advance(min(args.long_start - clock.steps, 500)) == 0:
+            break  # t_end reached
+    first = clock.steps + 1
+    w0 = wet_fraction(sim)
+    ms = timed_steps(sim, clock, stream, args.long_steps)
+    w1 = wet_fraction(sim)
+    rl = stage_roofline(sim, clock, cells, args.roofline_reps, peak)
+    return {"value": round(cells * args.long_steps / (ms / 1e3) / 1e9, 4), "unit": "GCUPS",
+            "steps": args.long_steps, "ms_per_step": round(ms / args.long_steps, 5),
+            "window": f"steps {first}..{first + args.long_steps - 1} of the same run from t=0 "
+                      f"(t = {clock.t * sim.cfg.scaling.t_unit():.2f} s at the end)",
+            "wet_fraction": [round(w0, 4), round(w1, 4)],
+            "roofline": {"frac": rl["frac"], "achieved": rl["achieved"],
+                         "processed_tile_frac": rl["processed_tile_frac"],
+                         "effective_frac": rl["effective_frac"]}}
+
+
+def c5_leg(args, peak):
+    """BASELINE.json configs[4] at its smallest point, the north-star grid: the C2 valley
+    generator at 8192 x 8192 on one GPU (weak-scaling base case of bench.py --gpus N)."""
+    import torch
+    sc = scenario_for("c2", args.c5_size, args.c5_size)
+    cells = sc.ncols * sc.nrows
+    sim, stream, setup_s = make_sim(sc, args.graph_steps)
+    clock = RunClock(sim)
+    clock.advance(args.warmup)
+    torch.cuda.synchronize()
+    clocks = ClockSampler(0)
+    with clocks:
+        ms = timed_steps(sim, clock, stream, args.c5_steps)
+    rl = stage_roofline(sim, clock, cells, max(4, args.roofline_reps // 2), peak)
+    out = {"value": round(cells * args.c5_steps / (ms / 1e3) / 1e9, 4), "unit": "GCUPS",
+           "steps": args.c5_steps, "warmup": args.warmup, "ms_per_step": round(ms / args.c5_steps, 5),
+           "config": workload_config(sc), "setup_seconds": round(setup_s, 2),
+           "roofline": {"bound": "hbm", "achieved": rl["achieved"], "peak": peak, "unit": "GB/s",
+                        "frac": rl["frac"], "traffic": None, **{k: v for k, v in rl.items()
+                                                               if k not in ("achieved", "frac")}},
+           "clocks": clocks.summary()}
+    nt = ncu_traffic()
+    c5p = (nt or {}).get("c5")
+    if c5p and c5p.get("grid") == [sc.ncols, sc.nrows]:
+        out["roofline"]["traffic"] = c5p["dram_bytes_per_step"]
+        out["roofline"]["traffic_source"] = nt.get("source")
+    sim.close()
+    del sim
+    torch.cuda.empty_cache()
+    return out
 
 
 def run_reference(args):
     """--impl reference: the reference's own CPU implementation on this host's cores, on the
-    grid our arm runs at this N (N=1: the config's grid; N>1: the weak-scaling grid of N
-    row-stacked copies, distributed.bench_main).  Under torchrun only rank 0 runs."""
+    grid our arm runs at this N (N=1: the config's grid; N>1: the grid of distributed.bench_main,
+    weak: N row-stacked copies, strong: the one grid).  Under torchrun only rank 0 runs."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     world = max(args.gpus, int(os.environ.get("WORLD_SIZE", "1")))
-    sc = scenario_for(args.config, args.ncols, args.nrows)
-    if world > 1:
-        from paper_2104_06784_b200 import scenarios
-        sc = (scenarios.SCENARIOS["c3"](args.ncols, args.nrows * world) if args.config == "c3"
-              else scenarios.stacked(sc, world))
+    from paper_2104_06784_b200 import distributed
+    sc, stack = distributed.bench_scenario(args, world) if world > 1 else \
+        (scenario_for(args.config, args.ncols, args.nrows), 1)
     lanes = os.cpu_count() or 1
     # bounded sample: at most ~2 minutes of CPU work
     steps = args.steps
-    probe = cpu_reference(args.config, args.ncols, args.nrows, 1, lanes, stack=world)
+    probe = cpu_reference(args.config, args.ncols, args.nrows, 1, lanes, stack=stack)
     per_step = probe["seconds"] / max(probe["steps"], 1)
     if per_step * steps > 120:
         steps = max(1, int(120 / per_step))
-    c = cpu_reference(args.config, args.ncols, args.nrows, steps, lanes, stack=world)
+    c = cpu_reference(args.config, args.ncols, args.nrows, steps, lanes, stack=stack)
     assert c["grid"] == [sc.ncols, sc.nrows], (c["grid"], sc.ncols, sc.nrows)
     v = round(c["value"] / 1e9, 6)
     cpu = {"value": v, "unit": "GCUPS", "cores": c["lanes"],
@@ -347,14 +452,25 @@ def run_reference(args):
            "sample": f"{c['steps']} steps of {sc.ncols}x{sc.nrows} {args.config} (of {args.steps} requested)"}
     if "note" in c:
         cpu["note"] = c["note"]
+    cfg = workload_config(sc)
+    cfg["parallelism"] = f"host CPU, {c['lanes']} threads"
     out = {"metric": METRIC, "value": v, "unit": "GCUPS", "n_gpus": args.gpus, "steps": c["steps"],
            "warmup": args.warmup, "ms_per_step": round(1e3 * c["seconds"] / c["steps"], 3),
-           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-           "data": "synthetic (scenarios.py)", "impl": "reference",
-           "config": {"workload": f"{sc.name} {sc.ncols}x{sc.nrows}", "grid": [sc.ncols, sc.nrows],
-                      "parallelism": f"host CPU, {c['lanes']} threads"},
+           "higher_is_better": True, "scaling": "strong" if getattr(args, "scaling", "weak") == "strong" else "weak",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic (scenarios.py)", "impl": "reference",
+           "config": cfg,
            "cpu_baseline": cpu, "e2e": {"value": v, "unit": "GCUPS", "h2d_bytes_per_step": 0,
                                         "d2h_bytes_per_step": 0}}
+    if world == 1 and not args.no_extra:
+        # the north-star grid beside it (our arm's c5_8192 object): a 2-step sample
+        try:
+            c5 = cpu_reference("c2", args.c5_size, args.c5_size, args.c5_ref_steps, lanes, timeout=900)
+            out["c5_8192"] = {"value": round(c5["value"] / 1e9, 6), "unit": "GCUPS",
+                              "steps": c5["steps"], "ms_per_step": round(1e3 * c5["seconds"] / c5["steps"], 3),
+                              "config": workload_config(scenario_for("c2", args.c5_size, args.c5_size)),
+                              "cores": c5["lanes"], "setup_seconds": round(c5.get("setup_seconds", 0.0), 1)}
+        except Exception as e:  # noqa: BLE001 - a reported gap, not a failed arm
+            out["c5_8192"] = {"unavailable": str(e)[:200]}
     print(json.dumps(out))
 
 
@@ -371,6 +487,14 @@ def main():
     ap.add_argument("--roofline-reps", type=int, default=20)
     ap.add_argument("--cpu-steps", type=int, default=60)  # ~10 s of the reference on 16 cores at C2
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the long-run window and the C5 8192^2 leg")
+    ap.add_argument("--long-start", type=int, default=1000)
+    ap.add_argument("--long-steps", type=int, default=200)
+    ap.add_argument("--c5-size", type=int, default=8192)
+    ap.add_argument("--c5-steps", type=int, default=20)
+    ap.add_argument("--c5-ref-steps", type=int, default=2)
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="N>1: weak = one copy of the N=1 workload per GPU; strong = one grid split N ways")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

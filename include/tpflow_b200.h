@@ -101,6 +101,9 @@ int tp_steps(tp_ctx* c, double t_next, double t_end, long max_steps, double* t, 
  * the summed device time of those kernels over the steps taken (measurement hook) */
 int tp_steps_timed(tp_ctx* c, double t_next, double t_end, long max_steps, double* t, long* steps, int* hit,
                    float* pred_ms, float* corr_ms);
+/* tiles the predictor / corrector launches processed, summed over the steps of the last
+ * tp_steps_timed call (the roofline's processed bytes, bench.py) */
+int tp_timed_tiles(tp_ctx* c, long long* pred_tiles, long long* corr_tiles);
 
 /* audit[0..4] = solid {initial, final, injected, outflow, clipped}, [5..9] fluid
  * (MassAudit, config.hpp:60-75); initial/final are host-owned (see tp_set_audit). */

@@ -63,6 +63,7 @@ def main() -> None:
     out = {"kind": kind, "lanes": lanes, "steps": n, "seconds": dt_wall, "setup_seconds": setup,
            "cells": sc.ncols * sc.nrows, "value": sc.ncols * sc.nrows * n / dt_wall,
            "unit": "cell-updates/s", "config": a.config, "grid": [sc.ncols, sc.nrows]}
+    del sim  # (8192^2: ~30 GB of host memory per instance)
     if lanes > 1 and a.check_serial > 0:
         # App. B1: multi-lane timings only count when they match the serial backend bitwise
         par = orc.OracleSim(sc, kind, lanes=lanes)

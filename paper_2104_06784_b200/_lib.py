@@ -77,6 +77,7 @@ SIGNATURES = {
     "tp_selftest_division": (C.c_int, [C.c_int, C.c_long, C.c_ulonglong, C.POINTER(C.c_ulonglong)]),
     "tp_selftest_minmod": (C.c_int, [C.c_int, C.c_long, _dp, _dp, _dp]),
     "tp_active_tiles": (C.c_int, [_vp, _ip, _ip, _ip]),
+    "tp_timed_tiles": (C.c_int, [_vp, C.POINTER(C.c_longlong), C.POINTER(C.c_longlong)]),
     "tp_peer_export": (C.c_int, [_vp, _vp]),
     "tp_peer_connect": (C.c_int, [_vp, C.c_int, C.c_int, _vp]),
     "tp_peer_connect_local": (C.c_int, [_vp, C.c_int, C.c_int, C.POINTER(_vp)]),

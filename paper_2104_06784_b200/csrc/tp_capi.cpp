@@ -132,6 +132,8 @@ struct tp_ctx {
     double* dB = nullptr;
     double* dGeo = nullptr;
     DevScalars* dSc = nullptr;
+    tpb::ClipList* dClip = nullptr;  // regularize's clipped-mass events (tp_types.h)
+    long long timed_tiles[2] = {0, 0};  // tiles processed per stage over the last tp_steps_timed
     double* dTallyP = nullptr;
     double* dTallyC = nullptr;
     signed char* dSide = nullptr;
@@ -383,6 +385,7 @@ void launch_post(tp_ctx* c, int loop) {
     a.ntx = c->ntx;
     a.nty = c->nty;
     a.loop = loop;
+    a.peered = c->peered ? 1 : 0;
     ck(tpb::launch_post(a, c->stream), "post_kernel");
 }
 
@@ -689,11 +692,13 @@ void create_impl(tp_ctx* c, const tp_params* p, const tp_dem* dem, int row0, int
     c->dB = c->rawB + 1;
     c->dGeo = c->rawGeo + 1;
     ck(cudaMalloc(&c->dSc, sizeof(DevScalars)), "cudaMalloc scalars");
+    ck(cudaMalloc(&c->dClip, sizeof(tpb::ClipList)), "cudaMalloc clip list");
     const size_t tb = sizeof(double) * 4ull * c->ntx * c->nty;
     ck(cudaMalloc(&c->dTallyP, tb), "cudaMalloc tally");
     ck(cudaMalloc(&c->dTallyC, tb), "cudaMalloc tally");
     ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
     c->own_stream = true;
+    ck(cudaMemsetAsync(c->dClip, 0, sizeof(tpb::ClipList), c->stream), "memset");
     ck(cudaMemsetAsync(c->rawA, 0, sbytes, c->stream), "memset");
     ck(cudaMemsetAsync(c->rawB, 0, sbytes, c->stream), "memset");
     ck(cudaMemsetAsync(c->dTallyP, 0, tb, c->stream), "memset");
@@ -784,6 +789,7 @@ void create_impl(tp_ctx* c, const tp_params* p, const tp_dem* dem, int row0, int
     h.lam_cur = 0;
     h.err_key = tpb::kNoError;
     h.max_steps = LLONG_MAX;
+    h.clip = c->dClip;
     ck(cudaMemcpyAsync(c->dSc, &h, sizeof(h), cudaMemcpyHostToDevice, c->stream), "scalars H2D");
     ck(cudaStreamSynchronize(c->stream), "sync");
 }
@@ -824,6 +830,7 @@ void tp_destroy(tp_ctx* c) {
     cudaFree(c->rawB);
     cudaFree(c->rawGeo);
     cudaFree(c->dSc);
+    cudaFree(c->dClip);
     cudaFree(c->dTallyP);
     cudaFree(c->dTallyC);
     cudaFree(c->dInflowTiles);
@@ -1165,9 +1172,25 @@ void steps_poll(tp_ctx* c, StepsRun& r) {
     r.finished = r.h.done != 0;
 }
 
+// A device error key with the slab's local row replaced by the global row, so keys of
+// different slabs order like the serial reference's loops (error keys: tp_kernels.cu).
+unsigned long long global_error_key(const tp_ctx* c, unsigned long long key) {
+    if (key == tpb::kNoError) return key;
+    const unsigned long long cls = key >> 62;
+    if (cls <= 1) {  // (cls << 62) | (j << 32) | (i << 1) | phase
+        const unsigned long long j = ((key >> 32) & 0x3fffffffull) + static_cast<unsigned long long>(c->row0);
+        return (cls << 62) | (j << 32) | (key & 0xffffffffull);
+    }
+    if (cls == 2) {  // (2 << 62) | (field << 56) | (j << 28) | i
+        const unsigned long long j = ((key >> 28) & 0xfffffffull) + static_cast<unsigned long long>(c->row0);
+        return (key & ~(0xfffffffull << 28)) | (j << 28);
+    }
+    return key;
+}
+
 void steps_end(tp_ctx* c, StepsRun& r, double* t, long* steps, int* hit) {
     const DevScalars& h = r.h;
-    if (c->peered) c->peer_base += 4ull * static_cast<unsigned long long>(r.launched + 1);
+    if (c->peered) c->peer_base += 4ull * static_cast<unsigned long long>(r.launched);
     *steps = static_cast<long>(h.steps);
     *t = h.t;
     *hit = h.steps > 0 ? h.hit : 0;
@@ -1235,13 +1258,23 @@ int tp_steps_group(tp_ctx* const* cs, int n, double t_next, double t_end, long m
         double tk = 0.0;
         long sk = 0;
         int hk = 0;
+        // the error the serial reference throws first: smallest key in global row order
+        int first = -1;
+        unsigned long long best = tpb::kNoError;
+        for (int k = 0; k < n; ++k) {
+            const unsigned long long gk = global_error_key(cs[k], runs[k].h.err_key);
+            if (gk < best) {
+                best = gk;
+                first = k;
+            }
+        }
         std::string err;
         for (int k = 0; k < n; ++k) {  // finish every member, then report the first error
             cudaSetDevice(cs[k]->device);
             try {
                 steps_end(cs[k], runs[k], &tk, &sk, &hk);
             } catch (const NumErr& e) {
-                if (err.empty()) err = e.msg;
+                if (k == first) err = e.msg;
             }
             if (k == 0) {
                 *t = tk;
@@ -1343,19 +1376,22 @@ int tp_peer_connect_local(tp_ctx* c, int rank, int nranks, tp_ctx* const* all) {
     TP_GUARD(c, {
         peer_check_layout(c, rank, nranks);
         tpb::PeerLink L{};
-        for (int r = 0; r < nranks; ++r) L.box[r] = all[r]->dBox;
+        // peer_lambda_kernel stores into every rank's mailbox, peer_halo_push_kernel into the
+        // neighbours' state: peer access to every other device of the group
+        for (int r = 0; r < nranks; ++r) {
+            L.box[r] = all[r]->dBox;
+            if (all[r]->device != c->device) {
+                const cudaError_t e = cudaDeviceEnablePeerAccess(all[r]->device, 0);
+                if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) ck(e, "peer access");
+                cudaGetLastError();
+            }
+        }
         for (int side = 0; side < 2; ++side) {
             const int nb = side == 0 ? rank - 1 : rank + 1;
             if (nb < 0 || nb >= nranks) continue;
             const tp_ctx* o = all[nb];
             if (o->nx != c->nx || (side == 0 ? o->row1 != c->row0 : o->row0 != c->row1))
                 throw ConfigErr{"peer: context " + std::to_string(nb) + " is not the adjacent slab"};
-            if (o->device != c->device) {
-                const cudaError_t e = cudaDeviceEnablePeerAccess(o->device, 0);
-                if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
-                    ck(e, "peer access");
-                cudaGetLastError();
-            }
             L.nbr_state[0][side] = o->dA;
             L.nbr_state[1][side] = o->dB;
             L.nbr_fs[side] = o->fs;
@@ -1390,6 +1426,7 @@ int tp_steps_timed(tp_ctx* c, double t_next, double t_end, long max_steps, doubl
         }
         c->last_tiles_stage = 1;
         DevScalars h{};
+        c->timed_tiles[0] = c->timed_tiles[1] = 0;
         for (;;) {
             ck(cudaGraphLaunch(c->graphT, c->stream), "graph launch");
             c->launches += 5;
@@ -1401,6 +1438,10 @@ int tp_steps_timed(tp_ctx* c, double t_next, double t_end, long max_steps, doubl
                 *pred_ms += a;
                 *corr_ms += b;
                 *steps = static_cast<long>(h.steps);
+                int n[2] = {0, 0};  // tiles the two stage launches of this step processed
+                ck(cudaMemcpy(n, c->dNact + 2, sizeof(n), cudaMemcpyDeviceToHost), "tiles D2H");
+                c->timed_tiles[0] += n[0];
+                c->timed_tiles[1] += n[1];
             }
             if (h.done) break;
         }
@@ -1647,6 +1688,13 @@ int tp_safe_tiles(tp_ctx* c, int* corr) {
 
 int tp_cond_skipped_tiles(tp_ctx* c, unsigned long long* n) {
     TP_GUARD(c, { *n = read_scalars(c).cond_skips; })
+}
+
+int tp_timed_tiles(tp_ctx* c, long long* pred, long long* corr) {
+    TP_GUARD(c, {
+        *pred = c->timed_tiles[0];
+        *corr = c->timed_tiles[1];
+    })
 }
 
 int tp_active_tiles(tp_ctx* c, int* pred, int* corr, int* total) {

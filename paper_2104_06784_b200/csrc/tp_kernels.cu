@@ -130,7 +130,11 @@ __device__ __forceinline__ unsigned long long cell_epilogue(double (&un)[6], con
                     atomicMin(&sc->err_key, key);
                     break;  // the reference throws here; leave the cell as computed
                 }
-                atomicAdd(&sc->audit[5 * p + 4], -w * P.cell_area);
+                clip_record(sc,
+                            (static_cast<unsigned long long>(CORR ? 1 : 0) << 62) |
+                                (static_cast<unsigned long long>(Y) << 32) |
+                                (static_cast<unsigned long long>(X) << 1) | static_cast<unsigned long long>(p),
+                            -w * P.cell_area, p);
                 un[p] = 0.0;
                 hp = 0.0;
             }
@@ -1021,6 +1025,7 @@ __device__ __forceinline__ int ring_tile(int ntx, int nty, int r) {
 __global__ void __launch_bounds__(NT) post_kernel(PostArgs a) {
     DevScalars* sc = a.sc;
     if (a.loop && sc->done) return;
+    clip_fold_block<NT>(sc);  // regularize's clipped mass of both stages, reference order
     // both stages' 4 tallies per ring tile: per-thread sums, warp shuffles, then the 8 warp
     // partials in warp order (deterministic)
     __shared__ double red[NT / 32][8];
@@ -1062,10 +1067,16 @@ __global__ void __launch_bounds__(NT) post_kernel(PostArgs a) {
             sc->steps += 1;
             sc->t = sc->hit ? sc->t_next : sc->t + dt;
             sc->lam_cur = sc->lam_bits;
-            if (sc->err_key != kNoError || sc->hit || sc->steps >= sc->max_steps) sc->done = 1;
+            // peer-joined slabs: a local error is published by the next step's stop-flag
+            // exchange, which stops every rank at the same step (a local stop here would leave
+            // the other ranks waiting for this one)
+            if ((!a.peered && sc->err_key != kNoError) || sc->hit || sc->steps >= sc->max_steps) sc->done = 1;
         }
     }
 }
+
+// Fold of the standalone regularize's clip events (one block).
+__global__ void __launch_bounds__(NT) clip_fold_kernel(DevScalars* sc) { clip_fold_block<NT>(sc); }
 
 // Standalone Simulator::regularize (solver.cpp:139-166) on the interior.
 template <bool FD>
@@ -1088,7 +1099,10 @@ __global__ void __launch_bounds__(NT) regularize_kernel(GridDesc g, Phys P, doub
                 atomicMin(&sc->err_key, key);
                 return;
             }
-            atomicAdd(&sc->audit[5 * p + 4], -w * P.cell_area);
+            clip_record(sc,
+                        (static_cast<unsigned long long>(Y) << 32) | (static_cast<unsigned long long>(X) << 1) |
+                            static_cast<unsigned long long>(p),
+                        -w * P.cell_area, p);
             s[p * g.fs + o] = 0.0;
             hp = 0.0;
         }
@@ -1169,6 +1183,9 @@ cudaError_t launch_regularize(const GridDesc& g, const Phys& P, double* s, const
     dim3 grid((g.nx - 6 + 31) / 32, (g.ny - 6 + NT / 32 - 1) / (NT / 32));
     if (fastdiv) regularize_kernel<true><<<grid, NT, 0, st>>>(g, P, s, geo, sc);
     else regularize_kernel<false><<<grid, NT, 0, st>>>(g, P, s, geo, sc);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    clip_fold_kernel<<<1, NT, 0, st>>>(sc);
     return cudaGetLastError();
 }
 
@@ -1313,7 +1330,8 @@ cudaError_t init_kernels() {
         reinterpret_cast<const void*>(&regularize_kernel<true>),
         reinterpret_cast<const void*>(&regularize_kernel<false>),
         reinterpret_cast<const void*>(&pack_state_kernel), reinterpret_cast<const void*>(&unpack_state_kernel),
-        reinterpret_cast<const void*>(&snapshot_kernel), reinterpret_cast<const void*>(&mass_kernel)};
+        reinterpret_cast<const void*>(&snapshot_kernel), reinterpret_cast<const void*>(&mass_kernel),
+        reinterpret_cast<const void*>(&clip_fold_kernel)};
     for (const void* f : fns)
         if ((e = cudaFuncGetAttributes(&fa, f)) != cudaSuccess) return e;
     return cudaSuccess;

@@ -54,8 +54,9 @@ __device__ __forceinline__ bool wait_seq(const unsigned long long* p, unsigned l
 }
 
 // Sequence numbers of one step (steps = DevScalars::steps before the step's post).
-// peer_base is advanced by the host after every tp_steps call by 4 * (graph steps + 1),
-// identically on every rank, so sequence numbers only grow.
+// peer_base is advanced by the host after every tp_steps call by 4 * (graph steps launched),
+// identically on every rank, so sequence numbers only grow (a step's numbers are at most
+// base + 4 * (launched - 1) + 3 < the next call's first, base + 4 * launched + 1).
 __device__ __forceinline__ unsigned long long seq_of(const DevScalars* sc, int phase) {
     return sc->peer_base + 4ull * static_cast<unsigned long long>(sc->steps) +
            static_cast<unsigned long long>(phase) + 1ull;
@@ -68,21 +69,24 @@ __global__ void peer_lambda_kernel(PeerLink L, DevScalars* sc) {
     __shared__ int timed_out;
     const int k = threadIdx.x;
     const unsigned long long seq = seq_of(sc, 0);
+    // exchange parity (PeerBox): peer_base / 4 + steps numbers the exchanges consecutively
+    // across tp_steps calls (the host advances peer_base by 4 per graph step launched)
+    const int slot = static_cast<int>(((sc->peer_base >> 2) + static_cast<unsigned long long>(sc->steps)) & 1ull);
     if (k == 0) timed_out = 0;
     __syncthreads();
     if (k < L.nranks) {
         PeerBox* b = L.box[k];
-        b->lam_val[L.rank] = sc->lam_cur;
-        b->stop_val[L.rank] = (sc->err_key != kNoError) ? 1ull : 0ull;
+        b->lam_val[slot][L.rank] = sc->lam_cur;
+        b->stop_val[slot][L.rank] = (sc->err_key != kNoError) ? 1ull : 0ull;
         __threadfence_system();
-        st_release_sys(&b->lam_seq[L.rank], seq);
+        st_release_sys(&b->lam_seq[slot][L.rank], seq);
     }
     __syncthreads();
     unsigned long long lam = 0ull, stop = 0ull;
     if (k < L.nranks) {
-        if (wait_seq(&L.my_box->lam_seq[k], seq, L.timeout_ns)) {
-            lam = *(volatile unsigned long long*)&L.my_box->lam_val[k];
-            stop = *(volatile unsigned long long*)&L.my_box->stop_val[k];
+        if (wait_seq(&L.my_box->lam_seq[slot][k], seq, L.timeout_ns)) {
+            lam = *(volatile unsigned long long*)&L.my_box->lam_val[slot][k];
+            stop = *(volatile unsigned long long*)&L.my_box->stop_val[slot][k];
         } else {
             atomicExch(&timed_out, 1);
         }

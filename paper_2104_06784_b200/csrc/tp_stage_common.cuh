@@ -50,6 +50,47 @@ __device__ __forceinline__ void lam_block_max(double lam, DevScalars* sc) {
     }
 }
 
+// One clipped-mass event of regularize (ClipList, tp_types.h); out of line (rare).
+static __device__ __noinline__ void clip_record(DevScalars* sc, unsigned long long key, double val, int p) {
+    ClipList* cl = sc->clip;
+    const int k = atomicAdd(&cl->n, 1);
+    if (k < kClipCap) {
+        cl->key[k] = key;
+        cl->val[k] = val;
+    } else {
+        atomicAdd(&sc->audit[5 * p + 4], val);
+        atomicAdd(&cl->overflow, 1);
+    }
+}
+
+// Fold the pending clip events into the audit in key order (= the reference's serial
+// (stage, j, i) order per phase), by one whole block; resets the list.
+template <int NTHREADS>
+__device__ __forceinline__ void clip_fold_block(DevScalars* sc) {
+    ClipList* cl = sc->clip;
+    const int n = min(*(volatile int*)&cl->n, kClipCap);
+    if (n == 0) return;  // uniform across the block
+    for (int i = threadIdx.x; i < n; i += NTHREADS) {
+        const unsigned long long ki = cl->key[i];
+        int r = 0;
+        for (int k = 0; k < n; ++k) {
+            const unsigned long long kk = cl->key[k];
+            r += (kk < ki || (kk == ki && k < i)) ? 1 : 0;
+        }
+        cl->order[r] = i;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int r = 0; r < n; ++r) {
+            const int i = cl->order[r];
+            const int p = static_cast<int>(cl->key[i] & 1ull);
+            sc->audit[5 * p + 4] += cl->val[i];
+        }
+        cl->n = 0;
+    }
+    __syncthreads();
+}
+
 // ---------------------------------------------------------------------------
 // TMA / mbarrier helpers (sm_90+ PTX, used here on sm_100a)
 // ---------------------------------------------------------------------------

@@ -54,6 +54,21 @@ enum StateField { S_WS = 0, S_WF, S_QSX, S_QSY, S_QFX, S_QFY, S_COUNT };
 
 constexpr unsigned long long kNoError = ~0ull;
 
+// Clipped-mass audit events of regularize (solver.cpp:139-166): the reference adds
+// -w * cell_area to audit.clipped cell by cell in (j, i) order, predictor then corrector.
+// The stage kernels append (key, value) events here; post_kernel (and the standalone
+// regularize's fold) sorts them by key and adds them in that order, so the audit is the
+// reference's sum bit for bit.  key = (stage << 62) | (j << 32) | (i << 1) | phase.
+// Past kClipCap events per fold the rest are added with atomics (order not reproduced).
+constexpr int kClipCap = 8192;
+struct ClipList {
+    int n;                               // events appended since the last fold
+    int overflow;                        // events added directly (cumulative, diagnostics)
+    unsigned long long key[kClipCap];
+    double val[kClipCap];
+    int order[kClipCap];                 // fold scratch: event index by rank
+};
+
 // Device-resident step scalars: the time loop of Simulator::run
 // (solver.cpp:637-649) lives here so the host never waits on dt.
 struct DevScalars {
@@ -72,6 +87,7 @@ struct DevScalars {
     double* dts;                  // optional per-step dt record (device)
     unsigned long long peer_base; // sequence base of the slab exchange (tp_peer.cu)
     unsigned long long cond_skips;  // conditional tiles left off the list by peer_wait_kernel (cumulative)
+    ClipList* clip;               // regularize's clipped-mass events (see ClipList)
 };
 
 struct GridDesc {
@@ -197,6 +213,8 @@ struct PostArgs {
     const double* tally_corr;
     int ntx, nty;
     int loop;
+    int peered;   // slabs joined by tp_peer_connect*: a local error stops the loop through the
+                  // next step's stop-flag exchange (peer_lambda_kernel), on every rank at once
 };
 
 // ---- device-resident row-slab exchange (tp_peer.cu) ----------------------------
@@ -205,9 +223,12 @@ constexpr int kMaxRanks = 16;
 // neighbours write halo-arrival sequence numbers, every rank writes its lambda slot.
 struct PeerBox {
     unsigned long long halo_seq[2][2];          // [buf A/B][side 0 = from south, 1 = from north]
-    unsigned long long lam_seq[kMaxRanks];      // [rank] sequence of lam_val/stop_val
-    unsigned long long lam_val[kMaxRanks];      // bits of the rank's local lambda (>= 0)
-    unsigned long long stop_val[kMaxRanks];     // 1 if the rank stopped (error)
+    // lambda / stop slots by step parity: a rank can run at most one step ahead of any
+    // reader (its step-n+1 exchange waits for every rank's step-n+1 write, which each rank
+    // makes only after reading its step-n slots), so two slots never collide
+    unsigned long long lam_seq[2][kMaxRanks];   // [step & 1][rank] sequence of lam_val/stop_val
+    unsigned long long lam_val[2][kMaxRanks];   // bits of the rank's local lambda (>= 0)
+    unsigned long long stop_val[2][kMaxRanks];  // 1 if the rank stopped (error)
     unsigned int push_done[2][2];               // local: CTAs finished pushing [buf][side]
     unsigned int pad[4];
     // [buf][side][tile column]: 1 if the 2 pushed rows hold a bit other than +0.0 within the

@@ -28,6 +28,57 @@ from typing import List, Optional, Sequence
 import numpy as np
 
 
+def row_work(sc, tx: int = 16, halo: int = 2) -> np.ndarray:
+    """Per-row work estimate of a Mode-I scenario for the stage kernels: the number of
+    16-column tiles in which the row's radius-2 neighbourhood holds wet cells (dry tiles are
+    bitwise no-ops and skipped).  Mode-II / no release: uniform."""
+    if sc.h0 is None or sc.hydrograph is not None:
+        return np.ones(sc.nrows)
+    wet = np.asarray(sc.h0) > 0.0
+    if sc.vx0 is not None:
+        wet |= (np.asarray(sc.vx0) != 0.0) | (np.asarray(sc.vy0) != 0.0)
+    nr, nc = wet.shape
+    ntx = (nc + tx - 1) // tx
+    pad = np.zeros((nr, ntx * tx), dtype=bool)
+    pad[:, :nc] = wet
+    # columns dilated by the radius-2 box (a tile's box reads 2 cells of each neighbour tile)
+    colw = pad.copy()
+    colw[:, 2:] |= pad[:, :-2]
+    colw[:, 1:] |= pad[:, :-1]
+    colw[:, :-1] |= pad[:, 1:]
+    colw[:, :-2] |= pad[:, 2:]
+    tiles = colw.reshape(nr, ntx, tx).any(axis=2)           # [rows, tile columns]
+    rows = tiles.copy()
+    for d in range(1, halo + 1):                            # rows dilated the same way
+        rows[d:] |= tiles[:-d]
+        rows[:-d] |= tiles[d:]
+    return rows.sum(axis=1).astype(np.float64)
+
+
+def decompose_balanced(work: np.ndarray, parts: int, floor: float = 0.05, min_rows: int = 2) -> List[tuple]:
+    """Contiguous row blocks [row0, row1) with near-equal work (strong scaling): `work` per
+    row (row_work), plus `floor` x its mean per row so dry rows are not free (boundary
+    fill, tile lists, later spreading).  Every slab keeps >= min_rows rows."""
+    nrows = len(work)
+    if parts < 1 or nrows < min_rows * parts:
+        raise ValueError(f"cannot split {nrows} rows into {parts} slabs of >= {min_rows} rows")
+    w = np.asarray(work, dtype=np.float64)
+    w = w + floor * max(w.mean(), 1e-300)
+    cum = np.concatenate([[0.0], np.cumsum(w)])
+    out, r = [], 0
+    for k in range(parts):
+        if k == parts - 1:
+            r1 = nrows
+        else:
+            target = cum[-1] * (k + 1) / parts
+            r1 = int(np.searchsorted(cum, target))
+            r1 = max(r1, r + min_rows)
+            r1 = min(r1, nrows - min_rows * (parts - 1 - k))
+        out.append((r, r1))
+        r = r1
+    return out
+
+
 def decompose(nrows: int, parts: int) -> List[tuple]:
     """Balanced contiguous row blocks [row0, row1) (each >= 2 rows)."""
     if parts < 1 or nrows < 2 * parts:
@@ -301,33 +352,55 @@ def assemble(states: Sequence[np.ndarray]) -> np.ndarray:
 # ---------------------------------------------------------------------------
 # bench.py --gpus N (torchrun): weak scaling, one slab per rank, device-resident exchange
 # ---------------------------------------------------------------------------
-def _slab_roofline(cells: int, world: int, steps: int, ms: float) -> dict:
-    """Per-GPU HBM roofline of a slab run: 464 algorithmic bytes per cell-update
-     of this GPU's share of the cells over the step time (the two stage
-    kernels are >= 96 % of it), against MEASURED_PEAKS.json hbm_gbs."""
+def bench_scenario(args, world: int):
+    """The grid bench.py runs at N = world GPUs, and the `stack` argument of the CPU
+    reference on it (oracle/cpu_bench.py).  weak: one copy of the N=1 workload per GPU,
+    stacked along the rows (Mode-II C3 stretches the channel instead); strong: the one
+    N=1 grid split N ways."""
+    from . import scenarios
+    if args.config == "c1":
+        base = scenarios.c1_hill(args.ncols)
+    elif args.config == "c3":
+        base = scenarios.SCENARIOS["c3"](args.ncols, args.nrows * (world if args.scaling == "weak" else 1))
+    else:
+        base = scenarios.SCENARIOS[args.config](args.ncols, args.nrows)
+    if args.scaling == "strong":
+        return base, 1
+    if args.config == "c3":
+        return base, world
+    return scenarios.stacked(base, world), world
+
+
+def bench_decomposition(sc, world: int, scaling: str) -> List[tuple]:
+    """weak: equal rows (every slab is one copy of the workload); strong: equal work
+    (wet-tile count from the initial state, decompose_balanced)."""
+    if scaling == "strong":
+        return decompose_balanced(row_work(sc), world)
+    return decompose(sc.nrows, world)
+
+
+def _peak_hbm():
     import json
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    peak, src = 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
     pp = os.path.join(root, "MEASURED_PEAKS.json")
     if os.path.exists(pp):
         with open(pp) as f:
-            peak, src = float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
-    achieved = 464.0 * (cells / world) * steps / (ms / 1e3) / 1e9
-    return {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-            "frac": round(achieved / peak, 4), "traffic": None,
-            "kernel": "whole step per GPU (stage_kernel<pred>+stage_kernel<corr> dominate)",
-            "peak_source": src}
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
 def bench_main(args, metric: str, clock_sampler=None) -> None:
-    """Each rank owns a [rows_per x ncols] slab of one (ncols x rows_per*N) grid of the
-    chosen scenario; slabs are joined by the device-resident exchange (tp_peer.cu over
-    CUDA IPC / NVLink).  Timed: K steps of the device loop on every rank, CUDA events on
-    the launching stream, max over ranks."""
+    """One slab per rank of the bench grid (bench_scenario), joined by the device-resident
+    exchange (tp_peer.cu over CUDA IPC / NVLink).  Timed: K steps of the device loop on
+    every rank along the run's output schedule, CUDA events on the launching stream, max
+    over ranks.  Also: the stage kernels' roofline per rank (processed-tile bytes, max over
+    ranks of the kernel time), e2e through the C ABI with pinned host buffers, and the CPU
+    reference on the same grid (rank 0)."""
     import json
+    import time
     import torch
     import torch.distributed as dist
-    from . import scenarios
+    import bench as B
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -335,92 +408,125 @@ def bench_main(args, metric: str, clock_sampler=None) -> None:
     ndev = torch.cuda.device_count()
     dev = local % ndev  # one GPU per rank; fewer GPUs than ranks only for functional runs
     torch.cuda.set_device(dev)
+    nccl = ndev >= world
     if not dist.is_initialized():
-        dist.init_process_group("nccl" if ndev >= world else "gloo",
-                                **({"device_id": torch.device(f"cuda:{dev}")} if ndev >= world else {}))
-    rows_per = args.nrows
-    # weak scaling: every rank's slab is one copy of the single-GPU workload (the N=1 line's
-    # config), stacked along the rows; Mode-II (C3) stretches the channel instead
-    if args.config == "c1":
-        base = scenarios.c1_hill(args.ncols)
-    elif args.config == "c3":
-        base = scenarios.SCENARIOS["c3"](args.ncols, rows_per * world)
-    else:
-        base = scenarios.SCENARIOS[args.config](args.ncols, rows_per)
-    sc = base if args.config == "c3" else scenarios.stacked(base, world)
-    rows = decompose(sc.nrows, world)[rank]
+        dist.init_process_group("nccl" if nccl else "gloo",
+                                **({"device_id": torch.device(f"cuda:{dev}")} if nccl else {}))
+
+    def reduce_max(vals):
+        t = torch.tensor(vals, dtype=torch.float64)
+        if nccl:
+            t = t.cuda()
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return [float(x) for x in t.cpu()]
+
+    def reduce_sum(vals):
+        t = torch.tensor(vals, dtype=torch.float64)
+        if nccl:
+            t = t.cuda()
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return [float(x) for x in t.cpu()]
+
+    sc, stack = bench_scenario(args, world)
+    parts = bench_decomposition(sc, world, args.scaling)
+    rows = parts[rank]
     stream = torch.cuda.Stream()
     slab = CudaSlab(sc, rows, device=dev, stream=stream)
     peer_connect_ranks(slab)
     sim = slab.sim
     sim.set_option("graph_steps", args.graph_steps)
-    tu = sc.config.scaling.t_unit()
-    t_end = sc.config.t_end / tu
-    t_next = min(sc.config.dt_out / tu, t_end)
+    clock = B.RunClock(sim)
 
-    t, n0, _ = sim.steps(0.0, t_next, args.warmup, t_end=t_end)
+    clock.advance(args.warmup)
     torch.cuda.synchronize()
     dist.barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     clocks = clock_sampler(dev) if clock_sampler else None
     if clocks:
         clocks.__enter__()
-    torch.cuda.synchronize()
-    e0.record(stream)
-    t, n, _ = sim.steps(t, t_next, args.steps, t_end=t_end)
-    e1.record(stream)
-    torch.cuda.synchronize()
+    ms_local = B.timed_steps(sim, clock, stream, args.steps)
     if clocks:
         clocks.__exit__(None, None, None)
     launches = sim.kernel_launches()
     act_p, act_c, ntiles = sim.active_tiles()
-    ms_t = torch.tensor([e0.elapsed_time(e1), float(n)], dtype=torch.float64)
-    if dist.get_backend() == "nccl":
-        ms_t = ms_t.cuda()
-    dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
-    ms, nmax = float(ms_t[0]), int(ms_t[1])
-    assert n == args.steps == nmax, (n, args.steps, nmax)
+    ms, = reduce_max([ms_local])
     cells = sc.ncols * sc.nrows
     value = cells * args.steps / (ms / 1e3) / 1e9
 
+    # roofline of the stage kernels on this rank's slab; whole-job: processed bytes of all
+    # ranks over the slowest rank's kernel time, against world x the per-GPU peak
+    peak, peak_src = _peak_hbm()
+    slab_cells = sc.ncols * (rows[1] - rows[0])
+    rl = B.stage_roofline(sim, clock, slab_cells, args.roofline_reps, peak)
+    kms, = reduce_max([rl["kernel_ms_per_step"]])
+    alg_all, = reduce_sum([rl["alg_bytes_per_step"]])
+    achieved = alg_all / (kms / 1e3) / 1e9 / world
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": None,
+                "kernel": "stage_kernel<pred>+stage_kernel<corr> per step, per GPU: processed-tile "
+                          "algorithmic bytes of all ranks / N / the slowest rank's kernel time",
+                "peak_source": peak_src, "kernel_ms_per_step_max": round(kms, 4),
+                "rank0": {k: rl[k] for k in ("frac", "kernel_ms_per_step", "processed_tile_frac")}}
+    nt = B.ncu_traffic()
+    if nt:
+        for cand in (nt, nt.get("wet"), nt.get("c5")):
+            if cand and cand.get("grid") == [sc.ncols, (rows[1] - rows[0])] and cand.get("config") == args.config:
+                roofline["traffic"] = cand["dram_bytes_per_step"]
+
     # e2e: the same steps through the C ABI with this rank's state from / to pinned host memory
+    import ctypes as Cc
     nbytes = 6 * sim.ny * sim.nx * 8
     h_in = torch.empty(6 * sim.ny * sim.nx, dtype=torch.float64, pin_memory=True)
     h_out = torch.empty_like(h_in, pin_memory=True)  # empty_like alone is pageable
     assert h_in.is_pinned() and h_out.is_pinned()
-    dp = C.POINTER(C.c_double)
-    sim._check(sim.L.tp_get_state(sim.h, C.cast(h_in.data_ptr(), dp)))
-    sim._check(sim.L.tp_get_state(sim.h, C.cast(h_out.data_ptr(), dp)))
+    dp = Cc.POINTER(Cc.c_double)
+    sim._check(sim.L.tp_get_state(sim.h, Cc.cast(h_in.data_ptr(), dp)))
+    sim._check(sim.L.tp_get_state(sim.h, Cc.cast(h_out.data_ptr(), dp)))
+    torch.cuda.synchronize()
     dist.barrier()
-    import time
     w0 = time.perf_counter()
-    sim._check(sim.L.tp_set_state(sim.h, C.cast(h_in.data_ptr(), dp)))
-    t2, ne, _ = sim.steps(t, t_next, args.steps, t_end=t_end)
-    sim._check(sim.L.tp_get_state(sim.h, C.cast(h_out.data_ptr(), dp)))
-    w = torch.tensor([time.perf_counter() - w0], dtype=torch.float64)
-    if dist.get_backend() == "nccl":
-        w = w.cuda()
-    dist.all_reduce(w, op=dist.ReduceOp.MAX)
-    e2e_v = cells * ne / float(w[0]) / 1e9
+    sim._check(sim.L.tp_set_state(sim.h, Cc.cast(h_in.data_ptr(), dp)))
+    ne = clock.advance(args.steps)
+    sim._check(sim.L.tp_get_state(sim.h, Cc.cast(h_out.data_ptr(), dp)))
+    w, = reduce_max([time.perf_counter() - w0])
+    e2e_v = cells * ne / w / 1e9
+    h2d_all, = reduce_sum([float(nbytes)])
+
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        lanes = os.cpu_count() or 1
+        try:
+            c = B.cpu_reference(args.config, args.ncols, args.nrows, max(1, args.cpu_steps // max(stack, 1)),
+                                lanes, stack=stack)
+            cpu = {"value": round(c["value"] / 1e9, 6), "unit": "GCUPS", "cores": c["lanes"],
+                   "kind": "reference" if c["kind"] == "ref" else "port",
+                   "sample": f"{c['steps']} steps of the same {sc.ncols}x{sc.nrows} grid from t=0 "
+                             f"(after 1 untimed step), BackendConfig::parallel({c['lanes']})",
+                   "seconds": round(c["seconds"], 3)}
+        except Exception as e:  # noqa: BLE001 - reported, not fatal to the GPU arm
+            cpu = {"unavailable": str(e)[:200]}
     if rank == 0:
+        cfg = B.workload_config(sc)
+        cfg.update({"parallelism": f"slab{world}", "scaling_mode": args.scaling,
+                    "slab_rows": [int(r1 - r0) for r0, r1 in parts],
+                    "decomposition": ("equal work: wet-tile rows of the initial state (decompose_balanced)"
+                                      if args.scaling == "strong" else "equal rows: one workload copy per GPU"),
+                    "exchange": "halo rows stored into the neighbour's buffers over peer memory, "
+                                "lambda all-reduce in device memory (tp_peer.cu)",
+                    "gpus_visible": ndev, "graph_steps": args.graph_steps,
+                    "l2": ("per-rank inputs larger than L2" if 18 * sim.ny * sim.nx * 8 > 126e6 else
+                           "per-rank inputs fit in L2 (functional size)"),
+                    "active_tiles_last_step_rank0": [act_p, act_c, ntiles]})
         out = {"metric": metric, "value": round(value, 4), "unit": "GCUPS", "n_gpus": world,
                "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 5),
-               "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+               "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
                "data": f"synthetic (deterministic {sc.name} generator in scenarios.py; no network data)",
-               "config": {"workload": f"{sc.name} {sc.ncols}x{sc.nrows} (weak: one {args.ncols}x{rows_per} "
-                                      f"copy of the single-GPU workload per GPU, stacked along the rows), "
-                                      f"row-block slabs joined by the device-resident exchange "
-                                      f"(halo rows stored into the neighbour's buffers over peer memory, "
-                                      f"lambda all-reduce in device memory; tp_peer.cu)",
-                          "grid": [sc.ncols, sc.nrows], "parallelism": f"slab{world}",
-                          "gpus_visible": ndev,
-                          "l2": ("per-rank inputs larger than L2" if 18 * sim.ny * sim.nx * 8 > 126e6 else
-                                 "per-rank inputs fit in L2 (functional size)"),
-                          "active_tiles_last_step_rank0": [act_p, act_c, ntiles]},
-               "e2e": {"value": round(e2e_v, 4), "unit": "GCUPS", "h2d_bytes_per_step": nbytes // max(ne, 1),
-                       "d2h_bytes_per_step": nbytes // max(ne, 1),
-                       "mode": f"per rank: tp_set_state(pinned host) + tp_steps({ne}) + tp_get_state, max over ranks"},
-               "roofline": _slab_roofline(cells, world, args.steps, ms),
+               "config": cfg,
+               "e2e": {"value": round(e2e_v, 4), "unit": "GCUPS",
+                       "h2d_bytes_per_step": int(h2d_all) // max(ne, 1),
+                       "d2h_bytes_per_step": int(h2d_all) // max(ne, 1),
+                       "mode": f"every rank: tp_set_state(pinned host) + tp_steps({ne}) + tp_get_state, "
+                               f"wall clock, max over ranks"},
+               "roofline": roofline, "cpu_baseline": cpu,
                "clocks": clocks.summary() if clocks else None,
                "gpu_launches": launches}
         print(json.dumps(out))

@@ -74,3 +74,25 @@ def test_reference_arm_runs_the_weak_scaling_grid():
     quiet = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--gpus", "2", "--steps", "1"],
                            cwd=root, capture_output=True, text=True, timeout=600, env=env)
     assert quiet.returncode == 0 and not quiet.stdout.strip()
+
+
+def test_balanced_decomposition_follows_wet_rows():
+    """Strong scaling (bench.py --scaling strong): slab boundaries split the wet-tile work
+    of the initial state evenly, not the rows."""
+    from paper_2104_06784_b200.distributed import decompose_balanced, row_work
+    sc = scenarios.c4_terrain(400, 300)
+    w = row_work(sc)
+    assert w.shape == (300,) and w.max() > 0
+    for parts in (2, 3, 4, 8):
+        p = decompose_balanced(w, parts)
+        assert p[0][0] == 0 and p[-1][1] == 300
+        assert all(a[1] == b[0] for a, b in zip(p[:-1], p[1:]))
+        assert all(r1 - r0 >= 2 for r0, r1 in p)
+        loads = [w[r0:r1].sum() + 0.05 * w.mean() * (r1 - r0) for r0, r1 in p]
+        # each slab within one row's work of the mean (rows are indivisible)
+        assert max(loads) - min(loads) <= 2 * (w.max() + 0.05 * w.mean()) + 1e-9, (parts, loads)
+    # a release in the top quarter only: the top slabs get fewer rows
+    sc2 = scenarios.c2_valley(160, 200)
+    p = decompose_balanced(row_work(sc2), 4)
+    sizes = [r1 - r0 for r0, r1 in p]
+    assert sizes != [50, 50, 50, 50]

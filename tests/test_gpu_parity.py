@@ -513,10 +513,41 @@ def test_regularize_clips_small_negatives(gpu, oracle_kind):
     a_r, a_g = ref.audit(), sim.audit_array()
     assert a_r[4] != 0.0 and a_r[9] != 0.0
     np.testing.assert_allclose(a_g, a_r, rtol=1e-12, atol=1e-300)
+    # the clipped slots are folded in the reference's (j, i) order (ClipList): bit for bit
+    assert_bitwise(a_g[[4, 9]], a_r[[4, 9]], "clipped audit")
     tr, dts_r, _ = ref.steps(0.0, 1.0e9, 20, t_end=1.0e9)
     tg, dts_g, _ = sim.steps(0.0, 1.0e9, 20, t_end=1.0e9, record_dts=True)
     assert_bitwise(dts_g, dts_r, "dt sequence")
     assert_bitwise(sim.state(), ref.state(), "state after 20 steps")
+    assert_bitwise(sim.audit_array()[[4, 9]], ref.audit()[[4, 9]], "clipped audit after 20 steps")
+
+
+def test_clipped_audit_in_device_loop_bitwise(gpu, oracle_kind):
+    """Small negative thicknesses planted in dry cells before each run are clipped by the
+    stage kernels' regularize (predictor: -w, corrector: the Heun average -w/2) inside the
+    device loop; the clipped slots of the audit match the reference's serial (j, i) sums bit
+    for bit (ClipList, tp_types.h)."""
+    sc = scenarios.c1_hill(72)
+    ref, sim = _pair(sc, oracle_kind)
+    rng = np.random.default_rng(11)
+    t = 0.0
+    for rnd in range(4):
+        s = ref.state()
+        dry = np.argwhere((s[0, 3:-3, 3:-3] == 0.0) & (s[1, 3:-3, 3:-3] == 0.0))
+        for k in rng.choice(len(dry), 80, replace=False):
+            j, i = dry[k] + 3
+            s[int(rng.integers(0, 2)), j, i] = -float(rng.uniform(1e-15, 4e-13))
+        ref.set_state(s)
+        sim.set_state(s)
+        tr, dts_r, _ = ref.steps(t, 1.0e9, 3, t_end=1.0e9)
+        tg, dts_g, _ = sim.steps(t, 1.0e9, 3, t_end=1.0e9, record_dts=True)
+        assert_bitwise(dts_g, dts_r, f"dt sequence, round {rnd}")
+        assert tg == tr
+        t = tr
+        assert_bitwise(sim.state(), ref.state(), f"state, round {rnd}")
+        a_r, a_g = ref.audit(), sim.audit_array()
+        assert_bitwise(a_g[[4, 9]], a_r[[4, 9]], f"clipped audit, round {rnd}")
+    assert a_r[4] != 0.0 and a_r[9] != 0.0
 
 
 def _fuzz_scenario(seed):

@@ -177,3 +177,38 @@ def test_fuzz_peer_slabs(gpu, oracle_kind, seed):
         assert_bitwise(assemble([s.state() for s in slabs]), ref.state()[:, 3:-3, 3:-3], f"interior, interval {k}")
         if t_r >= t_end:
             break
+
+
+@pytest.mark.parametrize("parts", [2, 3, 4])
+def test_peer_error_stops_every_rank(gpu, oracle_kind, parts):
+    """A NumericsError inside a peer-joined run (regularize's negative thickness,
+    solver.cpp:147-152) stops every slab at the same step through the next step's stop-flag
+    exchange (tp_peer.cu): the group raises the reference's error text instead of a
+    neighbour timeout.  With max_steps below graph_steps every replay is a one-step graph,
+    so the error lands on the last step of a replay."""
+    import torch
+    from oracle.oracle import OracleError, OracleSim
+    from paper_2104_06784_b200.config import NumericsError
+    sc = scenarios.wet_valley(64, 60)
+    ref = OracleSim(sc, oracle_kind)
+    rows = decompose(sc.nrows, parts)
+    slabs = [CudaSlab(sc, r, stream=torch.cuda.Stream()) for r in rows]
+    group = PeerGroup(slabs)
+    t_r, d_r, _ = ref.steps(0.0, 1e9, 3, t_end=1e9)
+    t_g, n_g, _ = group.steps(0.0, 1e9, 3, t_end=1e9)
+    assert t_g == t_r and n_g == 3
+    # plant a strongly negative solid thickness in the interior of the last slab
+    k = parts - 1
+    r0, r1 = rows[k]
+    J, I = (r0 + r1) // 2, 30
+    s = ref.state()
+    s[0, J + 3, I + 3] = -5.0  # far below what one step's inflow can refill
+    ref.set_state(s)
+    ls = slabs[k].state()
+    ls[0, J - r0 + 3, I + 3] = -5.0
+    slabs[k].sim.set_state(ls)
+    with pytest.raises(OracleError) as er:
+        ref.steps(t_r, 1e9, 10, t_end=1e9)
+    with pytest.raises(NumericsError) as eg:
+        group.steps(t_g, 1e9, 10, t_end=1e9)
+    assert str(eg.value) == str(er.value)
