@@ -26,7 +26,7 @@
 
 namespace tpb {
 size_t stage_smem_bytes();
-cudaError_t launch_stage(const StageArgs& a, bool fastdiv, bool corr, cudaStream_t st);
+cudaError_t launch_stage(const StageArgs& a, bool fastdiv, bool corr, bool peer, cudaStream_t st);
 cudaError_t launch_bc(const BcArgs& a, cudaStream_t st);
 cudaError_t launch_ghost_copy(const GridDesc& g, const double* src, double* dst, cudaStream_t st);
 cudaError_t launch_lambda(const GridDesc& g, const Phys& P, const double* s, const double* geo,
@@ -46,7 +46,7 @@ cudaError_t launch_init_velocity(const GridDesc& g, const double* geo, const dou
 cudaError_t launch_geo_check(const GridDesc& g, const double* geo, int* ok, cudaStream_t st);
 cudaError_t launch_peer_lambda(const PeerLink& L, DevScalars* sc, cudaStream_t st);
 cudaError_t launch_peer_halo(const PeerLink& L, const GridDesc& g, const double* s, int buf, DevScalars* sc,
-                             const CondArgs& ca, cudaStream_t st);
+                             cudaStream_t st);
 cudaError_t launch_pack_state(const GridDesc& g, const double* src, double* dst, bool unpack, cudaStream_t st);
 cudaError_t launch_mass(const GridDesc& g, const double* s, double* part, int blocks, cudaStream_t st);
 cudaError_t launch_snapshot(const GridDesc& g, const double* s, const double* geo, double* out, int ncols,
@@ -72,6 +72,7 @@ inline void ck(cudaError_t e, const char* what) {
 }
 
 constexpr size_t kCtrlBytes = offsetof(DevScalars, lam_bits);
+constexpr int kNactInts = 10;
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -138,8 +139,6 @@ struct tp_ctx {
     double* dTallyC = nullptr;
     signed char* dSide = nullptr;
     unsigned char* dInflowTiles = nullptr;  // per tile: its radius-2 box reads an inflow ghost
-    int* dCond = nullptr;   // conditional tiles of the stage in flight (peer-joined slabs)
-    int* dNcond = nullptr;
     double* dSamples = nullptr;
     double* dDts = nullptr;
     long dts_cap = 0;
@@ -163,8 +162,10 @@ struct tp_ctx {
     bool peered = false;
     unsigned long long peer_base = 0; // host copy of DevScalars::peer_base
     std::vector<void*> ipc_opened;    // CUDA-IPC mappings to close at destroy
-    int* dNact = nullptr;             // [8] list counts pred, corr; last-launch stats pred, corr;
-                                      // safe-tile counts pred, corr; tile-scheduler counters
+    int* dNact = nullptr;             // [kNactInts] list counts pred, corr; last-launch stats pred, corr;
+                                      // safe-tile counts pred, corr; tile-scheduler counters;
+                                      // back-region counts pred, corr (peer-joined slabs)
+    int stage_ctas = 0;               // stage grid cap (0: 2 per SM); peers sharing this device leave SMs free
     int last_tiles_stage = 1;         // stage of the last tiles_kernel enqueued (0 pred, 1 corr)
     bool lam_valid = false;
     bool ghosts_in_B = false;
@@ -289,20 +290,20 @@ tpb::StageArgs stage_args(tp_ctx* c, bool corr, int loop) {
     a.flag_out = corr ? c->dFlagA : c->dFlagB;
     a.nact_stat = c->dNact + 2;
     a.work = c->dNact + 6 + (corr ? 1 : 0);
+    a.nback = c->dNact + 8 + (corr ? 1 : 0);
+    a.max_ctas = c->stage_ctas;
+    if (loop && c->peered) {  // stage_kernel<..., PEER>: halo tiles wait in the kernel (tp_peer.cu)
+        const int buf = corr ? 1 : 0;
+        for (int side = 0; side < 2; ++side) {
+            a.has_nbr[side] = c->link.nbr_state[buf][side] ? 1 : 0;
+            a.halo_seq[side] = &c->dBox->halo_seq[buf][side];
+            a.halo_nz[side] = c->dBox->halo_nz[buf][side];
+        }
+        a.nyi = c->ny - 6;
+        a.peer_phase = 1 + buf;
+        a.timeout_ns = c->link.timeout_ns;
+    }
     return a;
-}
-
-tpb::CondArgs cond_args(tp_ctx* c, const tpb::StageArgs& a, bool corr) {
-    tpb::CondArgs ca{};
-    ca.tiles = c->dTiles;
-    ca.ntiles_active = c->dNact + (corr ? 1 : 0);
-    ca.cond_tiles = c->dCond;
-    ca.ncond = c->dNcond;
-    ca.tally = a.tally;
-    ca.ntx = c->ntx;
-    ca.nty = c->nty;
-    ca.nyi = c->ny - 6;
-    return ca;
 }
 
 tpb::TileArgs tile_args(tp_ctx* c, const tpb::StageArgs& a, bool corr) {
@@ -327,9 +328,9 @@ tpb::TileArgs tile_args(tp_ctx* c, const tpb::StageArgs& a, bool corr) {
     t.south_ineligible = c->g.has_south ? 0 : 1;
     t.north_ineligible = c->g.has_north ? 0 : 1;
     t.safe_ok = (c->fastdiv && c->geo_safe && c->geo_safe2) ? 1 : 0;
-    t.cond_halo = (a.loop && c->peered && c->ntx <= tpb::kMaxTileCols) ? 1 : 0;
-    t.cond_tiles = c->dCond;
-    t.ncond = c->dNcond;
+    t.cond_halo = (a.loop && c->peered) ? 1 : 0;
+    t.nback = c->dNact + 8 + (corr ? 1 : 0);
+    t.nback_reset = c->dNact + 8 + (corr ? 0 : 1);
     t.loop = a.loop;
     t.sc = c->dSc;
     return t;
@@ -351,7 +352,7 @@ cudaError_t launch_stage_sel(tp_ctx* c, const tpb::StageArgs& a, bool fastdiv, b
     cudaError_t e = tpb::launch_tiles(t, st);
     if (e != cudaSuccess) return e;
     if (ev0 && (e = cudaEventRecord(ev0, st)) != cudaSuccess) return e;
-    e = tpb::launch_stage(a, fastdiv, corr, st);
+    e = tpb::launch_stage(a, fastdiv, corr, false, st);
     if (e == cudaSuccess && ev1) e = cudaEventRecord(ev1, st);
     return e;
 }
@@ -413,13 +414,11 @@ void enqueue_loop_step(tp_ctx* c, cudaEvent_t* ev = nullptr) {
         ck(tpb::launch_pre(p, c->stream), corr ? "pre (corrector)" : "pre (predictor)");
         c->last_tiles_stage = corr;
         // halo rows after apply_boundaries (solver.cpp:639, :523), straight into the
-        // neighbours' buffers, then wait for theirs
+        // neighbours' buffers; the stage kernel waits for theirs before its halo tiles
         if (c->peered)
-            ck(tpb::launch_peer_halo(c->link, c->g, corr ? c->dB : c->dA, corr, c->dSc, cond_args(c, sa, corr != 0),
-                                     c->stream),
-               "peer halo");
+            ck(tpb::launch_peer_halo(c->link, c->g, corr ? c->dB : c->dA, corr, c->dSc, c->stream), "peer halo");
         if (ev) ck(cudaEventRecordWithFlags(ev[2 * corr], c->stream, cudaEventRecordExternal), "event");
-        ck(tpb::launch_stage(sa, c->fastdiv, corr != 0, c->stream), corr ? "corrector" : "predictor");
+        ck(tpb::launch_stage(sa, c->fastdiv, corr != 0, c->peered, c->stream), corr ? "corrector" : "predictor");
         if (ev) ck(cudaEventRecordWithFlags(ev[2 * corr + 1], c->stream, cudaEventRecordExternal), "event");
     }
     launch_post(c, 1);
@@ -709,11 +708,8 @@ void create_impl(tp_ctx* c, const tp_params* p, const tp_dem* dem, int row0, int
     ck(cudaMalloc(&c->dTiles, sizeof(int) * ntiles), "cudaMalloc tiles");
     ck(cudaMalloc(&c->dBox, sizeof(tpb::PeerBox)), "cudaMalloc mailbox");
     ck(cudaMemsetAsync(c->dBox, 0, sizeof(tpb::PeerBox), c->stream), "memset");
-    ck(cudaMalloc(&c->dNact, 8 * sizeof(int)), "cudaMalloc tiles");
-    ck(cudaMalloc(&c->dCond, sizeof(int) * ntiles), "cudaMalloc cond tiles");
-    ck(cudaMalloc(&c->dNcond, sizeof(int)), "cudaMalloc cond count");
-    ck(cudaMemsetAsync(c->dNcond, 0, sizeof(int), c->stream), "memset");
-    ck(cudaMemsetAsync(c->dNact, 0, 8 * sizeof(int), c->stream), "memset");
+    ck(cudaMalloc(&c->dNact, kNactInts * sizeof(int)), "cudaMalloc tiles");
+    ck(cudaMemsetAsync(c->dNact, 0, kNactInts * sizeof(int), c->stream), "memset");
     invalidate_flags(c, true, true);
     if (c->host_geometry) {
             // device geometry layout (tp_types.h GeoField): the 14 reference fields
@@ -834,8 +830,6 @@ void tp_destroy(tp_ctx* c) {
     cudaFree(c->dTallyP);
     cudaFree(c->dTallyC);
     cudaFree(c->dInflowTiles);
-    cudaFree(c->dCond);
-    cudaFree(c->dNcond);
     cudaFree(c->dSide);
     cudaFree(c->dSamples);
     cudaFree(c->dDts);
@@ -1155,6 +1149,7 @@ void steps_begin(tp_ctx* c, StepsRun& r, double t, double t_next, double t_end, 
     if (c->last_tiles_stage == 0) {  // the graphs start with a predictor list
         ck(cudaMemsetAsync(c->dNact, 0, sizeof(int), c->stream), "memset");
         ck(cudaMemsetAsync(c->dNact + 4, 0, sizeof(int), c->stream), "memset");
+        ck(cudaMemsetAsync(c->dNact + 8, 0, sizeof(int), c->stream), "memset");
     }
     c->last_tiles_stage = 1;
 }
@@ -1163,7 +1158,7 @@ void steps_launch(tp_ctx* c, StepsRun& r) {
     const bool big = (r.max_steps - r.h.steps) >= c->graph_steps;
     const int k = big ? c->graph_steps : 1;
     ck(cudaGraphLaunch(big ? c->graphK : c->graph1, c->stream), "graph launch");
-    c->launches += (c->peered ? 10L : 5L) * k;
+    c->launches += (c->peered ? 8L : 5L) * k;  // peered: + lambda exchange + 2 halo pushes
     r.launched += k;
 }
 
@@ -1378,8 +1373,16 @@ int tp_peer_connect_local(tp_ctx* c, int rank, int nranks, tp_ctx* const* all) {
         tpb::PeerLink L{};
         // peer_lambda_kernel stores into every rank's mailbox, peer_halo_push_kernel into the
         // neighbours' state: peer access to every other device of the group
+        c->stage_ctas = 0;
         for (int r = 0; r < nranks; ++r) {
             L.box[r] = all[r]->dBox;
+            if (r != rank && all[r]->device == c->device) {
+                // members sharing this device run their kernels beside this one's stage kernel,
+                // which may wait for their halo pushes: leave 4 SMs to them
+                int sms = 148;
+                cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+                c->stage_ctas = 2 * (sms - 4);
+            }
             if (all[r]->device != c->device) {
                 const cudaError_t e = cudaDeviceEnablePeerAccess(all[r]->device, 0);
                 if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) ck(e, "peer access");
@@ -1423,6 +1426,7 @@ int tp_steps_timed(tp_ctx* c, double t_next, double t_end, long max_steps, doubl
         if (c->last_tiles_stage == 0) {
             ck(cudaMemsetAsync(c->dNact, 0, sizeof(int), c->stream), "memset");
             ck(cudaMemsetAsync(c->dNact + 4, 0, sizeof(int), c->stream), "memset");
+            ck(cudaMemsetAsync(c->dNact + 8, 0, sizeof(int), c->stream), "memset");
         }
         c->last_tiles_stage = 1;
         DevScalars h{};

@@ -25,6 +25,7 @@
 
 #include "tp_face.cuh"
 #include "tp_stage_common.cuh"
+#include "tp_sync.cuh"
 #include "tp_types.h"
 
 namespace tpb {
@@ -287,7 +288,7 @@ __device__ __forceinline__ void stage_phase1(const double* __restrict__ S, const
 // ---------------------------------------------------------------------------
 // The fused stage kernel.
 // ---------------------------------------------------------------------------
-template <bool FD, bool CORR>
+template <bool FD, bool CORR, bool PEER>
 __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ StageArgs A) {
     extern __shared__ __align__(128) double sm[];
     __shared__ unsigned long long bar;   // state + stencil-geometry boxes
@@ -314,9 +315,49 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
     const double* __restrict__ geo = A.geo;
     const long long fs = g.fs;
     const int ntiles = A.ntx * A.nty;
-    const int nact = *A.ntiles_active;  // active-tile list of this stage (tiles_kernel)
+    // active-tile list of this stage (tiles_kernel); PEER: plus its back region (StageArgs::nback)
+    const int n_main = *A.ntiles_active;
+    const int nact = n_main + (PEER ? *A.nback : 0);
     if (blockIdx.x == 0 && threadIdx.x == 0) A.nact_stat[CORR ? 1 : 0] = nact;  // diagnostics
     const double dt = sc->dt;
+    // list entry li: the front of `tiles`, then (PEER) its back region from the end
+    auto entry_at = [&](int li) { return (!PEER || li < n_main) ? A.tiles[li] : A.tiles[ntiles - 1 - (li - n_main)]; };
+    // PEER, thread 0: make li a tile to process (or >= nact).  A back-region tile needs the
+    // neighbours' halo rows of this stage: the first one waits for their sequence numbers
+    // (tp_peer.cu); a conditional one (kTileCond) is dropped when the pushed rows hold only
+    // +0.0 in its box columns (then it is a bitwise no-op: its ring tally slot is zeroed) and
+    // the next entry is claimed instead.
+    bool halo_ok = false;
+    auto resolve = [&](int li, int& e) -> int {
+        e = 0;
+        while (li < nact) {
+            e = entry_at(li);
+            if (!PEER || li < n_main) return li;
+            if (!halo_ok) {
+                const unsigned long long want = seq_of(sc, A.peer_phase);
+                for (int side = 0; side < 2; ++side) {
+                    if (A.has_nbr[side] && !wait_seq(A.halo_seq[side], want, A.timeout_ns)) {
+                        atomicMin(&sc->err_key, kPeerTimeoutKey);
+                        sc->done = 1;
+                    }
+                }
+                halo_ok = true;
+            }
+            if (!(e & kTileCond)) return li;
+            const int tx = e & 0xffff, ty = (e >> 16) & 0x1fff;
+            bool keep = false;
+            if (ty == 0) keep |= !A.has_nbr[0] || A.halo_nz[0][tx] != 0u;
+            if ((ty + 1) * TY + 1 >= A.nyi) keep |= !A.has_nbr[1] || A.halo_nz[1][tx] != 0u;
+            if (keep) return li;
+            if (tx == 0 || tx == A.ntx - 1 || ty == 0 || ty == A.nty - 1) {
+                double* t4 = A.tally + 4ll * (static_cast<long long>(ty) * A.ntx + tx);
+                t4[0] = t4[1] = t4[2] = t4[3] = 0.0;
+            }
+            atomicAdd(&sc->cond_skips, 1ull);
+            li = static_cast<int>(gridDim.x) + atomicAdd(A.work, 1);
+        }
+        return li;
+    };
 
     // Persistent tiles: block b walks tiles b, b+G, b+2G, ... (row-major, so the
     // tiles in flight at any time are neighbours and share halos in L2).  The
@@ -329,31 +370,33 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
             tma_load_3d(sm + SM_C, &A.tm_c, 3 + (e & 0xffff) * TX + 1, 3 + ((e >> 16) & 0x1fff) * TY, G_NX, &barc);
         }
     };
-    (void)ntiles;
+    __shared__ int s_li0;  // this CTA's first list index (PEER: after resolve)
     if (threadIdx.x == 0) {
         mbar_init(&bar, 1);
         mbar_init(&barc, 1);
         mbar_init(&baru, 1);
-        if (static_cast<int>(blockIdx.x) < nact) {
-            const int e = A.tiles[blockIdx.x];
+        int e = 0;
+        const int li0 = resolve(static_cast<int>(blockIdx.x), e);
+        s_li0 = li0;
+        if (li0 < nact) {
             s_tile = e;
             const int bx0 = 1 + (e & 0xffff) * TX, by0 = 1 + ((e >> 16) & 0x1fff) * TY;
             mbar_expect_tx(&bar, kTmaBytes);
             // x coordinate + 1: the leading pad column of the device layout (tp_capi.cpp)
             tma_load_3d(S, &A.tm_s, bx0 + 1, by0, 0, &bar);
             tma_load_3d(sm + SM_G, &A.tm_g, bx0 + 1, by0, 0, &bar);
-            issue_cell(blockIdx.x, e);
+            issue_cell(li0, e);
         }
     }
     if (threadIdx.x == 0) s_flags = 0u;
-    __syncthreads();  // barrier init visible to all threads
+    __syncthreads();  // barrier init (and s_li0) visible to all threads
     double lam_local = 0.0;
     unsigned iter = 0;
     TPROBE_DECL
     // Dynamic tile scheduler: every CTA starts on list entry blockIdx.x, then claims the
     // next entry with one atomic per tile (claimed a tile ahead, so the TMA prefetch still
     // has a target) - CTAs that drew cheap, partially dry tiles take more of them.
-    for (int li = blockIdx.x; li < nact; ++iter) {
+    for (int li = s_li0; li < nact; ++iter) {
     const int entry = s_tile;  // written by thread 0 before the previous end-of-tile barrier
     const int tix = entry & 0xffff, tiy = (entry >> 16) & 0x1fff;
     const int tile = tiy * A.ntx + tix;
@@ -367,11 +410,16 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
     int nli = nact, next_entry = 0;
     if (threadIdx.x == 0) {
         nli = static_cast<int>(gridDim.x) + atomicAdd(A.work, 1);
-        if (nli < nact) next_entry = A.tiles[nli];
+        if (!PEER && nli < nact) next_entry = A.tiles[nli];
         s_nli[iter & 1u] = nli;
     }
-    // next tile's boxes into S/G (call only once they are dead)
+    // next tile's boxes into S/G (call only once they are dead).  PEER: the claimed entry is
+    // resolved here (a halo wait blocks thread 0 only, after the Phase-2 barrier)
     auto issue_next = [&]() {
+        if (PEER && threadIdx.x == 0) {
+            nli = resolve(nli, next_entry);
+            s_nli[iter & 1u] = nli;  // read by every thread after the end-of-tile barrier
+        }
         if (threadIdx.x == 0 && nli < nact) {
             const int e = next_entry;
             s_tile = e;
@@ -739,7 +787,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
 __device__ __forceinline__ void tiles_body(const TileArgs& a, int block) {
     const int ntiles = a.ntx * a.nty;
     const int t = block * blockDim.x + threadIdx.x;
-    bool active = false, safe = false, cond = false;
+    bool active = false, safe = false, cond = false, back = false;
     if (t < ntiles) {
         const int tx = t % a.ntx, ty = t / a.ntx;
         const bool ring = tx == 0 || tx == a.ntx - 1 || ty == 0 || ty == a.nty - 1;  // owns boundary faces
@@ -770,9 +818,10 @@ __device__ __forceinline__ void tiles_body(const TileArgs& a, int block) {
         }
         if (skip && halo_reach) {  // the halo rows decide: listed, conditional when peer-joined
             skip = false;
-            cond = a.cond_halo != 0;
+            cond = a.cond_halo != 0 && a.ntx <= kMaxTileCols;  // PeerBox::halo_nz covers kMaxTileCols
         }
         active = !skip;
+        back = active && halo_reach && a.cond_halo != 0;  // peer-joined: after the other tiles
         if (active && a.safe_ok && !(ghost_box && a.ring_ineligible) && !inflow_box && !(reach_s && a.south_ineligible) &&
             !(reach_n && a.north_ineligible)) {
             // safe: no value the box reads (this tile and the facing parts of its 8
@@ -801,22 +850,24 @@ __device__ __forceinline__ void tiles_body(const TileArgs& a, int block) {
         *a.ntiles_reset = 0;
         a.ntiles_reset[4] = 0;  // the other stage's safe-tile count (diagnostics)
         *a.work = 0;            // this stage's dynamic tile scheduler (its previous launch is done)
+        if (a.nback_reset) *a.nback_reset = 0;
     }
-    // conditional tiles go to their own list: peer_wait_kernel appends the ones whose halo
-    // columns are not dry once the neighbours' rows have arrived (tp_peer.cu)
-    const unsigned m = __ballot_sync(0xffffffffu, active && !cond);
+    // peer-joined slabs: tiles whose box reads halo rows go to the back of the list (the stage
+    // kernel claims them last and waits for the neighbours' rows first); the conditional ones
+    // carry kTileCond (dropped there when the pushed rows are dry in their columns)
+    const unsigned m = __ballot_sync(0xffffffffu, active && !back);
     const unsigned ms = __ballot_sync(0xffffffffu, active && safe);
-    const unsigned mc = __ballot_sync(0xffffffffu, cond);
+    const unsigned mb = __ballot_sync(0xffffffffu, back);
     const int lane = threadIdx.x & 31;
-    int base = 0, cbase = 0;
+    int base = 0, bbase = 0;
     if (lane == 0 && m) base = atomicAdd(a.ntiles_active, __popc(m));
     if (lane == 0 && ms) atomicAdd(a.ntiles_active + 4, __popc(ms));
-    if (lane == 0 && mc) cbase = atomicAdd(a.ncond, __popc(mc));
+    if (lane == 0 && mb) bbase = atomicAdd(a.nback, __popc(mb));
     base = __shfl_sync(0xffffffffu, base, 0);
-    cbase = __shfl_sync(0xffffffffu, cbase, 0);
+    bbase = __shfl_sync(0xffffffffu, bbase, 0);
     const int entry = ((t / a.ntx) << 16) | (t % a.ntx);
-    if (active && !cond) a.tiles[base + __popc(m & ((1u << lane) - 1u))] = entry | (safe ? kTileSafe : 0);
-    if (cond) a.cond_tiles[cbase + __popc(mc & ((1u << lane) - 1u))] = entry;
+    if (active && !back) a.tiles[base + __popc(m & ((1u << lane) - 1u))] = entry | (safe ? kTileSafe : 0);
+    if (back) a.tiles[ntiles - 1 - (bbase + __popc(mb & ((1u << lane) - 1u)))] = entry | (cond ? kTileCond : 0);
 }
 
 __global__ void __launch_bounds__(NT) tiles_kernel(TileArgs a) {
@@ -1119,11 +1170,13 @@ __global__ void __launch_bounds__(NT) regularize_kernel(GridDesc g, Phys P, doub
 size_t stage_smem_bytes() { return sizeof(double) * SM_END; }
 
 static int g_num_sms = 148;
-template <bool FD, bool CORR>
+template <bool FD, bool CORR, bool PEER>
 static cudaError_t launch_stage_t(const StageArgs& a, cudaStream_t st) {
     const int ntiles = a.ntx * a.nty;  // upper bound of the active list
-    dim3 grid(ntiles < 2 * g_num_sms ? ntiles : 2 * g_num_sms);
-    stage_kernel<FD, CORR><<<grid, NT, stage_smem_bytes(), st>>>(a);
+    int ctas = 2 * g_num_sms;
+    if (a.max_ctas > 0 && a.max_ctas < ctas) ctas = a.max_ctas;
+    dim3 grid(ntiles < ctas ? ntiles : ctas);
+    stage_kernel<FD, CORR, PEER><<<grid, NT, stage_smem_bytes(), st>>>(a);
     return cudaGetLastError();
 }
 
@@ -1144,9 +1197,13 @@ cudaError_t launch_tiles(const TileArgs& a, cudaStream_t st) {
     return cudaGetLastError();
 }
 
-cudaError_t launch_stage(const StageArgs& a, bool fastdiv, bool corr, cudaStream_t st) {
-    if (fastdiv) return corr ? launch_stage_t<true, true>(a, st) : launch_stage_t<true, false>(a, st);
-    return corr ? launch_stage_t<false, true>(a, st) : launch_stage_t<false, false>(a, st);
+cudaError_t launch_stage(const StageArgs& a, bool fastdiv, bool corr, bool peer, cudaStream_t st) {
+    if (peer) {
+        if (fastdiv) return corr ? launch_stage_t<true, true, true>(a, st) : launch_stage_t<true, false, true>(a, st);
+        return corr ? launch_stage_t<false, true, true>(a, st) : launch_stage_t<false, false, true>(a, st);
+    }
+    if (fastdiv) return corr ? launch_stage_t<true, true, false>(a, st) : launch_stage_t<true, false, false>(a, st);
+    return corr ? launch_stage_t<false, true, false>(a, st) : launch_stage_t<false, false, false>(a, st);
 }
 
 cudaError_t launch_bc(const BcArgs& a, cudaStream_t st) {
@@ -1315,10 +1372,17 @@ cudaError_t init_kernels() {
     int dev = 0;
     if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
     if ((e = cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
-    if ((e = cudaFuncSetAttribute(stage_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) != cudaSuccess) return e;
-    if ((e = cudaFuncSetAttribute(stage_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) != cudaSuccess) return e;
-    if ((e = cudaFuncSetAttribute(stage_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) != cudaSuccess) return e;
-    if ((e = cudaFuncSetAttribute(stage_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) != cudaSuccess) return e;
+    const void* stages[] = {
+        reinterpret_cast<const void*>(&stage_kernel<false, false, false>),
+        reinterpret_cast<const void*>(&stage_kernel<false, true, false>),
+        reinterpret_cast<const void*>(&stage_kernel<true, false, false>),
+        reinterpret_cast<const void*>(&stage_kernel<true, true, false>),
+        reinterpret_cast<const void*>(&stage_kernel<false, false, true>),
+        reinterpret_cast<const void*>(&stage_kernel<false, true, true>),
+        reinterpret_cast<const void*>(&stage_kernel<true, false, true>),
+        reinterpret_cast<const void*>(&stage_kernel<true, true, true>)};
+    for (const void* f : stages)
+        if ((e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) != cudaSuccess) return e;
     // load every kernel now (CUDA loads modules lazily per kernel on first launch: tens of
     // ms that would otherwise land inside the first timed call that happens to use one)
     cudaFuncAttributes fa;

@@ -10,8 +10,9 @@
 //     after apply_boundaries each slab stores its 2 edge interior rows of all 6 fields,
 //     at full padded width (W/E ghosts included, which keeps the reference's corner
 //     semantics), straight into the neighbour's halo rows, then releases a sequence number
-//     into the neighbour's mailbox (peer_halo_push_kernel); the neighbour's
-//     peer_wait_kernel acquires it before its stage kernel reads the box.
+//     into the neighbour's mailbox (peer_halo_push_kernel); the neighbour's stage kernel
+//     (stage_kernel<..., PEER>) acquires it before the first tile whose box reads those rows
+//     (such tiles are listed last, so the transfer overlaps the interior tiles).
 // Sequence numbers derive from the step counter, which every rank advances identically
 // (dt is identical), so the graph of a step is the same on every rank.  Stores are
 // made visible with __threadfence_system() + st.release.sys; waits use ld.acquire.sys.
@@ -19,48 +20,10 @@
 // sets the context's error key.
 #include <cuda_runtime.h>
 
+#include "tp_sync.cuh"
 #include "tp_types.h"
 
 namespace tpb {
-
-// Real exchanges take microseconds; the timeout only turns a lost rank into an error
-// instead of a hang (ranks that share one GPU by time slicing, as in the functional tests,
-// can see long hand-offs).
-constexpr unsigned long long kPeerTimeoutKey = (3ull << 62);  // error class 3: peer timeout
-
-__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
-    unsigned long long v;
-    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
-    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long gtime() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-}
-// spin until *p >= seq; false on timeout
-__device__ __forceinline__ bool wait_seq(const unsigned long long* p, unsigned long long seq,
-                                         unsigned long long timeout_ns) {
-    if (ld_acquire_sys(p) >= seq) return true;
-    const unsigned long long t0 = gtime();
-    for (;;) {
-        __nanosleep(200);
-        if (ld_acquire_sys(p) >= seq) return true;
-        if (gtime() - t0 > timeout_ns) return false;
-    }
-}
-
-// Sequence numbers of one step (steps = DevScalars::steps before the step's post).
-// peer_base is advanced by the host after every tp_steps call by 4 * (graph steps launched),
-// identically on every rank, so sequence numbers only grow (a step's numbers are at most
-// base + 4 * (launched - 1) + 3 < the next call's first, base + 4 * launched + 1).
-__device__ __forceinline__ unsigned long long seq_of(const DevScalars* sc, int phase) {
-    return sc->peer_base + 4ull * static_cast<unsigned long long>(sc->steps) +
-           static_cast<unsigned long long>(phase) + 1ull;
-}
 
 // lambda + stop all-reduce of one step (one CTA of kMaxRanks threads).  Runs whatever
 // the stop flag says, so every rank executes the same exchanges.
@@ -132,7 +95,7 @@ __global__ void peer_halo_push_kernel(PeerLink L, GridDesc g, const double* __re
             s[f * g.fs + static_cast<long long>(src_row + dr) * g.pitch + i];
     }
     // per tile column of the receiver (same columns): does any pushed value inside the box
-    // columns X0-2 .. X0+TX+1 have a bit other than +0.0 (its conditional tiles, peer_wait_kernel)
+    // columns X0-2 .. X0+TX+1 have a bit other than +0.0 (its conditional tiles, stage_kernel<PEER>)
     const int ntx = (g.nx - 6 + TX - 1) / TX;
     unsigned int* nz = L.nbr_box[side]->halo_nz[buf][side == 0 ? 1 : 0];
     for (int tx = blockIdx.x * blockDim.x + threadIdx.x; tx < ntx && tx < kMaxTileCols;
@@ -159,54 +122,13 @@ __global__ void peer_halo_push_kernel(PeerLink L, GridDesc g, const double* __re
     }
 }
 
-// Wait for the halo rows of buffer `buf` from both neighbours, then filter this stage's
-// conditional tiles (tiles_kernel: bitwise no-ops except that their box reads halo rows):
-// a tile is appended to the stage's active list only if a neighbour's pushed rows hold a
-// bit other than +0.0 within its box columns (halo_nz); a skipped ring tile zeroes its
-// tally slot.  The conditional list is reset for the next stage in every case.
-__global__ void peer_wait_kernel(PeerLink L, DevScalars* sc, int buf, CondArgs ca) {
-    const bool live = !*(volatile int*)&sc->done;
-    const int side = threadIdx.x;
-    if (live && side < 2 && L.nbr_state[buf][side]) {
-        if (!wait_seq(&L.my_box->halo_seq[buf][side], seq_of(sc, 1 + buf), L.timeout_ns)) {
-            atomicMin(&sc->err_key, kPeerTimeoutKey);
-            sc->done = 1;
-        }
-    }
-    __syncwarp();  // one warp: nothing else of the CTA sits at a barrier while lanes 0/1 spin
-    const int n = *ca.ncond;
-    for (int i = threadIdx.x; live && i < n; i += blockDim.x) {
-        const int e = ca.cond_tiles[i];
-        const int tx = e & 0xffff, ty = (e >> 16) & 0x1fff;
-        const volatile unsigned int* nz_s = L.my_box->halo_nz[buf][0];  // rows from the south neighbour
-        const volatile unsigned int* nz_n = L.my_box->halo_nz[buf][1];
-        bool keep = false;
-        if (ty == 0) keep |= !L.nbr_state[buf][0] || nz_s[tx] != 0u;
-        if ((ty + 1) * TY + 1 >= ca.nyi) keep |= !L.nbr_state[buf][1] || nz_n[tx] != 0u;
-        if (keep) {
-            ca.tiles[atomicAdd(ca.ntiles_active, 1)] = e;
-        } else {
-            if (tx == 0 || tx == ca.ntx - 1 || ty == 0 || ty == ca.nty - 1) {
-                double* t4 = ca.tally + 4ll * (static_cast<long long>(ty) * ca.ntx + tx);
-                t4[0] = t4[1] = t4[2] = t4[3] = 0.0;
-            }
-            atomicAdd(&sc->cond_skips, 1ull);
-        }
-    }
-    __syncwarp();
-    if (threadIdx.x == 0) *ca.ncond = 0;
-}
-
 cudaError_t launch_peer_lambda(const PeerLink& L, DevScalars* sc, cudaStream_t st) {
     peer_lambda_kernel<<<1, kMaxRanks, 0, st>>>(L, sc);
     return cudaGetLastError();
 }
 cudaError_t launch_peer_halo(const PeerLink& L, const GridDesc& g, const double* s, int buf, DevScalars* sc,
-                             const CondArgs& ca, cudaStream_t st) {
+                             cudaStream_t st) {
     peer_halo_push_kernel<<<dim3(16, 2), 256, 0, st>>>(L, g, s, buf, sc);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-    peer_wait_kernel<<<1, 32, 0, st>>>(L, sc, buf, ca);
     return cudaGetLastError();
 }
 

@@ -86,7 +86,7 @@ struct DevScalars {
     double audit[10];             // solid {initial, final, injected, outflow, clipped}, fluid {...}
     double* dts;                  // optional per-step dt record (device)
     unsigned long long peer_base; // sequence base of the slab exchange (tp_peer.cu)
-    unsigned long long cond_skips;  // conditional tiles left off the list by peer_wait_kernel (cumulative)
+    unsigned long long cond_skips;  // conditional tiles dropped by stage_kernel<PEER> (cumulative)
     ClipList* clip;               // regularize's clipped-mass events (see ClipList)
 };
 
@@ -138,6 +138,19 @@ struct StageArgs {
     unsigned short* flag_out;        // per-tile TileFlag bits of `out` (nonzero bits per region)
     int* nact_stat;                  // [2] list length of the last predictor / corrector launch
     int* work;                       // dynamic tile scheduler counter of this stage (zeroed by tiles_kernel)
+    int max_ctas;                    // grid cap (peer groups sharing one device leave SMs to the others)
+    // Peer-joined slabs (stage_kernel<..., PEER = true>, tp_peer.cu): the listed tiles whose box
+    // reads halo rows, and the conditional ones (kTileCond: bitwise no-ops unless the pushed rows
+    // are nonzero in their columns), sit at the BACK of `tiles` (tiles[ntx*nty-1-k], k < *nback).
+    // They are claimed after every other tile; the claiming thread waits for the neighbours'
+    // halo rows of this stage first (halo_seq), so the NVLink transfer overlaps interior tiles.
+    const int* nback;
+    const unsigned long long* halo_seq[2];  // this slab's mailbox slots for the stage's buffer [side 0 = south]
+    const unsigned int* halo_nz[2];         // [tile column] the pushed rows hold a bit other than +0.0
+    int has_nbr[2];
+    int nyi;                                // interior rows of this slab
+    int peer_phase;                         // 1 + buffer: the stage's sequence-number phase (tp_peer.cu)
+    unsigned long long timeout_ns;
 };
 
 // Per-tile output flags: which regions of the tile's interior hold a value with a nonzero
@@ -152,10 +165,12 @@ enum TileFlag : unsigned {
 // list-entry bit: every state value the tile's box reads is +-0 or in the safe window
 // (entries: tile column in bits 0-15, tile row in bits 16-28)
 constexpr int kTileSafe = 1 << 30;
+// list-entry bit (peer-joined slabs): a conditional tile (see StageArgs::nback)
+constexpr int kTileCond = 1 << 29;
 // A tile of a peer-joined slab that is a bitwise no-op except that its box reads halo rows
-// goes to TileArgs::cond_tiles; peer_wait_kernel lists it only if the neighbour's pushed
+// is listed with kTileCond; stage_kernel<PEER> processes it only if the neighbour's pushed
 // rows hold a bit other than +0.0 in its box columns (PeerBox::halo_nz, tp_peer.cu).
-constexpr int kMaxTileCols = 2048;  // halo_nz entries per side (ncols <= 32768)
+constexpr int kMaxTileCols = 2048;  // halo_nz entries per side (wider slabs list such tiles unconditionally)
 
 // Dry-tile classification before a stage.  flag_in: per-tile flags of the stage's input
 // buffer (the radius-2 box reads interior cells of the tile and the facing bands/corners
@@ -180,9 +195,10 @@ struct TileArgs {
     const unsigned char* inflow_tiles;  // per tile: its box reads a Mode-II inflow ghost (never skip, never safe); may be null
     int south_ineligible, north_ineligible;  // slab edges next to halo rows: never skip
     int safe_ok;          // FASTDIV on, geometry and constants inside the safe-window bounds (tp_capi.cpp)
-    int cond_halo;        // peer-joined slab: halo-reaching tiles that are otherwise no-ops go to cond_tiles
-    int* cond_tiles;      // their list (consumed and reset by peer_wait_kernel)
-    int* ncond;
+    int cond_halo;        // peer-joined slab: tiles whose box reads halo rows go to the back of `tiles`
+                          // (StageArgs::nback), flagged kTileCond when otherwise a no-op
+    int* nback;           // this stage's back-region count (zeroed by the other stage's tiles_kernel)
+    int* nback_reset;     // the other stage's
     int loop;
     DevScalars* sc;
 };
@@ -237,15 +253,6 @@ struct PeerBox {
 };
 // Where this slab's neighbours live (pointers valid in this process: own allocations,
 // allocations of contexts in this process, or CUDA-IPC mappings of other processes').
-// peer_wait_kernel's filter of the conditional tiles of one stage
-struct CondArgs {
-    int* tiles;           // the stage's active-tile list (TileArgs::tiles)
-    int* ntiles_active;
-    const int* cond_tiles;
-    int* ncond;           // reset to 0 after the filter
-    double* tally;        // the stage's ring tally (skipped ring tiles write zeros)
-    int ntx, nty, nyi;
-};
 struct PeerLink {
     double* nbr_state[2][2];     // [buf A/B][side 0 = rank-1 (south), 1 = rank+1 (north)]; null = none
     long long nbr_fs[2];
