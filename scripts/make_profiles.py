@@ -8,10 +8,20 @@ def raw(rep):
     return rows[0], rows[1], rows[2:]
 lines = [f"# ncu summary, {tag}\n"]
 summary = {}
-for cfg in ("c2", "wet"):
+GRID = {"c2": 2048, "wet": 2048, "c5": 8192}
+for cfg in ("c2", "wet", "c5"):
     rep = f"gpurun_out/prof_{tag}_{cfg}.ncu-rep"
     if not os.path.exists(rep):
         continue
+    n = GRID[cfg]
+    # processed-tile fraction of the captured run (bench.py's JSON line in the ncu log)
+    frac = None
+    try:
+        for ln in open(f"gpurun_out/prof_{tag}_{cfg}.log"):
+            if ln.startswith("{"):
+                frac = json.loads(ln)["roofline"]["processed_tile_frac"]
+    except Exception:
+        pass
     hdr, units, data = raw(rep)
     g = lambda r, k: r[hdr.index(k)] if k in hdr else ""
     keys = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
@@ -20,7 +30,8 @@ for cfg in ("c2", "wet"):
             "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
             "launch__occupancy_limit_registers", "launch__occupancy_limit_shared_mem", "smsp__inst_executed.sum",
             "launch__grid_size", "launch__block_size"]
-    lines.append(f"\n## {cfg} 2048x2048 (bench.py --config {cfg}), `ncu --set full --clock-control none`\n")
+    lines.append(f"\n## {cfg} {n}x{n} (bench.py --config {'c2' if cfg == 'c5' else cfg} --ncols {n} --nrows {n}), "
+                 f"`ncu --set full --clock-control none`\n")
     lines.append("| metric | unit | " + " | ".join(g(r, "Kernel Name")[:40] for r in data) + " |")
     lines.append("|---|---|" + "---|" * len(data))
     for k in keys:
@@ -35,14 +46,19 @@ for cfg in ("c2", "wet"):
         return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[u]
     traffic = sum(tobytes(r, "dram__bytes_read.sum") + tobytes(r, "dram__bytes_write.sum") for r in data)
     pct = lambda k: [round(float(g(r, k)), 2) for r in data] if k in hdr else None  # noqa: E731
-    summary[cfg] = {"config": cfg, "grid": [2048, 2048], "dram_bytes_per_step": traffic,
-                    "alg_bytes_per_step": 464 * 2048 * 2048,
+    alg = 464 * n * n
+    alg_proc = (208 * frac[0] + 256 * frac[1]) * n * n if frac else None
+    summary[cfg] = {"config": "c2" if cfg == "c5" else cfg, "grid": [n, n], "dram_bytes_per_step": traffic,
+                    "alg_bytes_per_step": alg, "processed_tile_frac": frac,
+                    "alg_bytes_processed_tiles_per_step": alg_proc,
                     "kernels": [g(r, "Kernel Name") for r in data],
                     "fp64_pipe_active_pct": pct("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
                     "issue_active_pct": pct("smsp__issue_active.avg.pct_of_peak_sustained_active"),
                     "dram_throughput_pct": pct("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed")}
-    lines.append(f"\nDRAM traffic per step (pred+corr): {traffic/1e6:.1f} MB; algorithmic 464 B x 2048^2 = "
-                 f"{464*2048*2048/1e6:.1f} MB (ratio {traffic/(464*2048*2048):.3f}).\n")
+    lines.append(f"\nDRAM traffic per step (pred+corr): {traffic/1e6:.1f} MB; algorithmic 464 B x {n}^2 = "
+                 f"{alg/1e6:.1f} MB (ratio {traffic/alg:.3f})" +
+                 (f"; algorithmic bytes of the processed tiles ({frac[0]:.3f}/{frac[1]:.3f} of the tiles) = "
+                  f"{alg_proc/1e6:.1f} MB (ratio {traffic/alg_proc:.3f})" if alg_proc else "") + ".\n")
 # launch list
 lc = f"gpurun_out/launches_{tag}.csv"
 if os.path.exists(lc):
@@ -62,6 +78,6 @@ if os.path.exists(lc):
         lines.append(f"| {k} | {len(v)} | {sum(v)/len(v)/1e3:.1f} | {100*sum(v)/tot:.1f}% |")
 open(f"{out_dir}/{tag}_ncu.md", "w").write("\n".join(lines) + "\n")
 if "c2" in summary:
-    d = summary["c2"]; d["wet"] = summary.get("wet"); d["source"] = f"profiles/{tag}_ncu.md"
+    d = summary["c2"]; d["wet"] = summary.get("wet"); d["c5"] = summary.get("c5"); d["source"] = f"profiles/{tag}_ncu.md"
     json.dump(d, open(f"{out_dir}/ncu_stage_summary.json", "w"), indent=1)
 print("\n".join(lines))
