@@ -113,11 +113,13 @@ class ClockSampler:
                 "reasons": names, "samples": len(self.samples)}
 
 
-def cpu_reference(config, ncols, nrows, steps, lanes, timeout=600, stack=1):
+def cpu_reference(config, ncols, nrows, steps, lanes, timeout=600, stack=1, check_serial=1):
     """The reference (oracle/_ref, else the C port) timed on this host, in a child process.
-    stack > 1: the weak-scaling grid of `bench.py --gpus stack` (row-stacked copies)."""
+    stack > 1: the weak-scaling grid of `bench.py --gpus stack` (row-stacked copies).
+    check_serial: steps of a serial run the parallel state must match bitwise (App. B1)."""
     cmd = [sys.executable, "-m", "oracle.cpu_bench", "--config", config, "--ncols", str(ncols),
-           "--nrows", str(nrows), "--steps", str(steps), "--lanes", str(lanes), "--stack", str(stack)]
+           "--nrows", str(nrows), "--steps", str(steps), "--lanes", str(lanes), "--stack", str(stack),
+           "--check-serial", str(check_serial)]
     try:
         out = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=timeout)
         line = [l for l in out.stdout.splitlines() if l.startswith("{")]
@@ -131,7 +133,7 @@ def cpu_reference(config, ncols, nrows, steps, lanes, timeout=600, stack=1):
     except Exception as e:  # crash of the racy pool (App. B1) -> serial
         err = str(e)
     if lanes > 1:
-        r = cpu_reference(config, ncols, nrows, max(1, steps // 4), 1, timeout, stack)
+        r = cpu_reference(config, ncols, nrows, max(1, steps // 4), 1, timeout, stack, 0)
         r["note"] = f"DataParallel({lanes}) failed ({err.strip()[:120]}); serial backend"
         return r
     raise RuntimeError("CPU reference failed: " + err)
@@ -464,7 +466,10 @@ def run_reference(args):
     if world == 1 and not args.no_extra:
         # the north-star grid beside it (our arm's c5_8192 object): a 2-step sample
         try:
-            c5 = cpu_reference("c2", args.c5_size, args.c5_size, args.c5_ref_steps, lanes, timeout=900)
+            # (the parallel-vs-serial bitwise check runs on the 2048^2 line; a serial 8192^2
+            # step alone takes about a minute)
+            c5 = cpu_reference("c2", args.c5_size, args.c5_size, args.c5_ref_steps, lanes, timeout=900,
+                               check_serial=0)
             out["c5_8192"] = {"value": round(c5["value"] / 1e9, 6), "unit": "GCUPS",
                               "steps": c5["steps"], "ms_per_step": round(1e3 * c5["seconds"] / c5["steps"], 3),
                               "config": workload_config(scenario_for("c2", args.c5_size, args.c5_size)),
