@@ -64,7 +64,9 @@ int tp_geometry(const tp_dem* dem, double L, double* out14);
 
 /* padded dims of this context and the scaled spacings */
 int tp_dims(const tp_ctx* c, int* nx, int* ny, double* dxi, double* deta);
-/* options: "fastdiv" (0/1, default 1), "graph_steps" (steps per CUDA graph, default 16) */
+/* options: "fastdiv" (0/1, default 1), "skip_dry" (0/1, default 1), "graph_steps" (steps per
+ * CUDA graph, default 16), "wide_tiles" (replay the graphs with one 512-thread stage CTA per SM
+ * while the last tile lists held <= this many tiles; default -1 = the SM count, 0 = never) */
 int tp_set_option(tp_ctx* c, const char* key, long value);
 
 /* Simulator::set_initial_thickness / set_initial_velocity / set_hydrograph

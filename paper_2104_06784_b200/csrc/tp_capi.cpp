@@ -26,7 +26,7 @@
 
 namespace tpb {
 size_t stage_smem_bytes();
-cudaError_t launch_stage(const StageArgs& a, bool fastdiv, bool corr, bool peer, cudaStream_t st);
+cudaError_t launch_stage(const StageArgs& a, bool fastdiv, bool corr, bool peer, bool wide, cudaStream_t st);
 cudaError_t launch_bc(const BcArgs& a, cudaStream_t st);
 cudaError_t launch_ghost_copy(const GridDesc& g, const double* src, double* dst, cudaStream_t st);
 cudaError_t launch_lambda(const GridDesc& g, const Phys& P, const double* s, const double* geo,
@@ -174,7 +174,11 @@ struct tp_ctx {
     bool hydro_set = false;
     int adv_only = 0;
     cudaGraphExec_t graphK = nullptr, graph1 = nullptr;
+    cudaGraphExec_t graphKw = nullptr, graph1w = nullptr;  // the same with wide stage CTAs (short lists)
     cudaGraphExec_t graphT = nullptr;   // one step with timing events around the stage kernels
+    int num_sms = 148;
+    int wide_tiles = -1;                // use the wide graphs while the last lists had <= this many tiles (-1: #SMs)
+    bool wide = false;                  // the graph family of the next replay
     cudaEvent_t evT[4] = {nullptr, nullptr, nullptr, nullptr};
     int graphK_steps = 0;
     long launches = 0;
@@ -261,10 +265,10 @@ void build_phys(tp_ctx* c) {
 }
 
 void drop_graphs(tp_ctx* c) {
-    if (c->graphK) cudaGraphExecDestroy(c->graphK);
-    if (c->graph1) cudaGraphExecDestroy(c->graph1);
-    if (c->graphT) cudaGraphExecDestroy(c->graphT);
-    c->graphK = c->graph1 = c->graphT = nullptr;
+    for (cudaGraphExec_t* gp : {&c->graphK, &c->graph1, &c->graphKw, &c->graph1w, &c->graphT}) {
+        if (*gp) cudaGraphExecDestroy(*gp);
+        *gp = nullptr;
+    }
 }
 
 tpb::StageArgs stage_args(tp_ctx* c, bool corr, int loop) {
@@ -352,7 +356,7 @@ cudaError_t launch_stage_sel(tp_ctx* c, const tpb::StageArgs& a, bool fastdiv, b
     cudaError_t e = tpb::launch_tiles(t, st);
     if (e != cudaSuccess) return e;
     if (ev0 && (e = cudaEventRecord(ev0, st)) != cudaSuccess) return e;
-    e = tpb::launch_stage(a, fastdiv, corr, false, st);
+    e = tpb::launch_stage(a, fastdiv, corr, false, false, st);
     if (e == cudaSuccess && ev1) e = cudaEventRecord(ev1, st);
     return e;
 }
@@ -393,7 +397,7 @@ void launch_post(tp_ctx* c, int loop) {
 // one whole step of the device loop: 5 kernels
 //   pre(bc(u,t) + predictor list + compute_dt) -> predictor -> pre(bc(u*,t+dt) + corrector list)
 //   -> corrector -> post(t += dt, audit, stop flag)
-void enqueue_loop_step(tp_ctx* c, cudaEvent_t* ev = nullptr) {
+void enqueue_loop_step(tp_ctx* c, cudaEvent_t* ev = nullptr, bool wide = false) {
     // slabs connected by tp_peer_connect*: the lambda + stop all-reduce before compute_dt
     if (c->peered) ck(tpb::launch_peer_lambda(c->link, c->dSc, c->stream), "peer lambda");
     for (int corr = 0; corr < 2; ++corr) {
@@ -418,19 +422,19 @@ void enqueue_loop_step(tp_ctx* c, cudaEvent_t* ev = nullptr) {
         if (c->peered)
             ck(tpb::launch_peer_halo(c->link, c->g, corr ? c->dB : c->dA, corr, c->dSc, c->stream), "peer halo");
         if (ev) ck(cudaEventRecordWithFlags(ev[2 * corr], c->stream, cudaEventRecordExternal), "event");
-        ck(tpb::launch_stage(sa, c->fastdiv, corr != 0, c->peered, c->stream), corr ? "corrector" : "predictor");
+        ck(tpb::launch_stage(sa, c->fastdiv, corr != 0, c->peered, wide, c->stream), corr ? "corrector" : "predictor");
         if (ev) ck(cudaEventRecordWithFlags(ev[2 * corr + 1], c->stream, cudaEventRecordExternal), "event");
     }
     launch_post(c, 1);
 }
 
-cudaGraphExec_t capture_steps(tp_ctx* c, int k, cudaEvent_t* ev = nullptr) {
+cudaGraphExec_t capture_steps(tp_ctx* c, int k, cudaEvent_t* ev = nullptr, bool wide = false) {
     cudaGraph_t graph = nullptr;
     const int saved_stage = c->last_tiles_stage;
     c->last_tiles_stage = 1;  // a replay always follows a corrector (tp_steps resets otherwise)
     ck(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal), "begin capture");
     try {
-        for (int s = 0; s < k; ++s) enqueue_loop_step(c, ev);
+        for (int s = 0; s < k; ++s) enqueue_loop_step(c, ev, wide);
     } catch (...) {
         cudaStreamEndCapture(c->stream, &graph);
         if (graph) cudaGraphDestroy(graph);
@@ -690,6 +694,7 @@ void create_impl(tp_ctx* c, const tp_params* p, const tp_dem* dem, int row0, int
     c->dA = c->rawA + 1;
     c->dB = c->rawB + 1;
     c->dGeo = c->rawGeo + 1;
+    cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device);
     ck(cudaMalloc(&c->dSc, sizeof(DevScalars)), "cudaMalloc scalars");
     ck(cudaMalloc(&c->dClip, sizeof(tpb::ClipList)), "cudaMalloc clip list");
     const size_t tb = sizeof(double) * 4ull * c->ntx * c->nty;
@@ -883,6 +888,10 @@ int tp_set_option(tp_ctx* c, const char* key, long value) {
         } else if (k == "skip_dry") {
             c->skip_dry = value != 0;
             drop_graphs(c);
+        } else if (k == "wide_tiles") {
+            // wide stage CTAs while the last tile lists had <= value tiles (-1: the SM count;
+            // 0: never; a large value: always)
+            c->wide_tiles = static_cast<int>(value);
         } else if (k == "graph_steps") {
             if (value < 1 || value > 4096) throw ConfigErr{"graph_steps must be in [1, 4096]"};
             c->graph_steps = static_cast<int>(value);
@@ -1144,6 +1153,8 @@ void steps_begin(tp_ctx* c, StepsRun& r, double t, double t_next, double t_end, 
         drop_graphs(c);
         c->graphK = capture_steps(c, c->graph_steps);
         c->graph1 = capture_steps(c, 1);
+        c->graphKw = capture_steps(c, c->graph_steps, nullptr, true);
+        c->graph1w = capture_steps(c, 1, nullptr, true);
         c->graphK_steps = c->graph_steps;
     }
     if (c->last_tiles_stage == 0) {  // the graphs start with a predictor list
@@ -1157,14 +1168,24 @@ void steps_begin(tp_ctx* c, StepsRun& r, double t, double t_next, double t_end, 
 void steps_launch(tp_ctx* c, StepsRun& r) {
     const bool big = (r.max_steps - r.h.steps) >= c->graph_steps;
     const int k = big ? c->graph_steps : 1;
-    ck(cudaGraphLaunch(big ? c->graphK : c->graph1, c->stream), "graph launch");
+    ck(cudaGraphLaunch(c->wide ? (big ? c->graphKw : c->graph1w) : (big ? c->graphK : c->graph1), c->stream),
+       "graph launch");
     c->launches += (c->peered ? 8L : 5L) * k;  // peered: + lambda exchange + 2 halo pushes
     r.launched += k;
+}
+
+// the graph family of the next replay: wide stage CTAs (one tile per SM, one face per thread)
+// while the last lists were short enough that every tile had an SM to itself
+void choose_wide(tp_ctx* c, const DevScalars& h) {
+    const int thr = c->wide_tiles >= 0 ? c->wide_tiles : c->num_sms;
+    const int n = h.last_nact[0] > h.last_nact[1] ? h.last_nact[0] : h.last_nact[1];
+    c->wide = n <= thr;
 }
 
 void steps_poll(tp_ctx* c, StepsRun& r) {
     r.h = read_scalars(c);
     r.finished = r.h.done != 0;
+    if (r.h.steps > 0) choose_wide(c, r.h);
 }
 
 // A device error key with the slab's local row replaced by the global row, so keys of

@@ -43,7 +43,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
     const long long tp_c0 = tp_last; const unsigned long long tp_g0 = gtimer();
 #define TPROBE(k) do { const long long _n = clock64(); tp_acc[k] += _n - tp_last; tp_last = _n; } while (0)
 #define TPROBE_FLUSH(corr)                                                          \
-    if ((threadIdx.x & 31) == 0) {                                                  \
+    if ((threadIdx.x & 31) == 0 && iter > 0) { /* warps that processed a tile */    \
         for (int _k = 0; _k < 16; ++_k) atomicAdd(&g_phase_cycles[corr][_k], tp_acc[_k]); \
         atomicAdd(&g_phase_cycles[corr][16], 1ull);                                 \
         atomicAdd(&g_phase_cycles[corr][17], static_cast<unsigned long long>(clock64() - tp_c0)); \
@@ -203,12 +203,53 @@ __device__ __forceinline__ unsigned long long cell_epilogue(double (&un)[6], con
 // fields of the whole box (see stage_kernel).  CHK = false is the safe-tile form
 // (DESIGN.md §3): every numerator is +-0 or in the FASTDIV window by construction, so
 // the window tests and their fix-up branches are compiled out.
-template <bool FD, bool CHK>
+template <bool FD, bool CHK, int NTH>
 __device__ __forceinline__ void stage_phase1(const double* __restrict__ S, const double* __restrict__ G,
                                              double* FX, double* FY, double* V, double* PJ, const Phys& P) {
+    if (NTH == 2 * NT) {
+        // wide CTA (short lists, one tile per SM): threads 0..NT-1 own one xi face each,
+        // threads NT..2NT-1 one eta face each (warp-uniform), the same face mapping as below
+        const int t = threadIdx.x & (NT - 1);
+        const int it = (t + TX * TY) & (NT - 1);
+        if (threadIdx.x < NT) {
+            if (it < NFX) {
+                const int fx = it < TX * TY ? it % TX : TX;
+                const int tyx = it < TX * TY ? it / TX : it - TX * TY;
+                const int kx = (tyx + 2) * W2 + fx + 1;  // xi face between kx and kx+1
+                double Lx[6], Rx[6], ox[6];
+#pragma unroll
+                for (int f = 0; f < 6; ++f) {
+                    const double* row = S + f * BOX + kx - 1;
+                    const double c0 = row[0], c1 = row[1], c2 = row[2], c3 = row[3];
+                    Lx[f] = edge_plus(c0, c1, c2);
+                    Rx[f] = edge_minus(c1, c2, c3);
+                }
+                face_flux<FD, true, CHK>(Lx, Rx, G[G_JB * BOX + kx], G[G_JB * BOX + kx + 1], G[G_NZ * BOX + kx],
+                                         G[G_NZ * BOX + kx + 1], G[G_A11 * BOX + kx], G[G_A11 * BOX + kx + 1],
+                                         G[G_A12 * BOX + kx], G[G_A12 * BOX + kx + 1], G[G_RJBFX * BOX + kx], P, ox);
+#pragma unroll
+                for (int f = 0; f < 6; ++f) FX[f * NFX + tyx * (TX + 1) + fx] = ox[f];
+            }
+        } else if (it < NFY) {
+            const int txy = it % TX, fy = it / TX;
+            const int ky = (fy + 1) * W2 + txy + 2;  // eta face between ky and ky+W2
+            double Ly[6], Ry[6], oy[6];
+#pragma unroll
+            for (int f = 0; f < 6; ++f) {
+                const double* col = S + f * BOX + ky - W2;
+                const double d0 = col[0], d1 = col[W2], d2 = col[2 * W2], d3 = col[3 * W2];
+                Ly[f] = edge_plus(d0, d1, d2);
+                Ry[f] = edge_minus(d1, d2, d3);
+            }
+            face_flux<FD, false, CHK>(Ly, Ry, G[G_JB * BOX + ky], G[G_JB * BOX + ky + W2], G[G_NZ * BOX + ky],
+                                      G[G_NZ * BOX + ky + W2], G[G_A22 * BOX + ky], G[G_A22 * BOX + ky + W2],
+                                      G[G_A21 * BOX + ky], G[G_A21 * BOX + ky + W2], G[G_RJBFY * BOX + ky], P, oy);
+#pragma unroll
+            for (int f = 0; f < 6; ++f) FY[f * NFY + it] = oy[f];
+        }
+    } else {
     // faces: thread t owns xi face t and eta face t, written as one straight-line
     // block so the two independent dependency chains interleave (ILP)
-    {
         // face index: the 15 last xi faces of the rows (a conflicted column walk) on warp 0,
         // which carries no second cell pass (that is warps 4-7)
         const int it = (threadIdx.x + TX * TY) & (NT - 1);
@@ -250,8 +291,8 @@ __device__ __forceinline__ void stage_phase1(const double* __restrict__ S, const
         }
     }
     // box cell k = (thread ^ 128) + pass * NT: the BOX - NT cells of the second pass go to
-    // warps 4-7, as the second bracket pass of Phase 2 goes to warps 0-1
-    for (int k = threadIdx.x ^ 128; k < BOX; k += NT) {
+    // warps 4-7, as the second bracket pass of Phase 2 goes to warps 0-1 (wide CTA: one pass)
+    for (int k = NTH == NT ? (threadIdx.x ^ 128) : static_cast<int>(threadIdx.x); k < BOX; k += NTH) {
         {
             // cell fields (solver.cpp:172-184) on box cell k
             if (P.adv_only) continue;  // velocities/pjb feed sources and brackets only
@@ -288,8 +329,12 @@ __device__ __forceinline__ void stage_phase1(const double* __restrict__ S, const
 // ---------------------------------------------------------------------------
 // The fused stage kernel.
 // ---------------------------------------------------------------------------
-template <bool FD, bool CORR, bool PEER>
-__global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ StageArgs A) {
+// NTH = NT: two CTAs per SM, each thread owns an xi and an eta face (the production shape);
+// NTH = 2 NT ("wide"): one CTA per SM, one face per thread, for short tile lists where every
+// tile has an SM to itself and the step time is one tile's latency (tp_capi.cpp picks the
+// graph per replay from the last list length).
+template <bool FD, bool CORR, bool PEER, int NTH>
+__global__ void __launch_bounds__(NTH, NTH == NT ? 2 : 1) stage_kernel(const __grid_constant__ StageArgs A) {
     extern __shared__ __align__(128) double sm[];
     __shared__ unsigned long long bar;   // state + stencil-geometry boxes
     __shared__ unsigned long long barc;  // per-cell geometry box
@@ -318,7 +363,10 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
     // active-tile list of this stage (tiles_kernel); PEER: plus its back region (StageArgs::nback)
     const int n_main = *A.ntiles_active;
     const int nact = n_main + (PEER ? *A.nback : 0);
-    if (blockIdx.x == 0 && threadIdx.x == 0) A.nact_stat[CORR ? 1 : 0] = nact;  // diagnostics
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        A.nact_stat[CORR ? 1 : 0] = nact;  // diagnostics
+        sc->last_nact[CORR ? 1 : 0] = nact;  // the host's dense / wide graph choice (tp_capi.cpp)
+    }
     const double dt = sc->dt;
     // list entry li: the front of `tiles`, then (PEER) its back region from the end
     auto entry_at = [&](int li) { return (!PEER || li < n_main) ? A.tiles[li] : A.tiles[ntiles - 1 - (li - n_main)]; };
@@ -441,8 +489,8 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
     // left off the list by tiles_kernel, and a listed dry tile computes the same +0.0)
 
     // ---- Phase 1: xi faces, eta faces, cell fields -----------------------------
-    if (FD && (entry & kTileSafe)) stage_phase1<FD, false>(S, G, FX, FY, V, PJ, P);  // safe tile
-    else stage_phase1<FD, true>(S, G, FX, FY, V, PJ, P);
+    if (FD && (entry & kTileSafe)) stage_phase1<FD, false, NTH>(S, G, FX, FY, V, PJ, P);  // safe tile
+    else stage_phase1<FD, true, NTH>(S, G, FX, FY, V, PJ, P);
     TPROBE(4);  // Phase 1 work
     __syncthreads();
     TPROBE(5);  // Phase 1 barrier
@@ -549,7 +597,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
             // one bracket per thread (the 16 threads without a Phase-3 cell included), the
             // NB - NT remaining ones on the first warps: every warp costs sources + 1 bracket
             // pass and only two warps a second pass (a warp's cost is per pass, not per lane)
-            for (int it = threadIdx.x; it < NB; it += NT) {
+            for (int it = threadIdx.x; it < NB; it += NTH) {
                 // interior cells in 16-wide row segments first (conflict-free smem walks), then
                 // rows 1 and TY+2, then columns 1 and TX+2
                 int bx, by;
@@ -777,7 +825,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(const __grid_constant__ St
     }  // tile loop
     TPROBE_FLUSH(CORR ? 1 : 0)
 
-    if (CORR) lam_block_max(lam_local, sc);
+    if (CORR) lam_block_max<NTH>(lam_local, sc);
 }
 
 // ---------------------------------------------------------------------------
@@ -1170,14 +1218,24 @@ __global__ void __launch_bounds__(NT) regularize_kernel(GridDesc g, Phys P, doub
 size_t stage_smem_bytes() { return sizeof(double) * SM_END; }
 
 static int g_num_sms = 148;
-template <bool FD, bool CORR, bool PEER>
+template <bool FD, bool CORR, bool PEER, int NTH>
 static cudaError_t launch_stage_t(const StageArgs& a, cudaStream_t st) {
     const int ntiles = a.ntx * a.nty;  // upper bound of the active list
-    int ctas = 2 * g_num_sms;
-    if (a.max_ctas > 0 && a.max_ctas < ctas) ctas = a.max_ctas;
+    int ctas = (NTH == NT ? 2 : 1) * g_num_sms;
+    if (a.max_ctas > 0 && a.max_ctas < 2 * g_num_sms) ctas = NTH == NT ? a.max_ctas : a.max_ctas / 2;
     dim3 grid(ntiles < ctas ? ntiles : ctas);
-    stage_kernel<FD, CORR, PEER><<<grid, NT, stage_smem_bytes(), st>>>(a);
+    stage_kernel<FD, CORR, PEER, NTH><<<grid, NTH, stage_smem_bytes(), st>>>(a);
     return cudaGetLastError();
+}
+
+template <int NTH>
+static cudaError_t launch_stage_n(const StageArgs& a, bool fastdiv, bool corr, bool peer, cudaStream_t st) {
+    if (peer) {
+        if (fastdiv) return corr ? launch_stage_t<true, true, true, NTH>(a, st) : launch_stage_t<true, false, true, NTH>(a, st);
+        return corr ? launch_stage_t<false, true, true, NTH>(a, st) : launch_stage_t<false, false, true, NTH>(a, st);
+    }
+    if (fastdiv) return corr ? launch_stage_t<true, true, false, NTH>(a, st) : launch_stage_t<true, false, false, NTH>(a, st);
+    return corr ? launch_stage_t<false, true, false, NTH>(a, st) : launch_stage_t<false, false, false, NTH>(a, st);
 }
 
 cudaError_t launch_pre(const PreArgs& a, cudaStream_t st) {
@@ -1197,13 +1255,8 @@ cudaError_t launch_tiles(const TileArgs& a, cudaStream_t st) {
     return cudaGetLastError();
 }
 
-cudaError_t launch_stage(const StageArgs& a, bool fastdiv, bool corr, bool peer, cudaStream_t st) {
-    if (peer) {
-        if (fastdiv) return corr ? launch_stage_t<true, true, true>(a, st) : launch_stage_t<true, false, true>(a, st);
-        return corr ? launch_stage_t<false, true, true>(a, st) : launch_stage_t<false, false, true>(a, st);
-    }
-    if (fastdiv) return corr ? launch_stage_t<true, true, false>(a, st) : launch_stage_t<true, false, false>(a, st);
-    return corr ? launch_stage_t<false, true, false>(a, st) : launch_stage_t<false, false, false>(a, st);
+cudaError_t launch_stage(const StageArgs& a, bool fastdiv, bool corr, bool peer, bool wide, cudaStream_t st) {
+    return wide ? launch_stage_n<2 * NT>(a, fastdiv, corr, peer, st) : launch_stage_n<NT>(a, fastdiv, corr, peer, st);
 }
 
 cudaError_t launch_bc(const BcArgs& a, cudaStream_t st) {
@@ -1372,15 +1425,17 @@ cudaError_t init_kernels() {
     int dev = 0;
     if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
     if ((e = cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
-    const void* stages[] = {
-        reinterpret_cast<const void*>(&stage_kernel<false, false, false>),
-        reinterpret_cast<const void*>(&stage_kernel<false, true, false>),
-        reinterpret_cast<const void*>(&stage_kernel<true, false, false>),
-        reinterpret_cast<const void*>(&stage_kernel<true, true, false>),
-        reinterpret_cast<const void*>(&stage_kernel<false, false, true>),
-        reinterpret_cast<const void*>(&stage_kernel<false, true, true>),
-        reinterpret_cast<const void*>(&stage_kernel<true, false, true>),
-        reinterpret_cast<const void*>(&stage_kernel<true, true, true>)};
+#define TP_STAGE_PTRS(N)                                                   \
+    reinterpret_cast<const void*>(&stage_kernel<false, false, false, N>), \
+        reinterpret_cast<const void*>(&stage_kernel<false, true, false, N>),  \
+        reinterpret_cast<const void*>(&stage_kernel<true, false, false, N>),  \
+        reinterpret_cast<const void*>(&stage_kernel<true, true, false, N>),   \
+        reinterpret_cast<const void*>(&stage_kernel<false, false, true, N>),  \
+        reinterpret_cast<const void*>(&stage_kernel<false, true, true, N>),   \
+        reinterpret_cast<const void*>(&stage_kernel<true, false, true, N>),   \
+        reinterpret_cast<const void*>(&stage_kernel<true, true, true, N>)
+    const void* stages[] = {TP_STAGE_PTRS(NT), TP_STAGE_PTRS(2 * NT)};
+#undef TP_STAGE_PTRS
     for (const void* f : stages)
         if ((e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) != cudaSuccess) return e;
     // load every kernel now (CUDA loads modules lazily per kernel on first launch: tens of

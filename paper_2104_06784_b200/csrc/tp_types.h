@@ -88,6 +88,7 @@ struct DevScalars {
     unsigned long long peer_base; // sequence base of the slab exchange (tp_peer.cu)
     unsigned long long cond_skips;  // conditional tiles dropped by stage_kernel<PEER> (cumulative)
     ClipList* clip;               // regularize's clipped-mass events (see ClipList)
+    int last_nact[2];             // tiles listed for the last predictor / corrector launch
 };
 
 struct GridDesc {

@@ -16,10 +16,15 @@ from tests.util import assert_bitwise, rel_err
 pytestmark = pytest.mark.gpu
 
 
-def _pair(sc, kind, fastdiv=True):
+def _pair(sc, kind, fastdiv=True, wide=None):
+    """wide: None = automatic (wide stage CTAs while the lists are shorter than the SM count,
+    i.e. almost always on these small grids), True / False = forced."""
     from oracle.oracle import OracleSim
     from paper_2104_06784_b200.simulator import Simulator
-    return OracleSim(sc, kind), Simulator.from_scenario(sc, fastdiv=fastdiv)
+    sim = Simulator.from_scenario(sc, fastdiv=fastdiv)
+    if wide is not None:
+        sim.set_option("wide_tiles", 1 << 30 if wide else 0)
+    return OracleSim(sc, kind), sim
 
 
 def test_division_identity(gpu):
@@ -84,11 +89,13 @@ def test_step_api_bitwise_c1(gpu, oracle_kind, fastdiv):
     np.testing.assert_allclose(a_g, a_r, rtol=1e-12, atol=1e-300)
 
 
+@pytest.mark.parametrize("wide", [False, True])
 @pytest.mark.parametrize("fastdiv", [False, True])
-def test_trajectory_c1_device_loop(gpu, oracle_kind, fastdiv):
-    """tp_steps (device-resident loop, CUDA graphs) == the reference run loop, 150 steps."""
+def test_trajectory_c1_device_loop(gpu, oracle_kind, fastdiv, wide):
+    """tp_steps (device-resident loop, CUDA graphs) == the reference run loop, 150 steps,
+    with the production stage CTAs and with the wide (one tile per SM) ones."""
     sc = scenarios.c1_hill(96)
-    ref, sim = _pair(sc, oracle_kind, fastdiv)
+    ref, sim = _pair(sc, oracle_kind, fastdiv, wide)
     tr, dts_r, hr = ref.steps(0.0, 1.0e9, 150, t_end=1.0e9)
     tg, dts_g, hg = sim.steps(0.0, 1.0e9, 150, t_end=1.0e9, record_dts=True)
     assert len(dts_g) == len(dts_r) == 150
@@ -113,10 +120,11 @@ def test_trajectory_output_hits(gpu, oracle_kind):
     assert_bitwise(sim.state(), ref.state(), "state at output times")
 
 
-def test_mode2_channel_inflow(gpu, oracle_kind):
+@pytest.mark.parametrize("wide", [False, True])
+def test_mode2_channel_inflow(gpu, oracle_kind, wide):
     """Mode-II hydrograph inflow (solver.cpp:108-136, hydrograph.hpp:31-45)."""
     sc = scenarios.c3_channel(96, 48, t_end=30.0, dt_out=0.5)
-    ref, sim = _pair(sc, oracle_kind)
+    ref, sim = _pair(sc, oracle_kind, wide=wide)
     tu = sc.config.scaling.t_unit()
     t_r = t_g = 0.0
     for k in range(1, 9):
@@ -208,12 +216,13 @@ def test_negative_thickness_error_matches(gpu, oracle_kind):
     assert str(eg.value) == str(er.value)
 
 
+@pytest.mark.parametrize("wide", [False, True])
 @pytest.mark.parametrize("name", ["c2", "wet", "c4"])
-def test_trajectory_other_terrains(gpu, oracle_kind, name):
+def test_trajectory_other_terrains(gpu, oracle_kind, name, wide):
     """valley (mostly dry: exercises the dry-tile fast path), fully wet valley, seeded terrain."""
     sc = {"c2": lambda: scenarios.c2_valley(160, 144), "wet": lambda: scenarios.wet_valley(128, 112),
           "c4": lambda: scenarios.c4_terrain(120, 90)}[name]()
-    ref, sim = _pair(sc, oracle_kind)
+    ref, sim = _pair(sc, oracle_kind, wide=wide)
     tr, dts_r, _ = ref.steps(0.0, 1.0e9, 60, t_end=1.0e9)
     tg, dts_g, _ = sim.steps(0.0, 1.0e9, 60, t_end=1.0e9, record_dts=True)
     assert_bitwise(dts_g, dts_r, "dt sequence")
@@ -590,7 +599,7 @@ def test_fuzz_scenarios_bitwise(gpu, oracle_kind, seed):
     """Random small scenarios (shape, terrain, release or inflow on random sides, parameters)
     through the run loop's output schedule: every dt and the final state bit-identical."""
     sc = _fuzz_scenario(seed)
-    ref, sim = _pair(sc, oracle_kind)
+    ref, sim = _pair(sc, oracle_kind, wide=None if seed % 2 == 0 else False)  # odd seeds: production CTAs
     tu = sc.config.scaling.t_unit()
     t_end, dt_out = sc.config.t_end / tu, sc.config.dt_out / tu
     t_r = t_g = 0.0

@@ -43,9 +43,11 @@ def test_cuda_slabs_equal_single_device(gpu, oracle_kind, make, parts):
                                   lambda: scenarios.moving_release(70, 52),
                                   lambda: scenarios.four_side_inflow(48, 40),
                                   lambda: scenarios.four_side_inflow(49, 46)])
-def test_peer_slabs_equal_single_device(gpu, oracle_kind, make, parts):
+@pytest.mark.parametrize("wide", [False, True])
+def test_peer_slabs_equal_single_device(gpu, oracle_kind, make, parts, wide):
     """Device-resident exchange (tp_peer.cu): halo rows stored into the neighbours'
-    buffers and lambda reduced in device memory inside the step graphs."""
+    buffers and lambda reduced in device memory inside the step graphs; the in-kernel halo
+    wait of the production and of the wide stage CTAs."""
     import torch
     from oracle.oracle import OracleSim
     sc = make()
@@ -54,6 +56,8 @@ def test_peer_slabs_equal_single_device(gpu, oracle_kind, make, parts):
     ref = OracleSim(sc, oracle_kind)
     t1, d1, _ = ref.steps(0.0, t_next, steps, t_end=1e9)
     slabs = [CudaSlab(sc, r, stream=torch.cuda.Stream()) for r in decompose(sc.nrows, parts)]
+    for s in slabs:
+        s.sim.set_option("wide_tiles", 1 << 30 if wide else 0)
     group = PeerGroup(slabs)
     t2, n2, _ = group.steps(0.0, t_next, steps, t_end=1e9)
     assert n2 == len(d1)
