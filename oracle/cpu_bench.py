@@ -54,12 +54,28 @@ def main() -> None:
     t0 = time.perf_counter()
     sim = orc.OracleSim(sc, kind, lanes=lanes if lanes > 1 else 0)
     setup = time.perf_counter() - t0
+    # the run loop's output schedule (solver.cpp:627-649), as bench.py's RunClock: steps go
+    # toward min(next output, t_end) and stop on exact hits (a dry Mode-II start jumps to the
+    # first output time in one step)
+    tu = sc.config.scaling.t_unit()
+    t_end, dt_out = sc.config.t_end / tu, sc.config.dt_out / tu
+    clock = {"t": 0.0, "next": dt_out}
+
+    def advance(k):
+        done = 0
+        while done < k and clock["t"] < t_end:
+            t_next = min(clock["next"], t_end)
+            clock["t"], d, hit = sim.steps(clock["t"], t_next, k - done, t_end=t_end)
+            done += len(d)
+            if hit and t_next == clock["next"]:
+                clock["next"] += dt_out
+        return done
+
     # one untimed step (first-touch of the buffers), then the timed sample
-    t, _, _ = sim.steps(0.0, 1e9, 1, t_end=1e9)
+    advance(1)
     t1 = time.perf_counter()
-    t, dts, _ = sim.steps(t, 1e9, a.steps, t_end=1e9)
+    n = advance(a.steps)
     dt_wall = time.perf_counter() - t1
-    n = len(dts)
     out = {"kind": kind, "lanes": lanes, "steps": n, "seconds": dt_wall, "setup_seconds": setup,
            "cells": sc.ncols * sc.nrows, "value": sc.ncols * sc.nrows * n / dt_wall,
            "unit": "cell-updates/s", "config": a.config, "grid": [sc.ncols, sc.nrows]}
@@ -68,8 +84,8 @@ def main() -> None:
         # App. B1: multi-lane timings only count when they match the serial backend bitwise
         par = orc.OracleSim(sc, kind, lanes=lanes)
         ser = orc.OracleSim(sc, kind, lanes=0)
-        par.steps(0.0, 1e9, a.check_serial, t_end=1e9)
-        ser.steps(0.0, 1e9, a.check_serial, t_end=1e9)
+        par.steps(0.0, min(dt_out, t_end), a.check_serial, t_end=t_end)
+        ser.steps(0.0, min(dt_out, t_end), a.check_serial, t_end=t_end)
         out["serial_match"] = bool(np.array_equal(par.state().view(np.uint64), ser.state().view(np.uint64)))
     print(json.dumps(out))
 
