@@ -9,9 +9,11 @@ import numpy as np  # noqa: E402
 from paper_2104_06784_b200 import scenarios  # noqa: E402
 from paper_2104_06784_b200.simulator import Simulator  # noqa: E402
 
-for sc in (scenarios.c1_hill(40), scenarios.wet_valley(37, 33),
-           scenarios.c3_channel(48, 32, t_end=30.0, dt_out=0.5)):
+for sc, wide in ((scenarios.c1_hill(40), 0), (scenarios.wet_valley(37, 33), 0),
+                 (scenarios.c3_channel(48, 32, t_end=30.0, dt_out=0.5), 0),
+                 (scenarios.c1_hill(40), 1 << 30), (scenarios.wet_valley(37, 33), 1 << 30)):
     sim = Simulator.from_scenario(sc)
+    sim.set_option("wide_tiles", wide)  # production (2 CTAs/SM) and wide (512-thread) stage CTAs
     tn = 0.5 / sc.config.scaling.t_unit() if sc.config.inflow else 1e9
     t, n, _ = sim.steps(0.0, tn, 6, t_end=1e9)
     sim.apply_boundaries(t)
@@ -23,3 +25,14 @@ for sc in (scenarios.c1_hill(40), scenarios.wet_valley(37, 33),
     sim.interior_mass_device()
     assert np.isfinite(s).all()
     print(sc.name, "ok", n)
+
+# peer-joined slabs on one device (in-kernel halo wait, back-region tiles), both CTA shapes
+import torch  # noqa: E402
+from paper_2104_06784_b200.distributed import CudaSlab, PeerGroup, decompose  # noqa: E402
+for wide in (0, 1 << 30):
+    sc = scenarios.c1_hill(64)
+    slabs = [CudaSlab(sc, r, stream=torch.cuda.Stream()) for r in decompose(sc.nrows, 3)]
+    for sl in slabs:
+        sl.sim.set_option("wide_tiles", wide)
+    t, n, _ = PeerGroup(slabs).steps(0.0, 1e9, 6, t_end=1e9)
+    print("peer group", "wide" if wide else "dense", "ok", n)
