@@ -19,11 +19,12 @@ __device__ __forceinline__ void face_flux(const double (&L)[6], const double (&R
                                           double jb_r, double nZ_l, double nZ_r, double ann_l,
                                           double ann_r, double ant_l, double ant_r, double rjbf,
                                           const Phys& P, double (&out)[6]) {
-    // solver.cpp:242-245
+    // solver.cpp:242-245.  Safe tiles (CHK = false) keep a_nn, a_nt unhalved: the factor 1/2
+    // is folded, with the pressure's 1/2, into one exact FMA per flux term (below)
     const double jbf = 0.5 * (jb_l + jb_r);
     const double cf = 0.5 * (nZ_l + nZ_r);
-    const double ann = 0.5 * (ann_l + ann_r);
-    const double ant = 0.5 * (ant_l + ant_r);
+    const double ann = CHK ? 0.5 * (ann_l + ann_r) : ann_l + ann_r;
+    const double ant = CHK ? 0.5 * (ant_l + ant_r) : ant_l + ant_r;
     const Rcp rj = mkrcp_const<FD, CHK>(jbf, rjbf);
 
     // solver.cpp:265-275
@@ -112,27 +113,43 @@ __device__ __forceinline__ void face_flux(const double (&L)[6], const double (&R
     double prL0, prR0, prL1, prR1;
     if (P.adv_only) {
         prL0 = prR0 = prL1 = prR1 = 0.0;
-    } else {
+    } else if (CHK) {
         prL0 = cf * P.oma * hL0 * 0.5;
         prR0 = cf * P.oma * hR0 * 0.5;
         prL1 = cf * htL * 0.5;
         prR1 = cf * htR * 0.5;
+    } else {  // safe tile: pressures without the exact factor 1/2 (folded below)
+        prL0 = cf * P.oma * hL0;
+        prR0 = cf * P.oma * hR0;
+        prL1 = cf * htL;
+        prR1 = cf * htR;
     }
 
     // physics::directional_flux (physics.hpp:84-95) + solver.cpp:298-315
     const double ejL = P.eps * jbf * htL;
     const double ejR = P.eps * jbf * htR;
     const double ha = 0.5 * a;
+    // Safe tiles: every value is +-0 or of magnitude in [2^-800, 2^300] (DESIGN.md §3 item 6),
+    // so scaling by 1/2 or 1/4 is exact and commutes with rounding:
+    //   q*v + (ej*(ANN/2))*(X/2)   == fma(1/4, (ej*ANN)*X, q*v)
+    //   (1/2)*(fl + fr) - ha*d     == fma(1/2, fl + fr, -(ha*d))
+    // bit for bit (one rounding each side), two FP64 instructions fewer per term.
+    auto pterm = [&](double qv, double ej, double anx, double pr) {
+        return CHK ? qv + ej * anx * pr : __fma_rn(0.25, ej * anx * pr, qv);
+    };
+    auto kt = [&](double fl, double fr, double d) {
+        return CHK ? 0.5 * (fl + fr) - ha * d : __fma_rn(0.5, fl + fr, -(ha * d));
+    };
     // solid
     {
         const double flm = L[0] * vnL0, frm = R[0] * vnR0;
-        const double fln = qnL0 * vnL0 + ejL * ann * prL0;
-        const double frn = qnR0 * vnR0 + ejR * ann * prR0;
-        const double flt = qtL0 * vnL0 + ejL * ant * prL0;
-        const double frt = qtR0 * vnR0 + ejR * ant * prR0;
-        const double mass = 0.5 * (flm + frm) - ha * (R[0] - L[0]);
-        const double momn = 0.5 * (fln + frn) - ha * (qnR0 - qnL0);
-        const double momt = 0.5 * (flt + frt) - ha * (qtR0 - qtL0);
+        const double fln = pterm(qnL0 * vnL0, ejL, ann, prL0);
+        const double frn = pterm(qnR0 * vnR0, ejR, ann, prR0);
+        const double flt = pterm(qtL0 * vnL0, ejL, ant, prL0);
+        const double frt = pterm(qtR0 * vnR0, ejR, ant, prR0);
+        const double mass = kt(flm, frm, R[0] - L[0]);
+        const double momn = kt(fln, frn, qnR0 - qnL0);
+        const double momt = kt(flt, frt, qtR0 - qtL0);
         out[0] = mass;
         out[2] = XI ? momn : momt;
         out[3] = XI ? momt : momn;
@@ -140,13 +157,13 @@ __device__ __forceinline__ void face_flux(const double (&L)[6], const double (&R
     // fluid
     {
         const double flm = L[1] * vnL1, frm = R[1] * vnR1;
-        const double fln = qnL1 * vnL1 + ejL * ann * prL1;
-        const double frn = qnR1 * vnR1 + ejR * ann * prR1;
-        const double flt = qtL1 * vnL1 + ejL * ant * prL1;
-        const double frt = qtR1 * vnR1 + ejR * ant * prR1;
-        const double mass = 0.5 * (flm + frm) - ha * (R[1] - L[1]);
-        const double momn = 0.5 * (fln + frn) - ha * (qnR1 - qnL1);
-        const double momt = 0.5 * (flt + frt) - ha * (qtR1 - qtL1);
+        const double fln = pterm(qnL1 * vnL1, ejL, ann, prL1);
+        const double frn = pterm(qnR1 * vnR1, ejR, ann, prR1);
+        const double flt = pterm(qtL1 * vnL1, ejL, ant, prL1);
+        const double frt = pterm(qtR1 * vnR1, ejR, ant, prR1);
+        const double mass = kt(flm, frm, R[1] - L[1]);
+        const double momn = kt(fln, frn, qnR1 - qnL1);
+        const double momt = kt(flt, frt, qtR1 - qtL1);
         out[1] = mass;
         out[4] = XI ? momn : momt;
         out[5] = XI ? momt : momn;

@@ -221,8 +221,8 @@ __device__ __forceinline__ void stage_phase1(const double* __restrict__ S, const
                 for (int f = 0; f < 6; ++f) {
                     const double* row = S + f * BOX + kx - 1;
                     const double c0 = row[0], c1 = row[1], c2 = row[2], c3 = row[3];
-                    Lx[f] = edge_plus(c0, c1, c2);
-                    Rx[f] = edge_minus(c1, c2, c3);
+                    Lx[f] = edge_p<CHK>(c0, c1, c2);
+                    Rx[f] = edge_m<CHK>(c1, c2, c3);
                 }
                 face_flux<FD, true, CHK>(Lx, Rx, G[G_JB * BOX + kx], G[G_JB * BOX + kx + 1], G[G_NZ * BOX + kx],
                                          G[G_NZ * BOX + kx + 1], G[G_A11 * BOX + kx], G[G_A11 * BOX + kx + 1],
@@ -238,8 +238,8 @@ __device__ __forceinline__ void stage_phase1(const double* __restrict__ S, const
             for (int f = 0; f < 6; ++f) {
                 const double* col = S + f * BOX + ky - W2;
                 const double d0 = col[0], d1 = col[W2], d2 = col[2 * W2], d3 = col[3 * W2];
-                Ly[f] = edge_plus(d0, d1, d2);
-                Ry[f] = edge_minus(d1, d2, d3);
+                Ly[f] = edge_p<CHK>(d0, d1, d2);
+                Ry[f] = edge_m<CHK>(d1, d2, d3);
             }
             face_flux<FD, false, CHK>(Ly, Ry, G[G_JB * BOX + ky], G[G_JB * BOX + ky + W2], G[G_NZ * BOX + ky],
                                       G[G_NZ * BOX + ky + W2], G[G_A22 * BOX + ky], G[G_A22 * BOX + ky + W2],
@@ -267,12 +267,12 @@ __device__ __forceinline__ void stage_phase1(const double* __restrict__ S, const
         for (int f = 0; f < 6; ++f) {
             const double* row = S + f * BOX + kx - 1;
             const double c0 = row[0], c1 = row[1], c2 = row[2], c3 = row[3];
-            Lx[f] = edge_plus(c0, c1, c2);
-            Rx[f] = edge_minus(c1, c2, c3);
+            Lx[f] = edge_p<CHK>(c0, c1, c2);
+            Rx[f] = edge_m<CHK>(c1, c2, c3);
             const double* col = S + f * BOX + ky - W2;
             const double d0 = col[0], d1 = col[W2], d2 = col[2 * W2], d3 = col[3 * W2];
-            Ly[f] = edge_plus(d0, d1, d2);
-            Ry[f] = edge_minus(d1, d2, d3);
+            Ly[f] = edge_p<CHK>(d0, d1, d2);
+            Ry[f] = edge_m<CHK>(d1, d2, d3);
         }
         double ox[6], oy[6];
         face_flux<FD, true, CHK>(Lx, Rx, G[G_JB * BOX + kx], G[G_JB * BOX + kx + 1], G[G_NZ * BOX + kx],
@@ -709,11 +709,23 @@ __global__ void __launch_bounds__(NTH, NTH == NT ? 2 : 1) stage_kernel(const __g
                 const double* bvx = BR;
                 const double* bvy = BR + BOX;
                 const double* bxy = BR + 2 * BOX;
-                const double s1 = 2.0 * (bvx[bk + 1] - bvx[bk - 1]), s2 = bxy[bk + W2] - bxy[bk - W2];
-                const double s3 = 2.0 * (bvy[bk + W2] - bvy[bk - W2]), s4 = bxy[bk + 1] - bxy[bk - 1];
+                const double s2 = bxy[bk + W2] - bxy[bk - W2], s4 = bxy[bk + 1] - bxy[bk - 1];
                 bool ok3 = !CHK || (r2x.ok && r2y.ok);
-                double v1 = dq<FD, CHK>(s1, r2x, ok3), v2 = dq<FD, CHK>(s2, r2y, ok3);
-                double v3 = dq<FD, CHK>(s3, r2y, ok3), v4 = dq<FD, CHK>(s4, r2x, ok3);
+                double s1, s3, v1, v3;
+                if (CHK) {
+                    s1 = 2.0 * (bvx[bk + 1] - bvx[bk - 1]);
+                    s3 = 2.0 * (bvy[bk + W2] - bvy[bk - W2]);
+                    v1 = dq<FD, CHK>(s1, r2x, ok3);
+                    v3 = dq<FD, CHK>(s3, r2y, ok3);
+                } else {
+                    // safe tile: (2 D) / (2 dxi) by the reciprocal RN(1/(2 dxi)) = RN(1/dxi) / 2 is
+                    // (D) / (dxi) by RN(1/dxi) bit for bit (every step scales by 2 exactly)
+                    s1 = bvx[bk + 1] - bvx[bk - 1];
+                    s3 = bvy[bk + W2] - bvy[bk - W2];
+                    v1 = dq<FD, CHK>(s1, rdx, ok3);
+                    v3 = dq<FD, CHK>(s3, rdy, ok3);
+                }
+                double v2 = dq<FD, CHK>(s2, r2y, ok3), v4 = dq<FD, CHK>(s4, r2x, ok3);
                 if (!ok3) {
                     dfix<FD>(v1, s1, r2x);
                     dfix<FD>(v2, s2, r2y);
