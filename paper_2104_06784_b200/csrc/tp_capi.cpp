@@ -173,8 +173,11 @@ struct tp_ctx {
     int n_samples = 0;
     bool hydro_set = false;
     int adv_only = 0;
-    cudaGraphExec_t graphK = nullptr, graph1 = nullptr;
-    cudaGraphExec_t graphKw = nullptr, graph1w = nullptr;  // the same with wide stage CTAs (short lists)
+    // unrolled step graphs of 1, 2, 4, ..., graph_steps steps: [0] dense stage CTAs, [1] wide
+    // (short lists); a replay runs a power-of-two number of steps (steps_launch)
+    static constexpr int kMaxGraphLog = 13;  // graph_steps <= 4096 (tp_set_option)
+    cudaGraphExec_t graphs[2][kMaxGraphLog] = {};
+    double dt_hint = 0.0;               // the last step's dt: sizes the next replays (steps to the output)
     cudaGraphExec_t graphT = nullptr;   // one step with timing events around the stage kernels
     int num_sms = 148;
     int wide_tiles = -1;                // use the wide graphs while the last lists had <= this many tiles (-1: #SMs)
@@ -265,10 +268,14 @@ void build_phys(tp_ctx* c) {
 }
 
 void drop_graphs(tp_ctx* c) {
-    for (cudaGraphExec_t* gp : {&c->graphK, &c->graph1, &c->graphKw, &c->graph1w, &c->graphT}) {
-        if (*gp) cudaGraphExecDestroy(*gp);
-        *gp = nullptr;
-    }
+    for (auto& fam : c->graphs)
+        for (cudaGraphExec_t& gx : fam) {
+            if (gx) cudaGraphExecDestroy(gx);
+            gx = nullptr;
+        }
+    if (c->graphT) cudaGraphExecDestroy(c->graphT);
+    c->graphT = nullptr;
+    c->graphK_steps = 0;
 }
 
 tpb::StageArgs stage_args(tp_ctx* c, bool corr, int loop) {
@@ -1126,11 +1133,15 @@ struct StepsRun {
     DevScalars h{};
     bool finished = false;
     double* dts = nullptr;
+    double t_next = 0.0;
 };
 
 void steps_begin(tp_ctx* c, StepsRun& r, double t, double t_next, double t_end, long max_steps, double* dts) {
     r.max_steps = max_steps;
     r.dts = dts;
+    r.t_next = t_next < t_end ? t_next : t_end;
+    r.h.t = t;
+    r.h.steps = 0;
     c->launches = 0;
     if (dts && c->dts_cap < max_steps) {
         cudaFree(c->dDts);
@@ -1149,12 +1160,10 @@ void steps_begin(tp_ctx* c, StepsRun& r, double t, double t_next, double t_end, 
         fresh_lambda(c);
         c->launches += 1;
     }
-    if (!c->graphK || c->graphK_steps != c->graph_steps) {
+    if (c->graphK_steps != c->graph_steps) {
         drop_graphs(c);
-        c->graphK = capture_steps(c, c->graph_steps);
-        c->graph1 = capture_steps(c, 1);
-        c->graphKw = capture_steps(c, c->graph_steps, nullptr, true);
-        c->graph1w = capture_steps(c, 1, nullptr, true);
+        for (int w = 0; w < 2; ++w)
+            for (int l = 0; (1 << l) <= c->graph_steps; ++l) c->graphs[w][l] = capture_steps(c, 1 << l, nullptr, w != 0);
         c->graphK_steps = c->graph_steps;
     }
     if (c->last_tiles_stage == 0) {  // the graphs start with a predictor list
@@ -1165,13 +1174,31 @@ void steps_begin(tp_ctx* c, StepsRun& r, double t, double t_next, double t_end, 
     c->last_tiles_stage = 1;
 }
 
-void steps_launch(tp_ctx* c, StepsRun& r) {
-    const bool big = (r.max_steps - r.h.steps) >= c->graph_steps;
-    const int k = big ? c->graph_steps : 1;
-    ck(cudaGraphLaunch(c->wide ? (big ? c->graphKw : c->graph1w) : (big ? c->graphK : c->graph1), c->stream),
-       "graph launch");
-    c->launches += (c->peered ? 8L : 5L) * k;  // peered: + lambda exchange + 2 halo pushes
-    r.launched += k;
+// Steps to launch before the next poll: up to the output time at the last dt (+1 in case dt
+// shrinks), at most graph_steps and the steps left.  A replay past a stop (output hit, t_end,
+// error) runs no-op launches, so long graphs are only used when no output is near.
+long steps_to_launch(const tp_ctx* c, const StepsRun& r) {
+    long n = static_cast<long>(r.max_steps - r.h.steps);
+    if (n > c->graph_steps) n = c->graph_steps;
+    if (c->dt_hint > 0.0) {
+        const double left = (r.t_next - r.h.t) / c->dt_hint;
+        const double est = left > 0.0 ? std::ceil(left) + 1.0 : 1.0;
+        if (est < static_cast<double>(n)) n = static_cast<long>(est);
+    }
+    return n < 1 ? 1 : n;
+}
+
+// n steps as back-to-back replays of the power-of-two graphs (largest first, one poll after)
+void steps_launch(tp_ctx* c, StepsRun& r, long n) {
+    for (int l = tp_ctx::kMaxGraphLog - 1; l >= 0; --l) {
+        const long k = 1L << l;
+        while (n >= k && c->graphs[0][l]) {
+            ck(cudaGraphLaunch(c->graphs[c->wide ? 1 : 0][l], c->stream), "graph launch");
+            c->launches += (c->peered ? 8L : 5L) * k;  // peered: + lambda exchange + 2 halo pushes
+            r.launched += k;
+            n -= k;
+        }
+    }
 }
 
 // the graph family of the next replay: wide stage CTAs (one tile per SM, one face per thread)
@@ -1185,7 +1212,10 @@ void choose_wide(tp_ctx* c, const DevScalars& h) {
 void steps_poll(tp_ctx* c, StepsRun& r) {
     r.h = read_scalars(c);
     r.finished = r.h.done != 0;
-    if (r.h.steps > 0) choose_wide(c, r.h);
+    if (r.h.steps > 0) {
+        choose_wide(c, r.h);
+        c->dt_hint = r.h.dt;
+    }
 }
 
 // A device error key with the slab's local row replaced by the global row, so keys of
@@ -1234,7 +1264,7 @@ int tp_steps(tp_ctx* c, double t_next, double t_end, long max_steps, double* t, 
         StepsRun r;
         steps_begin(c, r, *t, t_next, t_end, max_steps, dts);
         while (!r.finished) {
-            steps_launch(c, r);
+            steps_launch(c, r, steps_to_launch(c, r));
             steps_poll(c, r);
         }
         steps_end(c, r, t, steps, hit);
@@ -1255,9 +1285,11 @@ int tp_steps_group(tp_ctx* const* cs, int n, double t_next, double t_end, long m
             steps_begin(cs[k], runs[k], *t, t_next, t_end, max_steps, nullptr);
         }
         for (;;) {
-            for (int k = 0; k < n; ++k) {  // every member launches before anyone waits
+            // every member launches the same steps (member 0's estimate) before anyone waits
+            const long ns = steps_to_launch(cs[0], runs[0]);
+            for (int k = 0; k < n; ++k) {
                 cudaSetDevice(cs[k]->device);
-                steps_launch(cs[k], runs[k]);
+                steps_launch(cs[k], runs[k], ns);
             }
             bool any = false, all = true;
             for (int k = 0; k < n; ++k) {
@@ -1395,14 +1427,20 @@ int tp_peer_connect_local(tp_ctx* c, int rank, int nranks, tp_ctx* const* all) {
         // peer_lambda_kernel stores into every rank's mailbox, peer_halo_push_kernel into the
         // neighbours' state: peer access to every other device of the group
         c->stage_ctas = 0;
+        int nshare = 0;  // members on this device, this one included
+        for (int r = 0; r < nranks; ++r)
+            if (all[r]->device == c->device) ++nshare;
         for (int r = 0; r < nranks; ++r) {
             L.box[r] = all[r]->dBox;
             if (r != rank && all[r]->device == c->device) {
                 // members sharing this device run their kernels beside this one's stage kernel,
-                // which may wait for their halo pushes: leave 4 SMs to them
+                // which may wait for their halo pushes: the members' stage grids together leave
+                // 4 SMs to the small kernels (pre, halo push), so a push never waits for a stage
+                // CTA that is itself waiting (with 3+ members, stage kernels of several members
+                // could otherwise fill every SM)
                 int sms = 148;
                 cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
-                c->stage_ctas = 2 * (sms - 4);
+                c->stage_ctas = 2 * ((sms - 4) / nshare);
             }
             if (all[r]->device != c->device) {
                 const cudaError_t e = cudaDeviceEnablePeerAccess(all[r]->device, 0);
