@@ -240,6 +240,7 @@ void build_phys(tp_ctx* c) {
     P.eps_NR = P.eps * p.N_R;                            // physics.hpp:115
     P.h_dry = p.h_dry;
     P.eps_h = p.eps_h;
+    P.eps_h2 = p.eps_h * p.eps_h;
     P.dxi = c->dxi;
     P.deta = c->deta;
     P.two_dxi = 2.0 * c->dxi;

@@ -81,21 +81,21 @@ __device__ __forceinline__ void face_flux(const double (&L)[6], const double (&R
     if (FD) {  // four desingularisation divisions, one shared slow-path branch
         bool okf = true;
         // safe tile: the d's are +0 or positive (above), so no signed-zero select is needed
-        fL0 = desing_factor_g<CHK, !CHK>(dL0, P.eps_h, okf);
-        fR0 = desing_factor_g<CHK, !CHK>(dR0, P.eps_h, okf);
-        fL1 = desing_factor_g<CHK, !CHK>(dL1, P.eps_h, okf);
-        fR1 = desing_factor_g<CHK, !CHK>(dR1, P.eps_h, okf);
+        fL0 = desing_factor_g<CHK, !CHK>(dL0, P.eps_h, P.eps_h2, okf);
+        fR0 = desing_factor_g<CHK, !CHK>(dR0, P.eps_h, P.eps_h2, okf);
+        fL1 = desing_factor_g<CHK, !CHK>(dL1, P.eps_h, P.eps_h2, okf);
+        fR1 = desing_factor_g<CHK, !CHK>(dR1, P.eps_h, P.eps_h2, okf);
         if (!okf) {
-            fL0 = desing_factor<FD>(dL0, P.eps_h);
-            fR0 = desing_factor<FD>(dR0, P.eps_h);
-            fL1 = desing_factor<FD>(dL1, P.eps_h);
-            fR1 = desing_factor<FD>(dR1, P.eps_h);
+            fL0 = desing_factor<FD>(dL0, P.eps_h, P.eps_h2);
+            fR0 = desing_factor<FD>(dR0, P.eps_h, P.eps_h2);
+            fL1 = desing_factor<FD>(dL1, P.eps_h, P.eps_h2);
+            fR1 = desing_factor<FD>(dR1, P.eps_h, P.eps_h2);
         }
     } else {
-        fL0 = desing_factor<FD>(dL0, P.eps_h);
-        fR0 = desing_factor<FD>(dR0, P.eps_h);
-        fL1 = desing_factor<FD>(dL1, P.eps_h);
-        fR1 = desing_factor<FD>(dR1, P.eps_h);
+        fL0 = desing_factor<FD>(dL0, P.eps_h, P.eps_h2);
+        fR0 = desing_factor<FD>(dR0, P.eps_h, P.eps_h2);
+        fL1 = desing_factor<FD>(dL1, P.eps_h, P.eps_h2);
+        fR1 = desing_factor<FD>(dR1, P.eps_h, P.eps_h2);
     }
     const double vnL0 = jL0 * fL0;
     const double vnR0 = jR0 * fR0;

@@ -173,7 +173,7 @@ __device__ __forceinline__ unsigned long long cell_epilogue(double (&un)[6], con
         const double h = hs + hf;
         if (!(h < P.h_dry)) {
             double fsld, fflu;
-            desing_pair<FD>(hs, hf, P.eps_h, fsld, fflu);
+            desing_pair<FD>(hs, hf, P.eps_h, P.eps_h2, fsld, fflu);
             const double vsx = jsx * fsld, vsy = jsy * fsld;
             const double vfx = jfx * fflu, vfy = jfy * fflu;
             const double cel = sqrt(P.eps * nZ * h);
@@ -316,7 +316,7 @@ __device__ __forceinline__ void stage_phase1(const double* __restrict__ S, const
             const double h = hs + hf;
             double fsld, fflu;
             // safe tile: thicknesses are +0 or positive (TF_UNSAFE2 excludes -0), so are hs, hf
-            desing_pair<FD, CHK, !CHK>(hs, hf, P.eps_h, fsld, fflu);
+            desing_pair<FD, CHK, !CHK>(hs, hf, P.eps_h, P.eps_h2, fsld, fflu);
             V[0 * BOX + k] = jsx * fsld;
             V[1 * BOX + k] = jsy * fsld;
             V[2 * BOX + k] = jfx * fflu;
@@ -352,7 +352,15 @@ __global__ void __launch_bounds__(NTH, NTH == NT ? 2 : 1) stage_kernel(const __g
     double* FY = sm + SM_FY;
 
     DevScalars* sc = A.sc;
-    if (A.loop && *(volatile int*)&sc->done) return;
+    // the launch's scalars in one memory round trip (sparse steps are latency bound: the stop
+    // flag, the list length and this CTA's first list entry are independent loads, issued
+    // together instead of one after the other); the grid never exceeds the tile count, so
+    // tiles[blockIdx.x] is in bounds (its value is used only if it is on the list)
+    const int done0 = A.loop ? __ldcg(&sc->done) : 0;
+    const int n_main = __ldcg(A.ntiles_active);
+    const int e_first = __ldcg(A.tiles + blockIdx.x);
+    const double dt = __ldcg(&sc->dt);
+    if (done0) return;
 
     const GridDesc& g = A.g;
     const Phys& P = A.ph;
@@ -361,13 +369,11 @@ __global__ void __launch_bounds__(NTH, NTH == NT ? 2 : 1) stage_kernel(const __g
     const long long fs = g.fs;
     const int ntiles = A.ntx * A.nty;
     // active-tile list of this stage (tiles_kernel); PEER: plus its back region (StageArgs::nback)
-    const int n_main = *A.ntiles_active;
     const int nact = n_main + (PEER ? *A.nback : 0);
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         A.nact_stat[CORR ? 1 : 0] = nact;  // diagnostics
         sc->last_nact[CORR ? 1 : 0] = nact;  // the host's dense / wide graph choice (tp_capi.cpp)
     }
-    const double dt = sc->dt;
     // list entry li: the front of `tiles`, then (PEER) its back region from the end
     auto entry_at = [&](int li) { return (!PEER || li < n_main) ? A.tiles[li] : A.tiles[ntiles - 1 - (li - n_main)]; };
     // PEER, thread 0: make li a tile to process (or >= nact).  A back-region tile needs the
@@ -423,8 +429,8 @@ __global__ void __launch_bounds__(NTH, NTH == NT ? 2 : 1) stage_kernel(const __g
         mbar_init(&bar, 1);
         mbar_init(&barc, 1);
         mbar_init(&baru, 1);
-        int e = 0;
-        const int li0 = resolve(static_cast<int>(blockIdx.x), e);
+        int e = e_first;
+        const int li0 = PEER ? resolve(static_cast<int>(blockIdx.x), e) : static_cast<int>(blockIdx.x);
         s_li0 = li0;
         if (li0 < nact) {
             s_tile = e;
@@ -771,10 +777,10 @@ __global__ void __launch_bounds__(NTH, NTH == NT ? 2 : 1) stage_kernel(const __g
                     double fsld;
                     if (FD) {
                         bool okf = true;
-                        fsld = desing_factor_g(hs, P.eps_h, okf);
-                        if (!okf) fsld = desing_factor<FD>(hs, P.eps_h);
+                        fsld = desing_factor_g(hs, P.eps_h, P.eps_h2, okf);
+                        if (!okf) fsld = desing_factor<FD>(hs, P.eps_h, P.eps_h2);
                     } else {
-                        fsld = desing_factor<FD>(hs, P.eps_h);
+                        fsld = desing_factor<FD>(hs, P.eps_h, P.eps_h2);
                     }
                     const double vsx = jx * fsld;
                     const double vsy = jy * fsld;
@@ -1061,7 +1067,7 @@ __global__ void __launch_bounds__(NT) lambda_kernel(GridDesc g, Phys P, const do
         const double hf = dv<FD>(s[1 * g.fs + o], rj);
         const double h = hs + hf;
         double fsld, fflu;
-        desing_pair<FD>(hs, hf, P.eps_h, fsld, fflu);
+        desing_pair<FD>(hs, hf, P.eps_h, P.eps_h2, fsld, fflu);
         const double vsx = dv<FD>(s[2 * g.fs + o], rj) * fsld;
         const double vsy = dv<FD>(s[3 * g.fs + o], rj) * fsld;
         const double vfx = dv<FD>(s[4 * g.fs + o], rj) * fflu;
@@ -1511,9 +1517,9 @@ __global__ void selftest_div_kernel(long long n, unsigned long long seed, unsign
         // desingularisation factor, grouped vs single
         const double hh = fabs(a) * 1e-3;
         bool okg = true;
-        double fg = desing_factor_g(hh, 1e-6, okg);
-        if (!okg) fg = desing_factor<true>(hh, 1e-6);
-        if (__double_as_longlong(fg) != __double_as_longlong(desing_factor<false>(hh, 1e-6))) ++local;
+        double fg = desing_factor_g(hh, 1e-6, 1e-6 * 1e-6, okg);
+        if (!okg) fg = desing_factor<true>(hh, 1e-6, 1e-6 * 1e-6);
+        if (__double_as_longlong(fg) != __double_as_longlong(desing_factor<false>(hh, 1e-6, 1e-6 * 1e-6))) ++local;
         // square root: the branch-free sequence (when accepted) vs sqrt, and acceptance on
         // ordinary operands (+-0 included)
         const double xs = (mode == 3 && (i & 7) == 0) ? a : fabs(a) * (mode == 2 ? 1e-300 : 1.0);

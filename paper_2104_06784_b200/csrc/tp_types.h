@@ -19,6 +19,7 @@ struct Phys {
     double neg_eps_alpha;  // -eps * alpha_rho         (physics.hpp:147)
     double eps_NR;     // eps * N_R                   (physics.hpp:115)
     double h_dry, eps_h;
+    double eps_h2;     // RN(eps_h * eps_h): max(h, eps_h)^2 of the desingularisation is this or h*h
     double dxi, deta, two_dxi, two_deta;
     double cell_area;  // dxi * deta                  (solver.cpp:140)
     double cfl;
