@@ -341,6 +341,7 @@ tpb::TileArgs tile_args(tp_ctx* c, const tpb::StageArgs& a, bool corr) {
     t.north_ineligible = c->g.has_north ? 0 : 1;
     t.safe_ok = (c->fastdiv && c->geo_safe && c->geo_safe2) ? 1 : 0;
     t.cond_halo = (a.loop && c->peered) ? 1 : 0;
+    t.stage = corr ? 1 : 0;
     t.nback = c->dNact + 8 + (corr ? 1 : 0);
     t.nback_reset = c->dNact + 8 + (corr ? 0 : 1);
     t.loop = a.loop;
@@ -392,6 +393,7 @@ void launch_bc(tp_ctx* c, int buf, int tsrc, double t, int loop) {
 
 void launch_post(tp_ctx* c, int loop) {
     tpb::PostArgs a{};
+    a.inflow = inflow_desc(c);
     a.sc = c->dSc;
     a.tally_pred = c->dTallyP;
     a.tally_corr = c->dTallyC;

@@ -888,7 +888,10 @@ __device__ __forceinline__ void tiles_body(const TileArgs& a, int block) {
         }
         active = !skip;
         back = active && halo_reach && a.cond_halo != 0;  // peer-joined: after the other tiles
-        if (active && a.safe_ok && !(ghost_box && a.ring_ineligible) && !inflow_box && !(reach_s && a.south_ineligible) &&
+        // an inflow tile's box also reads Mode-II inflow ghosts, which the flags do not see:
+        // safe only while the stage's inflow values are inside the window (inflow_window_ok)
+        const bool inflow_ok = !inflow_box || (a.loop && a.sc->inflow_safe[a.stage]);
+        if (active && a.safe_ok && !(ghost_box && a.ring_ineligible) && inflow_ok && !(reach_s && a.south_ineligible) &&
             !(reach_n && a.north_ineligible)) {
             // safe: no value the box reads (this tile and the facing parts of its 8
             // neighbours; ghosts are clamp copies of them) is outside the window
@@ -983,6 +986,30 @@ __device__ void hydro_at(const Inflow& in, double t, double& h, double& phi, dou
         }
     }
     h = s[4 * (n - 1) + 1]; phi = s[4 * (n - 1) + 2]; speed = s[4 * (n - 1) + 3];
+}
+
+// The safe-tile window (DESIGN.md §3 item 6) over the Mode-II inflow ghosts bc_body writes at
+// time t (scaled): v = jb*hs, jb*hf, (jb*hs)*v_x, (jb*hs)*v_y, (jb*hf)*v_x, (jb*hf)*v_y with
+// jb in [1, 2^50] (the geometry window of a context that uses safe tiles).  Sufficient:
+// thicknesses +0 or positive, each of hs, hf, hs*|speed|, hf*|speed| zero or in [2^-98, 2^48]
+// (a factor 2^2 of margin for the roundings of the products); then every ghost value is
+// +-0 or of magnitude in [2^-100, 2^100).  NaN / inf fail the comparisons.  One thread.
+__device__ int inflow_window_ok(const Inflow& in, double t) {
+    if (!in.active) return 0;
+    double sh, sphi, sspeed;
+    hydro_at(in, t * in.t_unit, sh, sphi, sspeed);
+    const double h = sh / in.H;
+    const double speed = sspeed / in.v_unit;
+    const double hs = h * sphi;
+    const double hf = h * (1.0 - sphi);
+    auto zero_or_in = [](double x) {
+        const double m = fabs(x);
+        return x == 0.0 || (m >= 0x1p-98 && m <= 0x1p48);
+    };
+    auto plus = [](double x) { return __double2hiint(x) >= 0 && !(x < 0.0); };  // +0 or positive
+    const double sp = fabs(speed);
+    return (plus(hs) && plus(hf) && zero_or_in(hs) && zero_or_in(hf) && zero_or_in(speed) &&
+            zero_or_in(hs * sp) && zero_or_in(hf * sp)) ? 1 : 0;
 }
 
 __device__ __forceinline__ void bc_body(const BcArgs& a, int block) {
@@ -1115,7 +1142,11 @@ __global__ void __launch_bounds__(NT) pre_kernel(const __grid_constant__ PreArgs
         if (a.with_dt && blockIdx.x == 0 && threadIdx.x == 0) a.t.sc->done = 1;
         return;
     }
-    if (a.with_dt && blockIdx.x == 0 && threadIdx.x == 0) dt_body(a.P, a.t.sc, 0);
+    if (a.with_dt && blockIdx.x == 0 && threadIdx.x == 0) {
+        dt_body(a.P, a.t.sc, 0);
+        // the corrector's inflow ghosts are bc at t + dt (tsrc 2)
+        a.t.sc->inflow_safe[1] = inflow_window_ok(a.bc.inflow, a.t.sc->t + a.t.sc->dt);
+    }
     if (static_cast<int>(blockIdx.x) < a.nb_bc) bc_body(a.bc, blockIdx.x);
     else tiles_body(a.t, blockIdx.x - a.nb_bc);
 }
@@ -1188,6 +1219,8 @@ __global__ void __launch_bounds__(NT) post_kernel(PostArgs a) {
             // exchange, which stops every rank at the same step (a local stop here would leave
             // the other ranks waiting for this one)
             if ((!a.peered && sc->err_key != kNoError) || sc->hit || sc->steps >= sc->max_steps) sc->done = 1;
+            // the next predictor's inflow ghosts are bc at the new t (tsrc 1)
+            sc->inflow_safe[0] = inflow_window_ok(a.inflow, sc->t);
         }
     }
 }

@@ -81,6 +81,10 @@ struct DevScalars {
     long long max_steps;
     int done;        // stop flag: every loop kernel returns immediately when set
     int hit;         // exact_hit of the step in flight (solver.cpp:641)
+    // Mode-II inflow ghosts of the [predictor, corrector] stage in flight are inside the
+    // safe-tile window (inflow_window_ok): their tiles may take the safe forms.  Cleared by
+    // every write_ctrl (the first predictor of a tp_steps call keeps the checked forms).
+    int inflow_safe[2];
     unsigned long long lam_bits;  // atomicMax accumulator of lambda (bits of a double >= 0)
     unsigned long long lam_cur;   // lambda_max of the current state (compute_dt input)
     unsigned long long err_key;   // earliest error (see error keys in tp_kernels.cu)
@@ -197,6 +201,7 @@ struct TileArgs {
     const unsigned char* inflow_tiles;  // per tile: its box reads a Mode-II inflow ghost (never skip, never safe); may be null
     int south_ineligible, north_ineligible;  // slab edges next to halo rows: never skip
     int safe_ok;          // FASTDIV on, geometry and constants inside the safe-window bounds (tp_capi.cpp)
+    int stage;            // 0 predictor, 1 corrector (DevScalars::inflow_safe index)
     int cond_halo;        // peer-joined slab: tiles whose box reads halo rows go to the back of `tiles`
                           // (StageArgs::nback), flagged kTileCond when otherwise a no-op
     int* nback;           // this stage's back-region count (zeroed by the other stage's tiles_kernel)
@@ -227,6 +232,7 @@ struct PreArgs {
 
 struct PostArgs {
     DevScalars* sc;
+    Inflow inflow;   // the next predictor's inflow-window test (DevScalars::inflow_safe)
     const double* tally_pred;
     const double* tally_corr;
     int ntx, nty;

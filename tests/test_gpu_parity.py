@@ -501,6 +501,32 @@ def test_four_side_inflow_bitwise(gpu, oracle_kind, shape):
     np.testing.assert_allclose(sim.audit_array(), ref.audit(), rtol=1e-12, atol=1e-300)
 
 
+def test_inflow_window_edges_bitwise(gpu, oracle_kind):
+    """Inflow tiles take the safe-tile forms only while the stage's Mode-II ghost values are
+    inside the window (tp_kernels.cu inflow_window_ok, checked on the device per stage).  A
+    hydrograph that passes through depths and speeds far outside it (1e-35 m, 1e-33 m/s,
+    phi 0 and 1, a 1e-31 m/s speed) alternates the inflow tiles between the safe and the
+    checked forms: dt, state and audit stay bit-identical to the reference."""
+    import dataclasses
+    sc = scenarios.four_side_inflow(48, 40)
+    samples = [(0.0, 1e-35, 0.6, 1e-33), (5.0, 2.0, 1.0, 3.0), (10.0, 1e-30, 0.0, 2.0),
+               (15.0, 2.5, 0.5, 1e-31), (20.0, 0.0, 0.5, 0.0)]
+    sc = dataclasses.replace(sc, hydrograph=dataclasses.replace(sc.hydrograph, samples=samples))
+    sc.hydrograph.validate(sc.ncols, sc.nrows)
+    ref, sim = _pair(sc, oracle_kind)
+    tu = sc.config.scaling.t_unit()
+    t_r = t_g = 0.0
+    t_end = sc.config.t_end / tu
+    for k in range(1, 61):
+        t_next = min(k * sc.config.dt_out / tu, t_end)
+        t_r, dts_r, _ = ref.steps(t_r, t_next, 100_000, t_end=t_end)
+        t_g, dts_g, _ = sim.steps(t_g, t_next, 100_000, t_end=t_end, record_dts=True)
+        assert_bitwise(dts_g, dts_r, f"dts interval {k}")
+        assert t_r == t_g
+    assert_bitwise(sim.state(), ref.state(), "inflow window-edge state")
+    np.testing.assert_allclose(sim.audit_array(), ref.audit(), rtol=1e-12, atol=1e-300)
+
+
 def test_regularize_clips_small_negatives(gpu, oracle_kind):
     """regularize (solver.cpp:139-166): -1e-12 <= hp < 0 is clipped to 0 with its mass in the
     audit's 'clipped' slot, and the momenta of the now-dry phase are zeroed; then the run
