@@ -1170,16 +1170,17 @@ __device__ __forceinline__ int ring_tile(int ntx, int nty, int r) {
     return row * ntx + ((r & 1) ? ntx - 1 : 0);       // left/right columns
 }
 
-__global__ void __launch_bounds__(NT) post_kernel(PostArgs a) {
+constexpr int kPostThreads = 1024;  // one pass over the ring tiles of grids up to ~4000 tiles wide
+__global__ void __launch_bounds__(kPostThreads) post_kernel(PostArgs a) {
     DevScalars* sc = a.sc;
     if (a.loop && sc->done) return;
-    clip_fold_block<NT>(sc);  // regularize's clipped mass of both stages, reference order
-    // both stages' 4 tallies per ring tile: per-thread sums, warp shuffles, then the 8 warp
-    // partials in warp order (deterministic)
-    __shared__ double red[NT / 32][8];
+    // both stages' 4 tallies per ring tile: per-thread sums, warp shuffles, then the warp
+    // partials reduced by warp 0 in warp order (deterministic).  The tally loads are issued
+    // before the clip fold's count is read (independent slots of the audit).
+    __shared__ double red[kPostThreads / 32][8];
     const int nring = ring_tile_count(a.ntx, a.nty);
     double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-    for (int r = threadIdx.x; r < nring; r += NT) {
+    for (int r = threadIdx.x; r < nring; r += kPostThreads) {
         const long long o = 4ll * ring_tile(a.ntx, a.nty, r);
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -1194,14 +1195,18 @@ __global__ void __launch_bounds__(NT) post_kernel(PostArgs a) {
     if ((threadIdx.x & 31) == 0)
 #pragma unroll
         for (int q = 0; q < 8; ++q) red[threadIdx.x >> 5][q] = acc[q];
+    clip_fold_block<kPostThreads>(sc);  // regularize's clipped mass of both stages, reference order
     __syncthreads();
-    if (threadIdx.x == 0) {
-        double tot[8];
+    double tot[8];
+    if (threadIdx.x < 32) {
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-            tot[q] = 0.0;
-            for (int w = 0; w < NT / 32; ++w) tot[q] += red[w][q];
+            double v = red[threadIdx.x][q];
+            for (int d = 16; d > 0; d >>= 1) v += __shfl_down_sync(0xffffffffu, v, d);
+            tot[q] = v;
         }
+    }
+    if (threadIdx.x == 0) {
         // predictor then corrector, as the reference's two accumulate_boundary_fluxes calls
         for (int st = 0; st < 2; ++st) {
             sc->audit[2] += tot[4 * st + 0];  // solid injected
@@ -1335,7 +1340,7 @@ cudaError_t launch_dt(const Phys& P, DevScalars* sc, int loop, cudaStream_t st) 
 }
 
 cudaError_t launch_post(const PostArgs& a, cudaStream_t st) {
-    post_kernel<<<1, NT, 0, st>>>(a);
+    post_kernel<<<1, kPostThreads, 0, st>>>(a);
     return cudaGetLastError();
 }
 

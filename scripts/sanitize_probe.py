@@ -14,8 +14,13 @@ for sc, wide in ((scenarios.c1_hill(40), 0), (scenarios.wet_valley(37, 33), 0),
                  (scenarios.c1_hill(40), 1 << 30), (scenarios.wet_valley(37, 33), 1 << 30)):
     sim = Simulator.from_scenario(sc)
     sim.set_option("wide_tiles", wide)  # production (2 CTAs/SM) and wide (512-thread) stage CTAs
-    tn = 0.5 / sc.config.scaling.t_unit() if sc.config.inflow else 1e9
-    t, n, _ = sim.steps(0.0, tn, 6, t_end=1e9)
+    if sc.config.inflow:  # Mode-II: several output intervals (inflow-window checks, safe inflow tiles)
+        t, n = 0.0, 0
+        for k in range(1, 5):
+            t, nk, _ = sim.steps(t, k * 0.5 / sc.config.scaling.t_unit(), 6, t_end=1e9)
+            n += nk
+    else:
+        t, n, _ = sim.steps(0.0, 1e9, 6, t_end=1e9)
     sim.apply_boundaries(t)
     dt = sim.compute_dt(t, 1e9)
     sim.advance_step(dt, t)
