@@ -51,8 +51,10 @@ for b in blocks:
     rows = list(csv.reader(b[1:])); hdr = rows[0]; data = [r for r in rows[1:] if len(r) == len(hdr)]
     si = hdr.index("Warp Stall Sampling (All Samples)"); ii = hdr.index("Instructions Executed")
     reasons = [h for h in hdr if h.startswith("stall_") and "Not Issued" not in h]
-    m = re.search(r'\(bool\)(\d), \(bool\)(\d)', b[0])
-    fname = [f for f in mp if "stage_kernel" in f and f"ILb{m.group(1)}ELb{m.group(2)}E" in f][0]
+    # the exact instance: every template argument (FD, CORR, PEER, NTH) of the reported kernel
+    m = re.search(r'\(bool\)(\d), \(bool\)(\d), \(bool\)(\d), \(int\)(\d+)', b[0])
+    key = f"ILb{m.group(1)}ELb{m.group(2)}ELb{m.group(3)}ELi{m.group(4)}E"
+    fname = [f for f in mp if "stage_kernel" in f and key in f][0]
     base = int(data[0][0], 16)
     S = collections.Counter(); I = collections.Counter(); R = collections.defaultdict(collections.Counter)
     for r in data:
