@@ -48,6 +48,8 @@ cudaError_t launch_peer_lambda(const PeerLink& L, DevScalars* sc, cudaStream_t s
 cudaError_t launch_peer_halo(const PeerLink& L, const GridDesc& g, const double* s, int buf, DevScalars* sc,
                              cudaStream_t st);
 cudaError_t launch_pack_state(const GridDesc& g, const double* src, double* dst, bool unpack, cudaStream_t st);
+cudaError_t launch_flag_scan(const GridDesc& g, const double* s, int ntx, int nty, unsigned short* flags,
+                             cudaStream_t st);
 cudaError_t launch_mass(const GridDesc& g, const double* s, double* part, int blocks, cudaStream_t st);
 cudaError_t launch_snapshot(const GridDesc& g, const double* s, const double* geo, double* out, int ncols,
                             int nrows, double H, double h_dry, double eps_h, double vu, cudaStream_t st);
@@ -376,6 +378,13 @@ void invalidate_flags(tp_ctx* c, bool a_buf, bool b_buf) {
     const size_t n = static_cast<size_t>(c->ntx) * c->nty;
     if (a_buf) ck(cudaMemsetAsync(c->dFlagA, 0xff, n * sizeof(unsigned short), c->stream), "flags");
     if (b_buf) ck(cudaMemsetAsync(c->dFlagB, 0xff, n * sizeof(unsigned short), c->stream), "flags");
+}
+
+// Exact flags of buffer A after a write outside the stage kernels (flag_scan_kernel): the next
+// stage lists only the tiles that can change instead of every tile (after tp_set_state the
+// first step used to process the whole grid twice).
+void scan_flags_A(tp_ctx* c) {
+    ck(tpb::launch_flag_scan(c->g, c->dA, c->ntx, c->nty, c->dFlagA, c->stream), "flag scan");
 }
 
 void launch_bc(tp_ctx* c, int buf, int tsrc, double t, int loop) {
@@ -934,7 +943,7 @@ int tp_set_initial_thickness(tp_ctx* c, const double* h_m) {
            "thickness H2D");
         ck(tpb::launch_init_thickness(c->g, c->dGeo, d, c->ncols, c->nrows, c->p.H, c->p.phi_s0, c->dA, c->stream),
            "init_thickness_kernel");
-        invalidate_flags(c, true, false);
+        scan_flags_A(c);
         ck(cudaStreamSynchronize(c->stream), "sync");
         c->lam_valid = false;
         c->ghosts_in_B = false;
@@ -953,7 +962,7 @@ int tp_set_initial_velocity(tp_ctx* c, const double* vx, const double* vy) {
         ck(tpb::launch_init_velocity(c->g, c->dGeo, d, d + m, c->ncols, c->nrows, std::sqrt(c->p.g * c->p.L), c->dA,
                                      c->stream),
            "init_velocity_kernel");
-        invalidate_flags(c, true, false);
+        scan_flags_A(c);
         ck(cudaStreamSynchronize(c->stream), "sync");
         c->lam_valid = false;
         c->ghosts_in_B = false;
@@ -1061,7 +1070,7 @@ int tp_get_state(tp_ctx* c, double* out) {
 int tp_set_state(tp_ctx* c, const double* in) {
     TP_GUARD(c, {
         upload_state(c, c->dA, in);
-        invalidate_flags(c, true, false);
+        scan_flags_A(c);
         ck(cudaStreamSynchronize(c->stream), "sync");
         c->lam_valid = false;
         c->ghosts_in_B = false;
@@ -1112,7 +1121,7 @@ int tp_regularize(tp_ctx* c) {
         sync_ghosts(c);
         ck(tpb::launch_regularize(c->g, c->ph, c->dA, c->dGeo, c->dSc, c->fastdiv, c->stream),
            "regularize_kernel");
-        invalidate_flags(c, true, false);
+        scan_flags_A(c);
         c->lam_valid = false;
         check_error(c, c->dA);
     })

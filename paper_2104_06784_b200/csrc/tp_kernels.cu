@@ -1370,6 +1370,40 @@ __global__ void pack_state_kernel(GridDesc g, const double* __restrict__ src, do
         dst[k] = src[f * g.fs + j * g.pitch + i];
     }
 }
+// Exact per-tile output flags (TileFlag) of a state buffer written outside the stage kernels
+// (tp_set_state, initial conditions, regularize): the same bits the stage kernels' epilogue
+// reduces over their outputs (cell_epilogue + the tile's flag OR), so the next stage lists only
+// the tiles that are not bitwise no-ops instead of every tile ("unknown" flags).  One block of
+// NT threads per tile, thread t = interior cell t.
+__global__ void __launch_bounds__(NT) flag_scan_kernel(GridDesc g, const double* __restrict__ s, int ntx,
+                                                       unsigned short* __restrict__ flags) {
+    __shared__ unsigned s_f;
+    const int tile = blockIdx.x;
+    const int tix = tile % ntx, tiy = tile / ntx;
+    const int cx = threadIdx.x % TX, cy = threadIdx.x / TX;
+    const int X = 3 + tix * TX + cx, Y = 3 + tiy * TY + cy;
+    if (threadIdx.x == 0) s_f = 0u;
+    __syncthreads();
+    unsigned fb = 0u;
+    if (threadIdx.x < TX * TY && X <= g.nx - 4 && Y <= g.ny - 4) {
+        const long long o = static_cast<long long>(Y) * g.pitch + X;
+        unsigned long long bits = 0ull;
+        bool inwin2 = true;
+#pragma unroll
+        for (int f = 0; f < 6; ++f) {
+            const double v = s[f * g.fs + o];
+            bits |= static_cast<unsigned long long>(__double_as_longlong(v));
+            inwin2 = inwin2 && in_safe_window2(v);
+        }
+        inwin2 = inwin2 && __double2hiint(s[o]) >= 0 && __double2hiint(s[g.fs + o]) >= 0;
+        fb = (bits != 0ull ? cell_flag_bits(cx, cy) : 0u) | (inwin2 ? 0u : static_cast<unsigned>(TF_UNSAFE2));
+    }
+    const unsigned wf = __reduce_or_sync(0xffffffffu, fb);
+    if ((threadIdx.x & 31) == 0 && wf) atomicOr(&s_f, wf);
+    __syncthreads();
+    if (threadIdx.x == 0) flags[tile] = static_cast<unsigned short>(s_f);
+}
+
 __global__ void unpack_state_kernel(GridDesc g, const double* __restrict__ src, double* __restrict__ dst) {
     const long long n = 6ll * g.ny * g.nx;
     for (long long k = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; k < n;
@@ -1465,6 +1499,12 @@ __global__ void __launch_bounds__(256) mass_kernel(GridDesc g, const double* __r
 }
 cudaError_t launch_mass(const GridDesc& g, const double* s, double* part, int blocks, cudaStream_t st) {
     mass_kernel<<<blocks, 256, 0, st>>>(g, s, part);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_flag_scan(const GridDesc& g, const double* s, int ntx, int nty, unsigned short* flags,
+                             cudaStream_t st) {
+    flag_scan_kernel<<<ntx * nty, NT, 0, st>>>(g, s, ntx, flags);
     return cudaGetLastError();
 }
 
