@@ -139,6 +139,8 @@ struct tp_ctx {
     long long timed_tiles[2] = {0, 0};  // tiles processed per stage over the last tp_steps_timed
     double* dTallyP = nullptr;
     double* dTallyC = nullptr;
+    unsigned* dStampP = nullptr;  // ring-tally stamps (DevScalars::tally_epoch)
+    unsigned* dStampC = nullptr;
     signed char* dSide = nullptr;
     unsigned char* dInflowTiles = nullptr;  // per tile: its radius-2 box reads an inflow ghost
     double* dSamples = nullptr;
@@ -295,6 +297,7 @@ tpb::StageArgs stage_args(tp_ctx* c, bool corr, int loop) {
     a.geo = c->dGeo;
     a.sc = c->dSc;
     a.tally = corr ? c->dTallyC : c->dTallyP;
+    a.tally_stamp = corr ? c->dStampC : c->dStampP;
     a.ntx = c->ntx;
     a.nty = c->nty;
     a.loop = loop;
@@ -328,7 +331,6 @@ tpb::TileArgs tile_args(tp_ctx* c, const tpb::StageArgs& a, bool corr) {
     t.ntiles_active = c->dNact + (corr ? 1 : 0);
     t.ntiles_reset = c->dNact + (corr ? 0 : 1);
     t.work = c->dNact + 6 + (corr ? 1 : 0);
-    t.tally = a.tally;
     t.ntx = c->ntx;
     t.nty = c->nty;
     t.nxi = c->nx - 6;
@@ -406,6 +408,8 @@ void launch_post(tp_ctx* c, int loop) {
     a.sc = c->dSc;
     a.tally_pred = c->dTallyP;
     a.tally_corr = c->dTallyC;
+    a.stamp_pred = c->dStampP;
+    a.stamp_corr = c->dStampC;
     a.ntx = c->ntx;
     a.nty = c->nty;
     a.loop = loop;
@@ -719,10 +723,16 @@ void create_impl(tp_ctx* c, const tp_params* p, const tp_dem* dem, int row0, int
     c->dGeo = c->rawGeo + 1;
     cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device);
     ck(cudaMalloc(&c->dSc, sizeof(DevScalars)), "cudaMalloc scalars");
+    ck(cudaMemset(c->dSc, 0, sizeof(DevScalars)), "memset scalars");
     ck(cudaMalloc(&c->dClip, sizeof(tpb::ClipList)), "cudaMalloc clip list");
     const size_t tb = sizeof(double) * 4ull * c->ntx * c->nty;
     ck(cudaMalloc(&c->dTallyP, tb), "cudaMalloc tally");
     ck(cudaMalloc(&c->dTallyC, tb), "cudaMalloc tally");
+    const size_t sb = sizeof(unsigned) * static_cast<size_t>(c->ntx) * c->nty;
+    ck(cudaMalloc(&c->dStampP, sb), "cudaMalloc tally stamps");
+    ck(cudaMalloc(&c->dStampC, sb), "cudaMalloc tally stamps");
+    ck(cudaMemset(c->dStampP, 0, sb), "memset");
+    ck(cudaMemset(c->dStampC, 0, sb), "memset");
     ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
     c->own_stream = true;
     ck(cudaMemsetAsync(c->dClip, 0, sizeof(tpb::ClipList), c->stream), "memset");
@@ -857,6 +867,8 @@ void tp_destroy(tp_ctx* c) {
     cudaFree(c->dClip);
     cudaFree(c->dTallyP);
     cudaFree(c->dTallyC);
+    cudaFree(c->dStampP);
+    cudaFree(c->dStampC);
     cudaFree(c->dInflowTiles);
     cudaFree(c->dSide);
     cudaFree(c->dSamples);

@@ -360,6 +360,7 @@ __global__ void __launch_bounds__(NTH, NTH == NT ? 2 : 1) stage_kernel(const __g
     const int n_main = __ldcg(A.ntiles_active);
     const int e_first = __ldcg(A.tiles + blockIdx.x);
     const double dt = __ldcg(&sc->dt);
+    const unsigned epoch = __ldcg(&sc->tally_epoch);
     if (done0) return;
 
     const GridDesc& g = A.g;
@@ -402,11 +403,7 @@ __global__ void __launch_bounds__(NTH, NTH == NT ? 2 : 1) stage_kernel(const __g
             bool keep = false;
             if (ty == 0) keep |= !A.has_nbr[0] || A.halo_nz[0][tx] != 0u;
             if ((ty + 1) * TY + 1 >= A.nyi) keep |= !A.has_nbr[1] || A.halo_nz[1][tx] != 0u;
-            if (keep) return li;
-            if (tx == 0 || tx == A.ntx - 1 || ty == 0 || ty == A.nty - 1) {
-                double* t4 = A.tally + 4ll * (static_cast<long long>(ty) * A.ntx + tx);
-                t4[0] = t4[1] = t4[2] = t4[3] = 0.0;
-            }
+            if (keep) return li;  // (a dropped ring tile's tally slot keeps an old stamp)
             atomicAdd(&sc->cond_skips, 1ull);
             li = static_cast<int>(gridDim.x) + atomicAdd(A.work, 1);
         }
@@ -819,10 +816,13 @@ __global__ void __launch_bounds__(NTH, NTH == NT ? 2 : 1) stage_kernel(const __g
     }
 
     // ---- boundary mass tally of this stage (solver.cpp:352-376), ring tiles only
-    // (every ring tile writes its slot, zeros if no edge; out of line: a few tiles only)
-    if ((tix == 0 || tix == A.ntx - 1 || tiy == 0 || tiy == A.nty - 1) && threadIdx.x < 2)
+    // (every processed ring tile writes its slot, zeros if no edge, and stamps it with this
+    // step's epoch; out of line: a few tiles only)
+    if ((tix == 0 || tix == A.ntx - 1 || tiy == 0 || tiy == A.nty - 1) && threadIdx.x < 2) {
         ring_tally(FX, FY, X0, Y0, nx, ny, g.has_south, g.has_north, P.dxi, P.deta, dt,
                    A.tally + 4ll * tile, static_cast<int>(threadIdx.x));
+        if (threadIdx.x == 0) A.tally_stamp[tile] = 2u * epoch + (CORR ? 2u : 1u);
+    }
     // the tile's output flags: warp OR, one shared atomic per warp; the end-of-tile
     // barrier (FX/FY/V/PJ/BR/cell box are rewritten by the next tile) publishes them
     {
@@ -907,10 +907,6 @@ __device__ __forceinline__ void tiles_body(const TileArgs& a, int block) {
             if (xl && yr) u |= F[t + a.ntx - 1];
             if (xr && yr) u |= F[t + a.ntx + 1];
             safe = (u & TF_UNSAFE2) == 0u;
-        }
-        if (skip && ring) {
-#pragma unroll
-            for (int q = 0; q < 4; ++q) a.tally[4ll * t + q] = 0.0;
         }
     }
     // the other stage's counter was consumed by the stage before this one and is
@@ -1179,13 +1175,17 @@ __global__ void __launch_bounds__(kPostThreads) post_kernel(PostArgs a) {
     // before the clip fold's count is read (independent slots of the audit).
     __shared__ double red[kPostThreads / 32][8];
     const int nring = ring_tile_count(a.ntx, a.nty);
+    const unsigned epoch = sc->tally_epoch;
     double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
     for (int r = threadIdx.x; r < nring; r += kPostThreads) {
-        const long long o = 4ll * ring_tile(a.ntx, a.nty, r);
+        const int tile = ring_tile(a.ntx, a.nty, r);
+        const long long o = 4ll * tile;
+        // only the slots this step's stages wrote (a skipped tile's slot is a no-op: +0.0)
+        const bool wp = a.stamp_pred[tile] == 2u * epoch + 1u, wc = a.stamp_corr[tile] == 2u * epoch + 2u;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            acc[q] += a.tally_pred[o + q];
-            acc[4 + q] += a.tally_corr[o + q];
+            if (wp) acc[q] += a.tally_pred[o + q];
+            if (wc) acc[4 + q] += a.tally_corr[o + q];
         }
     }
 #pragma unroll
@@ -1207,6 +1207,7 @@ __global__ void __launch_bounds__(kPostThreads) post_kernel(PostArgs a) {
         }
     }
     if (threadIdx.x == 0) {
+        sc->tally_epoch = epoch + 1u;  // the next step's stamps
         // predictor then corrector, as the reference's two accumulate_boundary_fluxes calls
         for (int st = 0; st < 2; ++st) {
             sc->audit[2] += tot[4 * st + 0];  // solid injected

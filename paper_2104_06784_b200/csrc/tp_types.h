@@ -94,6 +94,10 @@ struct DevScalars {
     unsigned long long cond_skips;  // conditional tiles dropped by stage_kernel<PEER> (cumulative)
     ClipList* clip;               // regularize's clipped-mass events (see ClipList)
     int last_nact[2];             // tiles listed for the last predictor / corrector launch
+    // ring-tally epoch: a stage stamps each ring tile's tally slot it writes with
+    // 2 * epoch + 1 + stage; post folds the slots carrying this step's stamps, then advances it
+    // (monotonic: write_ctrl never resets it, so a slot from an earlier call never matches)
+    unsigned tally_epoch;
 };
 
 struct GridDesc {
@@ -134,7 +138,8 @@ struct StageArgs {
     double* out;                     // stage output state (interior written)
     const double* __restrict__ geo;  // 14 geometry fields
     DevScalars* sc;
-    double* tally;                   // per-tile boundary mass tally [ntiles][4]
+    double* tally;                   // per-tile boundary mass tally [ntiles][4] (ring tiles)
+    unsigned* tally_stamp;           // [ntiles]: 2 * epoch + 1 + stage of the slot's last write
     int ntx, nty;
     int loop;                        // 1 = obey sc->done (device-resident loop)
     int use_sc_dt;                   // read dt from sc (always 1 in practice)
@@ -182,7 +187,7 @@ constexpr int kMaxTileCols = 2048;  // halo_nz entries per side (wider slabs lis
 // buffer (the radius-2 box reads interior cells of the tile and the facing bands/corners
 // of its 8 neighbours only); flag_out: flags of its output buffer.  A tile whose box
 // and whose own output are all +0.0 bits is a bitwise no-op: it is left
-// off the list (its ring tally slot is zeroed here).  Flags are conservative: all bits
+// off the list (its ring tally slot keeps an old stamp, so post does not fold it).  Flags are conservative: all bits
 // set = unknown.
 struct TileArgs {
     const unsigned short* flag_in;
@@ -192,7 +197,6 @@ struct TileArgs {
                           // [4] past it: this stage's safe-tile count
     int* ntiles_reset;    // the other stage's counter
     int* work;            // this stage's dynamic tile scheduler counter (zeroed here)
-    double* tally;
     int ntx, nty;
     int nxi, nyi;         // interior columns / rows of this context (a tile's box may reach the ghost band
                           // or the halo rows without being an edge tile: a last tile of one column / row)
@@ -235,6 +239,8 @@ struct PostArgs {
     Inflow inflow;   // the next predictor's inflow-window test (DevScalars::inflow_safe)
     const double* tally_pred;
     const double* tally_corr;
+    const unsigned* stamp_pred;   // DevScalars::tally_epoch stamps of the two tallies
+    const unsigned* stamp_corr;
     int ntx, nty;
     int loop;
     int peered;   // slabs joined by tp_peer_connect*: a local error stops the loop through the
