@@ -33,6 +33,7 @@ cudaError_t launch_lambda(const GridDesc& g, const Phys& P, const double* s, con
                           DevScalars* sc, bool fastdiv, cudaStream_t st);
 cudaError_t launch_dt(const Phys& P, DevScalars* sc, int loop, cudaStream_t st);
 cudaError_t launch_post(const PostArgs& a, cudaStream_t st);
+cudaError_t launch_prepost(const PrePostArgs& a, cudaStream_t st);
 cudaError_t launch_regularize(const GridDesc& g, const Phys& P, double* s, const double* geo,
                               DevScalars* sc, bool fastdiv, cudaStream_t st);
 cudaError_t init_kernels();
@@ -182,6 +183,7 @@ struct tp_ctx {
     static constexpr int kMaxGraphLog = 13;  // graph_steps <= 4096 (tp_set_option)
     cudaGraphExec_t graphs[2][kMaxGraphLog] = {};
     double dt_hint = 0.0;               // the last step's dt: sizes the next replays (steps to the output)
+    bool merge_post = true;             // option "merge_post": post + the next pre in one launch
     cudaGraphExec_t graphT = nullptr;   // one step with timing events around the stage kernels
     int num_sms = 148;
     int wide_tiles = -1;                // use the wide graphs while the last lists had <= this many tiles (-1: #SMs)
@@ -298,6 +300,7 @@ tpb::StageArgs stage_args(tp_ctx* c, bool corr, int loop) {
     a.sc = c->dSc;
     a.tally = corr ? c->dTallyC : c->dTallyP;
     a.tally_stamp = corr ? c->dStampC : c->dStampP;
+    a.inflow = inflow_desc(c);  // corrector in the loop: the next predictor's inflow-window test
     a.ntx = c->ntx;
     a.nty = c->nty;
     a.loop = loop;
@@ -402,9 +405,8 @@ void launch_bc(tp_ctx* c, int buf, int tsrc, double t, int loop) {
     ck(tpb::launch_bc(b, c->stream), "bc_kernel");
 }
 
-void launch_post(tp_ctx* c, int loop) {
+tpb::PostArgs post_args(tp_ctx* c, int loop) {
     tpb::PostArgs a{};
-    a.inflow = inflow_desc(c);
     a.sc = c->dSc;
     a.tally_pred = c->dTallyP;
     a.tally_corr = c->dTallyC;
@@ -414,31 +416,70 @@ void launch_post(tp_ctx* c, int loop) {
     a.nty = c->nty;
     a.loop = loop;
     a.peered = c->peered ? 1 : 0;
-    ck(tpb::launch_post(a, c->stream), "post_kernel");
+    return a;
 }
+
+void launch_post(tp_ctx* c, int loop) { ck(tpb::launch_post(post_args(c, loop), c->stream), "post_kernel"); }
 
 // one whole step of the device loop: 5 kernels
 //   pre(bc(u,t) + predictor list + compute_dt) -> predictor -> pre(bc(u*,t+dt) + corrector list)
 //   -> corrector -> post(t += dt, audit, stop flag)
+// the loop's bc of a stage's input buffer (apply_boundaries, solver.cpp:639 / :523)
+tpb::BcArgs loop_bc(tp_ctx* c, int corr) {
+    tpb::BcArgs b{};
+    b.g = c->g;
+    b.s = corr ? c->dB : c->dA;
+    b.geo = c->dGeo;
+    b.inflow = inflow_desc(c);
+    b.sc = c->dSc;
+    b.t = 0.0;
+    b.tsrc = corr ? 2 : 1;
+    b.loop = 1;
+    return b;
+}
+
+// bc + the stage's list (+ compute_dt before the predictor): pre_kernel
+void launch_loop_pre(tp_ctx* c, const tpb::StageArgs& sa, int corr) {
+    tpb::PreArgs p{};
+    p.bc = loop_bc(c, corr);
+    p.t = tile_args(c, sa, corr != 0);
+    p.P = c->ph;
+    p.nb_bc = tpb::bc_blocks(c->g);
+    p.with_dt = corr ? 0 : 1;
+    ck(tpb::launch_pre(p, c->stream), corr ? "pre (corrector)" : "pre (predictor)");
+}
+
+// the step graphs merge each step's post into the next step's pre (option "merge_post",
+// unpeered contexts): pre, then per step predictor, pre(corrector), corrector, and between
+// steps one prepost_kernel; a standalone post ends the replay.  4 launches per step + 1.
+bool merged_loop(const tp_ctx* c) { return c->merge_post && !c->peered; }
+
+void enqueue_merged_steps(tp_ctx* c, int k, bool wide) {
+    const tpb::StageArgs pa = stage_args(c, false, 1), ca = stage_args(c, true, 1);
+    tpb::PrePostArgs pp{};
+    pp.pre.bc = loop_bc(c, 0);
+    pp.pre.t = tile_args(c, pa, false);
+    pp.pre.P = c->ph;
+    pp.pre.nb_bc = tpb::bc_blocks(c->g);
+    pp.pre.with_dt = 1;
+    pp.post = post_args(c, 1);
+    for (int s = 0; s < k; ++s) {
+        if (s == 0) launch_loop_pre(c, pa, 0);
+        else ck(tpb::launch_prepost(pp, c->stream), "prepost");
+        ck(tpb::launch_stage(pa, c->fastdiv, false, false, wide, c->stream), "predictor");
+        launch_loop_pre(c, ca, 1);
+        ck(tpb::launch_stage(ca, c->fastdiv, true, false, wide, c->stream), "corrector");
+    }
+    launch_post(c, 1);
+    c->last_tiles_stage = 1;
+}
+
 void enqueue_loop_step(tp_ctx* c, cudaEvent_t* ev = nullptr, bool wide = false) {
     // slabs connected by tp_peer_connect*: the lambda + stop all-reduce before compute_dt
     if (c->peered) ck(tpb::launch_peer_lambda(c->link, c->dSc, c->stream), "peer lambda");
     for (int corr = 0; corr < 2; ++corr) {
         const tpb::StageArgs sa = stage_args(c, corr != 0, 1);
-        tpb::PreArgs p{};
-        p.bc.g = c->g;
-        p.bc.s = corr ? c->dB : c->dA;
-        p.bc.geo = c->dGeo;
-        p.bc.inflow = inflow_desc(c);
-        p.bc.sc = c->dSc;
-        p.bc.t = 0.0;
-        p.bc.tsrc = corr ? 2 : 1;
-        p.bc.loop = 1;
-        p.t = tile_args(c, sa, corr != 0);
-        p.P = c->ph;
-        p.nb_bc = tpb::bc_blocks(c->g);
-        p.with_dt = corr ? 0 : 1;
-        ck(tpb::launch_pre(p, c->stream), corr ? "pre (corrector)" : "pre (predictor)");
+        launch_loop_pre(c, sa, corr);
         c->last_tiles_stage = corr;
         // halo rows after apply_boundaries (solver.cpp:639, :523), straight into the
         // neighbours' buffers; the stage kernel waits for theirs before its halo tiles
@@ -457,7 +498,9 @@ cudaGraphExec_t capture_steps(tp_ctx* c, int k, cudaEvent_t* ev = nullptr, bool 
     c->last_tiles_stage = 1;  // a replay always follows a corrector (tp_steps resets otherwise)
     ck(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal), "begin capture");
     try {
-        for (int s = 0; s < k; ++s) enqueue_loop_step(c, ev, wide);
+        if (merged_loop(c) && !ev) enqueue_merged_steps(c, k, wide);
+        else
+            for (int s = 0; s < k; ++s) enqueue_loop_step(c, ev, wide);
     } catch (...) {
         cudaStreamEndCapture(c->stream, &graph);
         if (graph) cudaGraphDestroy(graph);
@@ -927,6 +970,11 @@ int tp_set_option(tp_ctx* c, const char* key, long value) {
             // wide stage CTAs while the last tile lists had <= value tiles (-1: the SM count;
             // 0: never; a large value: always)
             c->wide_tiles = static_cast<int>(value);
+        } else if (k == "merge_post") {
+            // 1: one launch for each step's post and the next step's pre (default); 0: five
+            // launches per step
+            c->merge_post = value != 0;
+            drop_graphs(c);
         } else if (k == "graph_steps") {
             if (value < 1 || value > 4096) throw ConfigErr{"graph_steps must be in [1, 4096]"};
             c->graph_steps = static_cast<int>(value);
@@ -1222,7 +1270,8 @@ void steps_launch(tp_ctx* c, StepsRun& r, long n) {
         const long k = 1L << l;
         while (n >= k && c->graphs[0][l]) {
             ck(cudaGraphLaunch(c->graphs[c->wide ? 1 : 0][l], c->stream), "graph launch");
-            c->launches += (c->peered ? 8L : 5L) * k;  // peered: + lambda exchange + 2 halo pushes
+            // merged: 4 per step + the final post; peered: + lambda exchange + 2 halo pushes
+            c->launches += merged_loop(c) ? 4L * k + 1L : (c->peered ? 8L : 5L) * k;
             r.launched += k;
             n -= k;
         }

@@ -326,6 +326,8 @@ __device__ __forceinline__ void stage_phase1(const double* __restrict__ S, const
     }
 }
 
+__device__ int inflow_window_ok(const Inflow& in, double t);  // below, with bc_body
+
 // ---------------------------------------------------------------------------
 // The fused stage kernel.
 // ---------------------------------------------------------------------------
@@ -362,6 +364,16 @@ __global__ void __launch_bounds__(NTH, NTH == NT ? 2 : 1) stage_kernel(const __g
     const double dt = __ldcg(&sc->dt);
     const unsigned epoch = __ldcg(&sc->tally_epoch);
     if (done0) return;
+    if (CORR && A.loop && blockIdx.x == 0 && threadIdx.x == 0) {
+        // the step's end as post will make it (solver.cpp:641-644), for prepost_kernel, and the
+        // next predictor's inflow-window test (its bc is at that time)
+        const double ta = sc->hit ? sc->t_next : sc->t + dt;
+        const long long sa = sc->steps + 1;
+        sc->t_after = ta;
+        sc->steps_after = sa;
+        sc->stop_after = (sc->hit || sa >= sc->max_steps || !(ta < sc->t_end)) ? 1 : 0;
+        sc->inflow_safe[0] = inflow_window_ok(A.inflow, ta);
+    }
 
     const GridDesc& g = A.g;
     const Phys& P = A.ph;
@@ -1166,18 +1178,17 @@ __device__ __forceinline__ int ring_tile(int ntx, int nty, int r) {
     return row * ntx + ((r & 1) ? ntx - 1 : 0);       // left/right columns
 }
 
-constexpr int kPostThreads = 1024;  // one pass over the ring tiles of grids up to ~4000 tiles wide
-__global__ void __launch_bounds__(kPostThreads) post_kernel(PostArgs a) {
+// post_kernel's work on one block of NTH threads: both stages' 4 tallies per ring tile
+// (per-thread sums, warp shuffles, then the warp partials reduced by warp 0 in warp order:
+// deterministic), the clip fold, the audit, and in the loop t, steps, lambda and the stop flag.
+// red: NTH/32 x 8 doubles of shared scratch.
+template <int NTH>
+__device__ __forceinline__ void post_work(const PostArgs& a, double (*red)[8]) {
     DevScalars* sc = a.sc;
-    if (a.loop && sc->done) return;
-    // both stages' 4 tallies per ring tile: per-thread sums, warp shuffles, then the warp
-    // partials reduced by warp 0 in warp order (deterministic).  The tally loads are issued
-    // before the clip fold's count is read (independent slots of the audit).
-    __shared__ double red[kPostThreads / 32][8];
     const int nring = ring_tile_count(a.ntx, a.nty);
     const unsigned epoch = sc->tally_epoch;
     double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-    for (int r = threadIdx.x; r < nring; r += kPostThreads) {
+    for (int r = threadIdx.x; r < nring; r += NTH) {
         const int tile = ring_tile(a.ntx, a.nty, r);
         const long long o = 4ll * tile;
         // only the slots this step's stages wrote (a skipped tile's slot is a no-op: +0.0)
@@ -1195,13 +1206,13 @@ __global__ void __launch_bounds__(kPostThreads) post_kernel(PostArgs a) {
     if ((threadIdx.x & 31) == 0)
 #pragma unroll
         for (int q = 0; q < 8; ++q) red[threadIdx.x >> 5][q] = acc[q];
-    clip_fold_block<kPostThreads>(sc);  // regularize's clipped mass of both stages, reference order
+    clip_fold_block<NTH>(sc);  // regularize's clipped mass of both stages, reference order
     __syncthreads();
     double tot[8];
     if (threadIdx.x < 32) {
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-            double v = red[threadIdx.x][q];
+            double v = threadIdx.x < NTH / 32 ? red[threadIdx.x][q] : 0.0;
             for (int d = 16; d > 0; d >>= 1) v += __shfl_down_sync(0xffffffffu, v, d);
             tot[q] = v;
         }
@@ -1225,10 +1236,48 @@ __global__ void __launch_bounds__(kPostThreads) post_kernel(PostArgs a) {
             // exchange, which stops every rank at the same step (a local stop here would leave
             // the other ranks waiting for this one)
             if ((!a.peered && sc->err_key != kNoError) || sc->hit || sc->steps >= sc->max_steps) sc->done = 1;
-            // the next predictor's inflow ghosts are bc at the new t (tsrc 1)
-            sc->inflow_safe[0] = inflow_window_ok(a.inflow, sc->t);
         }
     }
+}
+
+constexpr int kPostThreads = 1024;  // one pass over the ring tiles of grids up to ~4000 tiles wide
+__global__ void __launch_bounds__(kPostThreads) post_kernel(PostArgs a) {
+    if (a.loop && a.sc->done) return;
+    __shared__ double red[kPostThreads / 32][8];
+    post_work<kPostThreads>(a, red);
+}
+
+// One launch for post of the last step and pre of the next predictor (device loop of an
+// unpeered context; 4 launches per step instead of 5): the last block does post_kernel's work
+// and then compute_dt (pre_kernel's block-0 duty); every other block does the bc or list share
+// of pre_kernel.  Those blocks must not read t / steps / hit / dt (the last block rewrites
+// them): they take the step's end from DevScalars::t_after / stop_after, written by the
+// corrector at its start, and err_key (final: only stage kernels write it).  Slots post reads
+// (ring tallies by stamp, clip events) are not written by the list or bc work.
+__global__ void __launch_bounds__(NT) prepost_kernel(const __grid_constant__ PrePostArgs a) {
+    DevScalars* sc = a.post.sc;
+    if (__ldcg(&sc->done)) return;  // stopped earlier (or the last block has just stopped it)
+    if (blockIdx.x == gridDim.x - 1) {
+        __shared__ double red[NT / 32][8];
+        post_work<NT>(a.post, red);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            // pre_kernel's stop test at the new step, then compute_dt of the next step
+            if (sc->done || !(sc->t < sc->t_end) || sc->steps >= sc->max_steps) {
+                sc->done = 1;
+            } else {
+                dt_body(a.pre.P, sc, 0);
+                sc->inflow_safe[1] = inflow_window_ok(a.pre.bc.inflow, sc->t + sc->dt);
+            }
+        }
+        return;
+    }
+    if (__ldcg(&sc->stop_after) || __ldcg(&sc->err_key) != kNoError) return;  // the loop stops
+    BcArgs bc = a.pre.bc;
+    bc.t = __ldcg(&sc->t_after);
+    bc.tsrc = 0;
+    if (static_cast<int>(blockIdx.x) < a.pre.nb_bc) bc_body(bc, blockIdx.x);
+    else tiles_body(a.pre.t, blockIdx.x - a.pre.nb_bc);
 }
 
 // Fold of the standalone regularize's clip events (one block).
@@ -1337,6 +1386,12 @@ cudaError_t launch_lambda(const GridDesc& g, const Phys& P, const double* s, con
 
 cudaError_t launch_dt(const Phys& P, DevScalars* sc, int loop, cudaStream_t st) {
     dt_kernel<<<1, 1, 0, st>>>(P, sc, loop);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_prepost(const PrePostArgs& a, cudaStream_t st) {
+    const int n = a.pre.t.ntx * a.pre.t.nty;
+    prepost_kernel<<<a.pre.nb_bc + (n + NT - 1) / NT + 1, NT, 0, st>>>(a);
     return cudaGetLastError();
 }
 
@@ -1542,6 +1597,7 @@ cudaError_t init_kernels() {
         reinterpret_cast<const void*>(&bc_kernel), reinterpret_cast<const void*>(&ghost_copy_kernel),
         reinterpret_cast<const void*>(&lambda_kernel<true>), reinterpret_cast<const void*>(&lambda_kernel<false>),
         reinterpret_cast<const void*>(&dt_kernel), reinterpret_cast<const void*>(&post_kernel),
+        reinterpret_cast<const void*>(&prepost_kernel),
         reinterpret_cast<const void*>(&tiles_kernel), reinterpret_cast<const void*>(&pre_kernel),
         reinterpret_cast<const void*>(&regularize_kernel<true>),
         reinterpret_cast<const void*>(&regularize_kernel<false>),

@@ -98,6 +98,12 @@ struct DevScalars {
     // 2 * epoch + 1 + stage; post folds the slots carrying this step's stamps, then advances it
     // (monotonic: write_ctrl never resets it, so a slot from an earlier call never matches)
     unsigned tally_epoch;
+    // the step in flight as the corrector sees it at its start (device loop): the time and step
+    // count after it and whether the loop stops after it for any reason but an error; read by
+    // prepost_kernel's pre blocks, which must not read t / steps / hit (its post block rewrites them)
+    double t_after;
+    long long steps_after;
+    int stop_after;
 };
 
 struct GridDesc {
@@ -162,6 +168,7 @@ struct StageArgs {
     int nyi;                                // interior rows of this slab
     int peer_phase;                         // 1 + buffer: the stage's sequence-number phase (tp_peer.cu)
     unsigned long long timeout_ns;
+    Inflow inflow;                          // corrector (device loop): the next predictor's inflow-window test
 };
 
 // Per-tile output flags: which regions of the tile's interior hold a value with a nonzero
@@ -236,7 +243,6 @@ struct PreArgs {
 
 struct PostArgs {
     DevScalars* sc;
-    Inflow inflow;   // the next predictor's inflow-window test (DevScalars::inflow_safe)
     const double* tally_pred;
     const double* tally_corr;
     const unsigned* stamp_pred;   // DevScalars::tally_epoch stamps of the two tallies
@@ -246,6 +252,14 @@ struct PostArgs {
     int peered;   // slabs joined by tp_peer_connect*: a local error stops the loop through the
                   // next step's stop-flag exchange (peer_lambda_kernel), on every rank at once
 };
+
+// post of one step + pre of the next predictor in one launch (device loop, unpeered): the last
+// block runs post_kernel's work and compute_dt, the others bc + the predictor's list
+struct PrePostArgs {
+    PreArgs pre;
+    PostArgs post;
+};
+
 
 // ---- device-resident row-slab exchange (tp_peer.cu) ----------------------------
 constexpr int kMaxRanks = 16;
