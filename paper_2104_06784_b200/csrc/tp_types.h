@@ -124,7 +124,10 @@ struct Inflow {
 // Stage kernel tile: TX x TY interior cells, NT threads.  TX*TY*2 + TX + TY = 511
 // faces <= 2 * NT, so the face work of a tile is exactly two rounds.
 constexpr int TX = 16;
-constexpr int TY = 15;
+#ifndef TP_TY
+#define TP_TY 15
+#endif
+constexpr int TY = TP_TY;
 constexpr int NT = 256;
 constexpr int W2 = TX + 4;
 constexpr int H2 = TY + 4;
