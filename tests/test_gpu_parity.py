@@ -120,6 +120,32 @@ def test_trajectory_output_hits(gpu, oracle_kind):
     assert_bitwise(sim.state(), ref.state(), "state at output times")
 
 
+@pytest.mark.parametrize("opts", [{"merge_post": 0}, {"graph_steps": 1}, {"graph_steps": 3},
+                                  {"graph_steps": 64}, {"merge_post": 0, "graph_steps": 5}])
+def test_loop_structure_options_bitwise(gpu, oracle_kind, opts):
+    """The device loop's structure is not semantics: post merged into the next pre or not
+    (prepost_kernel), and replay batches of any length (power-of-two graphs sized to the next
+    output), give the reference's dt sequence and state bit for bit along an output schedule
+    with hits, a Mode-II inflow and a run past the hydrograph."""
+    sc = scenarios.four_side_inflow(48, 40)
+    ref, sim = _pair(sc, oracle_kind)
+    for k, v in opts.items():
+        sim.set_option(k, v)
+    tu = sc.config.scaling.t_unit()
+    t_r = t_g = 0.0
+    t_end = sc.config.t_end / tu
+    for k in range(1, 41):
+        t_next = min(k * sc.config.dt_out / tu, t_end)
+        t_r, dts_r, _ = ref.steps(t_r, t_next, 100_000, t_end=t_end)
+        t_g, dts_g, _ = sim.steps(t_g, t_next, 100_000, t_end=t_end, record_dts=True)
+        assert_bitwise(dts_g, dts_r, f"dts interval {k} {opts}")
+        assert t_r == t_g
+        if opts.get("merge_post", 1) == 0:  # five launches per step (and per no-op step)
+            assert sim.kernel_launches() >= 5 * len(dts_g)
+    assert_bitwise(sim.state(), ref.state(), f"state {opts}")
+    np.testing.assert_allclose(sim.audit_array(), ref.audit(), rtol=1e-12, atol=1e-300)
+
+
 @pytest.mark.parametrize("wide", [False, True])
 def test_mode2_channel_inflow(gpu, oracle_kind, wide):
     """Mode-II hydrograph inflow (solver.cpp:108-136, hydrograph.hpp:31-45)."""
