@@ -49,8 +49,8 @@ cudaError_t launch_peer_lambda(const PeerLink& L, DevScalars* sc, cudaStream_t s
 cudaError_t launch_peer_halo(const PeerLink& L, const GridDesc& g, const double* s, int buf, DevScalars* sc,
                              cudaStream_t st);
 cudaError_t launch_pack_state(const GridDesc& g, const double* src, double* dst, bool unpack, cudaStream_t st);
-cudaError_t launch_flag_scan(const GridDesc& g, const double* s, int ntx, int nty, unsigned short* flags,
-                             cudaStream_t st);
+cudaError_t launch_flag_scan(const GridDesc& g, const Phys& P, const double* s, const double* geo, int ntx,
+                             int nty, unsigned short* flags, DevScalars* sc, bool fastdiv, cudaStream_t st);
 cudaError_t launch_mass(const GridDesc& g, const double* s, double* part, int blocks, cudaStream_t st);
 cudaError_t launch_snapshot(const GridDesc& g, const double* s, const double* geo, double* out, int ncols,
                             int nrows, double H, double h_dry, double eps_h, double vu, cudaStream_t st);
@@ -387,9 +387,16 @@ void invalidate_flags(tp_ctx* c, bool a_buf, bool b_buf) {
 
 // Exact flags of buffer A after a write outside the stage kernels (flag_scan_kernel): the next
 // stage lists only the tiles that can change instead of every tile (after tp_set_state the
-// first step used to process the whole grid twice).
+// first step used to process the whole grid twice).  The same pass computes compute_dt's
+// lambda of A (what fresh_lambda would), so lam_valid holds afterwards.
 void scan_flags_A(tp_ctx* c) {
-    ck(tpb::launch_flag_scan(c->g, c->dA, c->ntx, c->nty, c->dFlagA, c->stream), "flag scan");
+    ck(cudaMemsetAsync(&c->dSc->lam_bits, 0, sizeof(unsigned long long), c->stream), "memset");
+    ck(tpb::launch_flag_scan(c->g, c->ph, c->dA, c->dGeo, c->ntx, c->nty, c->dFlagA, c->dSc, c->fastdiv, c->stream),
+       "flag scan");
+    ck(cudaMemcpyAsync(&c->dSc->lam_cur, &c->dSc->lam_bits, sizeof(unsigned long long), cudaMemcpyDeviceToDevice,
+                       c->stream),
+       "lam copy");
+    c->lam_valid = true;
 }
 
 void launch_bc(tp_ctx* c, int buf, int tsrc, double t, int loop) {
@@ -1005,7 +1012,6 @@ int tp_set_initial_thickness(tp_ctx* c, const double* h_m) {
            "init_thickness_kernel");
         scan_flags_A(c);
         ck(cudaStreamSynchronize(c->stream), "sync");
-        c->lam_valid = false;
         c->ghosts_in_B = false;
     })
 }
@@ -1024,7 +1030,6 @@ int tp_set_initial_velocity(tp_ctx* c, const double* vx, const double* vy) {
            "init_velocity_kernel");
         scan_flags_A(c);
         ck(cudaStreamSynchronize(c->stream), "sync");
-        c->lam_valid = false;
         c->ghosts_in_B = false;
     })
 }
@@ -1132,7 +1137,6 @@ int tp_set_state(tp_ctx* c, const double* in) {
         upload_state(c, c->dA, in);
         scan_flags_A(c);
         ck(cudaStreamSynchronize(c->stream), "sync");
-        c->lam_valid = false;
         c->ghosts_in_B = false;
     })
 }
@@ -1182,7 +1186,6 @@ int tp_regularize(tp_ctx* c) {
         ck(tpb::launch_regularize(c->g, c->ph, c->dA, c->dGeo, c->dSc, c->fastdiv, c->stream),
            "regularize_kernel");
         scan_flags_A(c);
-        c->lam_valid = false;
         check_error(c, c->dA);
     })
 }

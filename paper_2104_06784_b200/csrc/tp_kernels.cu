@@ -1088,14 +1088,12 @@ __global__ void ghost_copy_kernel(GridDesc g, const double* __restrict__ src, do
 // ---------------------------------------------------------------------------
 // compute_dt lambda loop (solver.cpp:556-573) + exact reduce_max.
 // ---------------------------------------------------------------------------
+// lambda of one interior cell at offset o (solver.cpp:560-571, physics.hpp:178-189)
 template <bool FD>
-__global__ void __launch_bounds__(NT) lambda_kernel(GridDesc g, Phys P, const double* __restrict__ s,
-                                                    const double* __restrict__ geo, DevScalars* sc) {
-    const int X = 3 + blockIdx.x * 32 + (threadIdx.x & 31);
-    const int Y = 3 + blockIdx.y * (NT / 32) + (threadIdx.x >> 5);
+__device__ __forceinline__ double cell_lambda(const GridDesc& g, const Phys& P, const double* __restrict__ s,
+                                              const double* __restrict__ geo, long long o) {
     double lam = 0.0;
-    if (X <= g.nx - 4 && Y <= g.ny - 4) {
-        const long long o = static_cast<long long>(Y) * g.pitch + X;
+    {
         const double jb = __ldg(geo + G_JB * g.fs + o);
         const Rcp rj = mkrcp<FD>(jb);
         const double hs = dv<FD>(s[0 * g.fs + o], rj);
@@ -1114,6 +1112,16 @@ __global__ void __launch_bounds__(NT) lambda_kernel(GridDesc g, Phys P, const do
             lam = smax(lx, ly);
         }
     }
+    return lam;
+}
+
+template <bool FD>
+__global__ void __launch_bounds__(NT) lambda_kernel(GridDesc g, Phys P, const double* __restrict__ s,
+                                                    const double* __restrict__ geo, DevScalars* sc) {
+    const int X = 3 + blockIdx.x * 32 + (threadIdx.x & 31);
+    const int Y = 3 + blockIdx.y * (NT / 32) + (threadIdx.x >> 5);
+    double lam = 0.0;
+    if (X <= g.nx - 4 && Y <= g.ny - 4) lam = cell_lambda<FD>(g, P, s, geo, static_cast<long long>(Y) * g.pitch + X);
     lam_block_max(lam, sc);
 }
 
@@ -1431,8 +1439,13 @@ __global__ void pack_state_kernel(GridDesc g, const double* __restrict__ src, do
 // reduces over their outputs (cell_epilogue + the tile's flag OR), so the next stage lists only
 // the tiles that are not bitwise no-ops instead of every tile ("unknown" flags).  One block of
 // NT threads per tile, thread t = interior cell t.
-__global__ void __launch_bounds__(NT) flag_scan_kernel(GridDesc g, const double* __restrict__ s, int ntx,
-                                                       unsigned short* __restrict__ flags) {
+// FD: also compute_dt's lambda over the tile (cell_lambda, as lambda_kernel; cells whose six
+// values are all +0.0 bits contribute 0 without the arithmetic), so the state needs no second
+// pass for it.
+template <bool FD>
+__global__ void __launch_bounds__(NT) flag_scan_kernel(GridDesc g, Phys P, const double* __restrict__ s,
+                                                       const double* __restrict__ geo, int ntx,
+                                                       unsigned short* __restrict__ flags, DevScalars* sc) {
     __shared__ unsigned s_f;
     const int tile = blockIdx.x;
     const int tix = tile % ntx, tiy = tile / ntx;
@@ -1441,6 +1454,7 @@ __global__ void __launch_bounds__(NT) flag_scan_kernel(GridDesc g, const double*
     if (threadIdx.x == 0) s_f = 0u;
     __syncthreads();
     unsigned fb = 0u;
+    double lam = 0.0;
     if (threadIdx.x < TX * TY && X <= g.nx - 4 && Y <= g.ny - 4) {
         const long long o = static_cast<long long>(Y) * g.pitch + X;
         unsigned long long bits = 0ull;
@@ -1453,10 +1467,11 @@ __global__ void __launch_bounds__(NT) flag_scan_kernel(GridDesc g, const double*
         }
         inwin2 = inwin2 && __double2hiint(s[o]) >= 0 && __double2hiint(s[g.fs + o]) >= 0;
         fb = (bits != 0ull ? cell_flag_bits(cx, cy) : 0u) | (inwin2 ? 0u : static_cast<unsigned>(TF_UNSAFE2));
+        if (bits != 0ull) lam = cell_lambda<FD>(g, P, s, geo, o);
     }
     const unsigned wf = __reduce_or_sync(0xffffffffu, fb);
     if ((threadIdx.x & 31) == 0 && wf) atomicOr(&s_f, wf);
-    __syncthreads();
+    lam_block_max(lam, sc);  // (its barrier also publishes s_f)
     if (threadIdx.x == 0) flags[tile] = static_cast<unsigned short>(s_f);
 }
 
@@ -1558,9 +1573,10 @@ cudaError_t launch_mass(const GridDesc& g, const double* s, double* part, int bl
     return cudaGetLastError();
 }
 
-cudaError_t launch_flag_scan(const GridDesc& g, const double* s, int ntx, int nty, unsigned short* flags,
-                             cudaStream_t st) {
-    flag_scan_kernel<<<ntx * nty, NT, 0, st>>>(g, s, ntx, flags);
+cudaError_t launch_flag_scan(const GridDesc& g, const Phys& P, const double* s, const double* geo, int ntx,
+                             int nty, unsigned short* flags, DevScalars* sc, bool fastdiv, cudaStream_t st) {
+    if (fastdiv) flag_scan_kernel<true><<<ntx * nty, NT, 0, st>>>(g, P, s, geo, ntx, flags, sc);
+    else flag_scan_kernel<false><<<ntx * nty, NT, 0, st>>>(g, P, s, geo, ntx, flags, sc);
     return cudaGetLastError();
 }
 
