@@ -338,6 +338,10 @@ def run_b200(args):
         torch.cuda.empty_cache()
         # the north-star grid (BASELINE.json configs[4]): C5 8192^2, N=1
         extra["c5_8192"] = c5_leg(args, peak)
+        # the latency-bound sparse steps (the per-step floor): BASELINE.json
+        # configs[2] (C3 Mode-II channel) and configs[0] (C1 hill), along their output schedules
+        extra["sparse_steps"] = {"c3_4096x2048": sparse_leg("c3", 4096, 2048, 400, args),
+                                 "c1_256": sparse_leg("c1", 256, 256, 500, args)}
 
     cpu = None
     if not args.no_cpu:
@@ -422,6 +426,27 @@ def c5_leg(args, peak):
     if c5p and c5p.get("grid") == [sc.ncols, sc.nrows]:
         out["roofline"]["traffic"] = c5p["dram_bytes_per_step"]
         out["roofline"]["traffic_source"] = nt.get("source")
+    sim.close()
+    del sim
+    torch.cuda.empty_cache()
+    return out
+
+
+def sparse_leg(config, ncols, nrows, steps, args):
+    """ms per step of a latency-bound workload (a few dozen listed tiles per stage) along its
+    run's output schedule, after 10 untimed steps; CUDA events on the launching stream."""
+    import torch
+    sc = scenario_for(config, ncols, nrows)
+    sim, stream, _ = make_sim(sc, args.graph_steps)
+    clock = RunClock(sim)
+    clock.advance(10)
+    torch.cuda.synchronize()
+    ms = timed_steps(sim, clock, stream, steps)
+    act = sim.active_tiles()
+    out = {"ms_per_step": round(ms / steps, 5), "steps": steps,
+           "value": round(sc.ncols * sc.nrows * steps / (ms / 1e3) / 1e9, 4), "unit": "GCUPS",
+           "tiles_listed_last_step": [act[0], act[1]], "tiles": act[2],
+           "workload": workload_config(sc)["workload"]}
     sim.close()
     del sim
     torch.cuda.empty_cache()
