@@ -440,7 +440,9 @@ tpb::BcArgs loop_bc(tp_ctx* c, int corr) {
     b.inflow = inflow_desc(c);
     b.sc = c->dSc;
     b.t = 0.0;
-    b.tsrc = corr ? 2 : 1;
+    // corrector: Hydrograph::at(t + dt) as evaluated once after compute_dt (tsrc 3)
+    b.tsrc = corr ? 3 : 1;
+    b.stage = corr ? 1 : 0;
     b.loop = 1;
     return b;
 }

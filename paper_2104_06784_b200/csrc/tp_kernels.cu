@@ -326,7 +326,7 @@ __device__ __forceinline__ void stage_phase1(const double* __restrict__ S, const
     }
 }
 
-__device__ int inflow_window_ok(const Inflow& in, double t);  // below, with bc_body
+__device__ int inflow_stage_values(const Inflow& in, double t, double* val);  // below, with bc_body
 
 // ---------------------------------------------------------------------------
 // The fused stage kernel.
@@ -364,16 +364,6 @@ __global__ void __launch_bounds__(NTH, NTH == NT ? 2 : 1) stage_kernel(const __g
     const double dt = __ldcg(&sc->dt);
     const unsigned epoch = __ldcg(&sc->tally_epoch);
     if (done0) return;
-    if (CORR && A.loop && blockIdx.x == 0 && threadIdx.x == 0) {
-        // the step's end as post will make it (solver.cpp:641-644), for prepost_kernel, and the
-        // next predictor's inflow-window test (its bc is at that time)
-        const double ta = sc->hit ? sc->t_next : sc->t + dt;
-        const long long sa = sc->steps + 1;
-        sc->t_after = ta;
-        sc->steps_after = sa;
-        sc->stop_after = (sc->hit || sa >= sc->max_steps || !(ta < sc->t_end)) ? 1 : 0;
-        sc->inflow_safe[0] = inflow_window_ok(A.inflow, ta);
-    }
 
     const GridDesc& g = A.g;
     const Phys& P = A.ph;
@@ -856,6 +846,18 @@ __global__ void __launch_bounds__(NTH, NTH == NT ? 2 : 1) stage_kernel(const __g
     TPROBE_FLUSH(CORR ? 1 : 0)
 
     if (CORR) lam_block_max<NTH>(lam_local, sc);
+    if (CORR && A.loop && blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {
+        // for the next kernel (prepost_kernel): the step's end as post will make it
+        // (solver.cpp:641-644) and the next predictor's inflow values at that time (its bc) with
+        // their window test.  In the last CTA after its tiles (a sparse list leaves it idle):
+        // off every tile's critical path.
+        const double ta = sc->hit ? sc->t_next : sc->t + dt;
+        const long long sa = sc->steps + 1;
+        sc->t_after = ta;
+        sc->steps_after = sa;
+        sc->stop_after = (sc->hit || sa >= sc->max_steps || !(ta < sc->t_end)) ? 1 : 0;
+        sc->inflow_safe[0] = inflow_stage_values(A.inflow, ta, sc->inflow_val[0]);
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -996,16 +998,20 @@ __device__ void hydro_at(const Inflow& in, double t, double& h, double& phi, dou
     h = s[4 * (n - 1) + 1]; phi = s[4 * (n - 1) + 2]; speed = s[4 * (n - 1) + 3];
 }
 
-// The safe-tile window (DESIGN.md §3 item 6) over the Mode-II inflow ghosts bc_body writes at
-// time t (scaled): v = jb*hs, jb*hf, (jb*hs)*v_x, (jb*hs)*v_y, (jb*hf)*v_x, (jb*hf)*v_y with
+// Hydrograph::at at time t (scaled) into val (sh, sphi, sspeed: what bc_body's inflow threads
+// then read, BcArgs::tsrc 3), and the safe-tile window (DESIGN.md §3 item 6) over the Mode-II
+// inflow ghosts bc_body writes from them: v = jb*hs, jb*hf, (jb*hs)*v_x, (jb*hs)*v_y, (jb*hf)*v_x, (jb*hf)*v_y with
 // jb in [1, 2^50] (the geometry window of a context that uses safe tiles).  Sufficient:
 // thicknesses +0 or positive, each of hs, hf, hs*|speed|, hf*|speed| zero or in [2^-98, 2^48]
 // (a factor 2^2 of margin for the roundings of the products); then every ghost value is
 // +-0 or of magnitude in [2^-100, 2^100).  NaN / inf fail the comparisons.  One thread.
-__device__ int inflow_window_ok(const Inflow& in, double t) {
+__device__ int inflow_stage_values(const Inflow& in, double t, double* val) {
     if (!in.active) return 0;
     double sh, sphi, sspeed;
     hydro_at(in, t * in.t_unit, sh, sphi, sspeed);
+    val[0] = sh;
+    val[1] = sphi;
+    val[2] = sspeed;
     const double h = sh / in.H;
     const double speed = sspeed / in.v_unit;
     const double hs = h * sphi;
@@ -1037,12 +1043,18 @@ __device__ __forceinline__ void bc_body(const BcArgs& a, int block) {
     if (a.inflow.active) {
         const int side = a.inflow.ghost_side[idx];
         if (side) {
-            double t = a.t;
-            if (a.tsrc == 1) t = a.sc->t;
-            else if (a.tsrc == 2) t = a.sc->t + a.sc->dt;
-            const double t_seconds = t * a.inflow.t_unit;
             double sh, sphi, sspeed;
-            hydro_at(a.inflow, t_seconds, sh, sphi, sspeed);
+            if (a.tsrc == 3) {  // evaluated once by the previous kernel (inflow_stage_values)
+                const double* v = a.sc->inflow_val[a.stage];
+                sh = v[0];
+                sphi = v[1];
+                sspeed = v[2];
+            } else {
+                double t = a.t;
+                if (a.tsrc == 1) t = a.sc->t;
+                else if (a.tsrc == 2) t = a.sc->t + a.sc->dt;
+                hydro_at(a.inflow, t * a.inflow.t_unit, sh, sphi, sspeed);
+            }
             const double h = sh / a.inflow.H;
             const double speed = sspeed / a.inflow.v_unit;
             const double hs = h * sphi;
@@ -1161,7 +1173,7 @@ __global__ void __launch_bounds__(NT) pre_kernel(const __grid_constant__ PreArgs
     if (a.with_dt && blockIdx.x == 0 && threadIdx.x == 0) {
         dt_body(a.P, a.t.sc, 0);
         // the corrector's inflow ghosts are bc at t + dt (tsrc 2)
-        a.t.sc->inflow_safe[1] = inflow_window_ok(a.bc.inflow, a.t.sc->t + a.t.sc->dt);
+        a.t.sc->inflow_safe[1] = inflow_stage_values(a.bc.inflow, a.t.sc->t + a.t.sc->dt, a.t.sc->inflow_val[1]);
     }
     if (static_cast<int>(blockIdx.x) < a.nb_bc) bc_body(a.bc, blockIdx.x);
     else tiles_body(a.t, blockIdx.x - a.nb_bc);
@@ -1196,16 +1208,32 @@ __device__ __forceinline__ void post_work(const PostArgs& a, double (*red)[8]) {
     const int nring = ring_tile_count(a.ntx, a.nty);
     const unsigned epoch = sc->tally_epoch;
     double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-    for (int r = threadIdx.x; r < nring; r += NTH) {
-        const int tile = ring_tile(a.ntx, a.nty, r);
-        const long long o = 4ll * tile;
-        // only the slots this step's stages wrote (a skipped tile's slot is a no-op: +0.0)
-        const bool wp = a.stamp_pred[tile] == 2u * epoch + 1u, wc = a.stamp_corr[tile] == 2u * epoch + 2u;
+    // only the slots this step's stages wrote count (a skipped tile's slot is a no-op: +0.0).
+    // Slots and stamps are loaded together, two ring tiles per thread per round, and the
+    // stale ones selected away: tallies are +0 or positive, so adding +0.0 is exact.
+    for (int r0 = threadIdx.x; r0 < nring; r0 += 2 * NTH) {
+        double vp[2][4], vc[2][4];
+        bool wp[2], wc[2];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            if (wp) acc[q] += a.tally_pred[o + q];
-            if (wc) acc[4 + q] += a.tally_corr[o + q];
+        for (int u = 0; u < 2; ++u) {
+            const int r = r0 + u * NTH;
+            const int tile = ring_tile(a.ntx, a.nty, r < nring ? r : 0);
+            const long long o = 4ll * tile;
+            wp[u] = r < nring && a.stamp_pred[tile] == 2u * epoch + 1u;
+            wc[u] = r < nring && a.stamp_corr[tile] == 2u * epoch + 2u;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                vp[u][q] = a.tally_pred[o + q];
+                vc[u][q] = a.tally_corr[o + q];
+            }
         }
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                acc[q] += wp[u] ? vp[u][q] : 0.0;
+                acc[4 + q] += wc[u] ? vc[u][q] : 0.0;
+            }
     }
 #pragma unroll
     for (int q = 0; q < 8; ++q)
@@ -1275,15 +1303,15 @@ __global__ void __launch_bounds__(NT) prepost_kernel(const __grid_constant__ Pre
                 sc->done = 1;
             } else {
                 dt_body(a.pre.P, sc, 0);
-                sc->inflow_safe[1] = inflow_window_ok(a.pre.bc.inflow, sc->t + sc->dt);
+                sc->inflow_safe[1] = inflow_stage_values(a.pre.bc.inflow, sc->t + sc->dt, sc->inflow_val[1]);
             }
         }
         return;
     }
     if (__ldcg(&sc->stop_after) || __ldcg(&sc->err_key) != kNoError) return;  // the loop stops
     BcArgs bc = a.pre.bc;
-    bc.t = __ldcg(&sc->t_after);
-    bc.tsrc = 0;
+    bc.tsrc = 3;  // Hydrograph::at(t_after): evaluated by the corrector (inflow_val[0])
+    bc.stage = 0;
     if (static_cast<int>(blockIdx.x) < a.pre.nb_bc) bc_body(bc, blockIdx.x);
     else tiles_body(a.pre.t, blockIdx.x - a.pre.nb_bc);
 }

@@ -104,6 +104,10 @@ struct DevScalars {
     double t_after;
     long long steps_after;
     int stop_after;
+    // Hydrograph::at (sh, sphi, sspeed) at the [predictor, corrector] stage's bc time, evaluated
+    // once by the kernel before that stage's bc (corrector end / compute_dt) and read by every
+    // inflow ghost thread of the bc (BcArgs::tsrc 3) instead of each one scanning the samples
+    double inflow_val[2][3];
 };
 
 struct GridDesc {
@@ -231,7 +235,8 @@ struct BcArgs {
     Inflow inflow;
     DevScalars* sc;
     double t;       // used when tsrc == 0
-    int tsrc;       // 0: t argument, 1: sc->t, 2: sc->t + sc->dt
+    int tsrc;       // 0: t argument, 1: sc->t, 2: sc->t + sc->dt, 3: sc->inflow_val[stage]
+    int stage;      // tsrc 3: 0 predictor, 1 corrector
     int loop;
 };
 
