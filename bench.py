@@ -308,6 +308,18 @@ def run_b200(args):
                                 "dram_throughput_pct": prof["dram_throughput_pct"],
                                 "kernels": ["stage_kernel<pred>", "stage_kernel<corr>"],
                                 "source": nt.get("source")}
+        ir = nt.get("instruction_roofline")
+        if ir:
+            # the processed tiles against the instruction ceilings of the same code: the FP64
+            # pipe (64 thread ops per clock per SM) and issue (128 thread instructions per
+            # clock per SM) at the measured instruction counts per cell-update
+            rate = roofline["achieved"] * 1e9 / ALG_BYTES_PER_CELL_UPDATE / 1e9  # processed GCUPS
+            roofline["co_bound"].update({
+                "fp64_thread_ops_per_cell_update": ir["fp64_thread_ops_per_cell_update"],
+                "thread_instructions_per_cell_update": ir["thread_instructions_per_cell_update"],
+                "fp64_ceiling_gcups": ir["fp64_ceiling_gcups"], "issue_ceiling_gcups": ir["issue_ceiling_gcups"],
+                "processed_gcups": round(rate, 3),
+                "frac_of_issue_ceiling": round(rate / ir["issue_ceiling_gcups"], 4)})
 
     # e2e leg: through the C ABI with HOST (pinned) buffers, copies inside the timed region
     import ctypes as C

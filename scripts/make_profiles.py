@@ -76,8 +76,49 @@ if os.path.exists(lc):
     lines.append("|---|---|---|---|")
     for k, v in sorted(agg.items(), key=lambda x: -sum(x[1])):
         lines.append(f"| {k} | {len(v)} | {sum(v)/len(v)/1e3:.1f} | {100*sum(v)/tot:.1f}% |")
-open(f"{out_dir}/{tag}_ncu.md", "w").write("\n".join(lines) + "\n")
+# instruction ceilings from the fully wet capture (every tile processed: per cell-update counts
+# are exact): FP64-pipe thread instructions (DADD, DMUL, DFMA, DSETP) and all thread
+# instructions of both stage kernels, from the SASS source page
+iroof = None
+rep = f"gpurun_out/prof_{tag}_wet.ncu-rep"
+if os.path.exists(rep):
+    import re
+    txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+                         capture_output=True, text=True).stdout.split("\n")
+    blocks, cur = [], None
+    for ln in txt:
+        if ln.startswith('"Kernel Name"'):
+            cur = [ln]; blocks.append(cur)
+        elif cur is not None:
+            cur.append(ln)
+    fp64 = allt = 0
+    seen = set()
+    for b in blocks:
+        if b[0] in seen:
+            continue
+        seen.add(b[0])
+        rows = list(csv.reader(b[1:])); hdr = rows[0]
+        ti = hdr.index("Thread Instructions Executed")
+        for r in rows[1:]:
+            if len(r) != len(hdr):
+                continue
+            op = re.sub(r'^@!?U?P\w+\s+', '', r[1].strip()).split(' ')[0].split('.')[0]
+            allt += int(r[ti])
+            if op in ("DADD", "DMUL", "DFMA", "DSETP"):
+                fp64 += int(r[ti])
+    cells = GRID["wet"] ** 2
+    peaks = json.load(open("MEASURED_PEAKS.json")) if os.path.exists("MEASURED_PEAKS.json") else {}
+    clk = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
+    f_cu, t_cu = fp64 / cells, allt / cells
+    iroof = {"fp64_thread_ops_per_cell_update": round(f_cu, 1), "thread_instructions_per_cell_update": round(t_cu, 1),
+             "fp64_ceiling_gcups": round(148 * 64 * clk / f_cu / 1e9, 3),
+             "issue_ceiling_gcups": round(148 * 128 * clk / t_cu / 1e9, 3),
+             "how": "fully wet 2048^2 capture, both stage kernels; 64 FP64 and 128 thread instructions "
+                    "per clock per SM, 148 SMs, sm_max_mhz"}
+    lines.append(f"\n## Instruction ceilings (fully wet capture)\n\n{json.dumps(iroof)}\n")
 if "c2" in summary:
     d = summary["c2"]; d["wet"] = summary.get("wet"); d["c5"] = summary.get("c5"); d["source"] = f"profiles/{tag}_ncu.md"
+    d["instruction_roofline"] = iroof
     json.dump(d, open(f"{out_dir}/ncu_stage_summary.json", "w"), indent=1)
+open(f"{out_dir}/{tag}_ncu.md", "w").write("\n".join(lines) + "\n")
 print("\n".join(lines))
