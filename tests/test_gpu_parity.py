@@ -319,6 +319,28 @@ def test_safe_window_edges(gpu, oracle_kind):
     assert_bitwise(sim.state(), ref.state(), "state around out-of-window values")
 
 
+def test_set_state_exact_flags(gpu, oracle_kind):
+    """tp_set_state scans the new state's tile flags (flag_scan_kernel) instead of marking
+    every tile unknown: a state round-tripped through the host lists exactly the tiles the
+    uninterrupted run lists, and both runs stay bit-identical to the reference (dt, state)."""
+    from paper_2104_06784_b200.simulator import Simulator
+    sc = scenarios.c1_hill(160)
+    ref, sim = _pair(sc, oracle_kind)
+    other = Simulator.from_scenario(sc)
+    tr, dts_r, _ = ref.steps(0.0, 1.0e9, 40, t_end=1.0e9)
+    t1, _, _ = sim.steps(0.0, 1.0e9, 20, t_end=1.0e9)
+    t2, _, _ = other.steps(0.0, 1.0e9, 20, t_end=1.0e9)
+    other.set_state(other.state())  # host round trip: flags and lambda rebuilt from the state
+    t1, d1, _ = sim.steps(t1, 1.0e9, 1, t_end=1.0e9, record_dts=True)
+    t2, d2, _ = other.steps(t2, 1.0e9, 1, t_end=1.0e9, record_dts=True)
+    assert sim.active_tiles() == other.active_tiles()
+    assert_bitwise(d2, d1, "dt after the round trip")
+    sim.steps(t1, 1.0e9, 19, t_end=1.0e9)
+    other.steps(t2, 1.0e9, 19, t_end=1.0e9)
+    assert_bitwise(other.state(), ref.state(), "state after set_state")
+    assert_bitwise(sim.state(), ref.state(), "state")
+
+
 @pytest.mark.parametrize("make", [lambda: scenarios.c1_hill(96), lambda: scenarios.wet_valley(96, 80),
                                   lambda: scenarios.c3_channel(96, 48, t_end=30.0, dt_out=0.5)])
 def test_full_tile_list_bitwise(gpu, oracle_kind, make):
