@@ -16,7 +16,7 @@ sc = scenarios.c1_hill(n) if name == "c1" else scenarios.SCENARIOS[name](n, n //
 t0 = time.time()
 sim = Simulator.from_scenario(sc, fastdiv=bool(fastdiv))
 sim.set_option("graph_steps", gs)
-for kv in os.environ.get("QP_OPTS", "").split():  # e.g. QP_OPTS="device_loop=0 wide_tiles=0"
+for kv in os.environ.get("QP_OPTS", "").split():  # e.g. QP_OPTS="merge_post=0 wide_tiles=0"
     k, v = kv.split("=")
     sim.set_option(k, int(v))
 print(f"setup {time.time()-t0:.2f}s  grid {sc.ncols}x{sc.nrows} wet frac {np.mean(sc.h0 > 0) if sc.h0 is not None else 0:.3f}")
